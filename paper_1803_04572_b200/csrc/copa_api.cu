@@ -1,0 +1,472 @@
+// copa_api.cu — the C ABI (include/copa.h): validation, workspace layout, orchestration of one
+// outer iteration on one stream, and the allreduce hand-off points C1/C2.
+#include <cub/cub.cuh>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "copa_internal.cuh"
+
+using namespace copa;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+copa_status fail(copa_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+copa_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(COPA_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(call, where)                     \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(int64_t n) {
+    size_t o = off;
+    off = align_up(off + sizeof(T) * (size_t)(n > 0 ? n : 1));
+    return base ? reinterpret_cast<T*>(base + o) : nullptr;
+  }
+};
+
+// Segment layout shared by workspace_size (base = nullptr) and init.
+size_t carve(Handle& h, char* base) {
+  Carver c{base};
+  const int64_t R = h.R, RR = R * R;
+  h.err = c.take<int>(16);
+  h.scal = c.take<double>(S_COUNT);
+  h.H = c.take<double>(RR);
+  h.DH = c.take<double>(RR);
+  h.FH = c.take<double>(RR);
+  h.HtH = c.take<double>(RR);
+  h.VtV = c.take<double>(RR);
+  h.LW = c.take<double>(RR);
+  h.comm2 = c.take<double>(h.J * R + 2 * RR);
+  if (base) { h.FV = h.comm2; h.WtW = h.comm2 + h.J * R; h.M = h.WtW + RR; }
+  h.V = c.take<double>(h.J * R);
+  h.DV = c.take<double>(h.J * R);
+  h.W = c.take<double>(h.K * R);
+  h.DW = c.take<double>(h.K * R);
+  h.m = c.take<int32_t>(h.K);
+  h.rank = c.take<int32_t>(h.K);
+  h.srow = c.take<int64_t>(h.K + 1);
+  h.Pp = c.take<double>(h.S * R);
+  h.Qt = c.take<double>(h.S * R);
+  h.Nst = c.take<double>(h.S * R);
+  h.partial = c.take<double>((int64_t)kPartBlocks * RR);
+  h.host_fit = c.take<double>(1024);  // device ring of per-iteration FIT values
+  if (h.smooth) {
+    h.Bk = c.take<double>(h.K * h.l * h.l);
+    h.fiber_ptr = c.take<int64_t>(h.K + 1);
+    h.fiber_col = c.take<int32_t>(h.F);
+    h.fiber_val = c.take<double>(h.F * h.l);
+    h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
+  } else {
+    h.row_patient = c.take<int32_t>(h.rows);
+  }
+  return c.off;
+}
+
+copa_status check_args(const copa_problem* p, const copa_options* o) {
+  if (!p || !o) return fail(COPA_E_ARG, "null problem/options");
+  if (p->R < 1) return fail(COPA_E_ARG, "R must be >= 1");
+  if (p->R > kMaxR) return fail(COPA_E_UNSUPPORTED, "R > 64 not supported by this build");
+  if (p->J < 1 || p->J > kMaxJ) return fail(COPA_E_UNSUPPORTED, "J must be in [1, 65535]");
+  if (p->K_local < 0 || p->rows < 0 || p->nnz < 0) return fail(COPA_E_ARG, "negative size");
+  if (p->K_local > 0 && (!p->patient_row_ptr || !p->row_ptr)) return fail(COPA_E_ARG, "null CSR pointer");
+  if (p->nnz > 0 && (!p->col || !p->val)) return fail(COPA_E_ARG, "null col/val");
+  if (o->admm_inner < 1) return fail(COPA_E_ARG, "admm_inner must be >= 1");
+  const copa_constraint* cs[3] = {&o->on_H, &o->on_W, &o->on_V};
+  for (auto c : cs) {
+    if (c->kind < COPA_NONE || c->kind > COPA_L0) return fail(COPA_E_ARG, "unknown constraint kind");
+    if ((c->kind == COPA_L1 || c->kind == COPA_NONNEG_L1) && !(c->param >= 0)) return fail(COPA_E_ARG, "lambda < 0");
+    if (c->kind == COPA_L0 && !(c->param > 0)) return fail(COPA_E_ARG, "mu <= 0");
+  }
+  if (!(o->rank_tol >= 0) || !(o->basis_tol >= 0)) return fail(COPA_E_ARG, "tolerances must be >= 0");
+  if (o->smooth_l < 0) return fail(COPA_E_ARG, "smooth_l < 0");
+  if (o->smooth_l > 0) {
+    if (o->smooth_l > kMaxL) return fail(COPA_E_UNSUPPORTED, "smooth_l > 16 not supported");
+    if (o->smooth_degree < 0 || o->smooth_degree > kMaxDeg || o->smooth_degree >= o->smooth_l)
+      return fail(COPA_E_ARG, "smooth_degree must be in [0, min(7, l-1)]");
+    if (p->K_local > 0 && !p->visit_time) return fail(COPA_E_ARG, "smoothness requires visit times");
+    if (o->smooth_l * p->R > 32 * 16) return fail(COPA_E_UNSUPPORTED, "smooth_l * R > 512 not supported");
+  } else if (p->R > kMaxQ) {
+    // plain path: tall patients have q = R; this build's thread-per-patient polar needs q <= 16
+    return fail(COPA_E_UNSUPPORTED, "R > 16 without smoothness not supported by this build");
+  }
+  if (!o->H0 || !o->V0 || (p->K_local > 0 && !o->W0_local)) return fail(COPA_E_ARG, "null initial factors");
+  return COPA_OK;
+}
+
+void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
+  h.p = *p;
+  h.o = *o;
+  h.stream = (cudaStream_t)o->stream;
+  h.smooth = o->smooth_l > 0;
+  h.l = o->smooth_l;
+  h.d = o->smooth_degree;
+  h.K = p->K_local;
+  h.J = p->J;
+  h.rows = p->rows;
+  h.nnz = p->nnz;
+  h.R = p->R;
+  h.S = h.smooth ? h.K * h.l : h.rows;
+}
+
+copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
+  *F_out = 0;
+  *cub_bytes = 0;
+  if (!h.smooth) return COPA_OK;
+  size_t tb = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(h.K + 1));
+  *cub_bytes = tb;
+  if (h.K == 0) return COPA_OK;
+  int64_t* counts = nullptr;
+  void* tmp = nullptr;
+  CUDA_TRY(cudaMallocAsync(&counts, sizeof(int64_t) * (size_t)(h.K + 2), h.stream), "cudaMallocAsync(count)");
+  CUDA_TRY(cudaMallocAsync(&tmp, tb + 256, h.stream), "cudaMallocAsync(scan)");
+  launch_count_fibers(h, counts);
+  cub::DeviceScan::InclusiveSum(tmp, tb, counts, counts, (int)(h.K + 1), h.stream);
+  int64_t F = 0;
+  CUDA_TRY(cudaMemcpyAsync(&F, counts + h.K, sizeof(int64_t), cudaMemcpyDeviceToHost, h.stream), "count copy");
+  cudaFreeAsync(counts, h.stream);
+  cudaFreeAsync(tmp, h.stream);
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "count sync");
+  CUDA_TRY(cudaGetLastError(), "count kernels");
+  *F_out = F;
+  return COPA_OK;
+}
+
+copa_status allreduce(Handle& h, double* buf, int64_t n) {
+  if (!h.o.allreduce) return COPA_OK;
+  int rc = h.o.allreduce(buf, n, (void*)h.stream, h.o.allreduce_ctx);
+  if (rc != 0) return fail(COPA_E_COMM, "allreduce callback returned " + std::to_string(rc));
+  return COPA_OK;
+}
+
+copa_status check_err(Handle& h) {
+  int err = 0;
+  CUDA_TRY(cudaMemcpyAsync(&err, h.err, sizeof(int), cudaMemcpyDeviceToHost, h.stream), "err copy");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "stream sync");
+  CUDA_TRY(cudaGetLastError(), "kernel launch");
+  if (err & ERR_SHAPE) return fail(COPA_E_SHAPE, "invalid CSR/times (monotonicity, column range, duplicates)");
+  if (err & ERR_INPUT_NONFINITE) return fail(COPA_E_NONFINITE, "non-finite input value");
+  if (err & ERR_DEGEN) return fail(COPA_E_DEGENERATE, "trace(G) = 0 with automatic rho");
+  if (err & ERR_CHOL) return fail(COPA_E_CHOL, "non-positive pivot in chol(G + rho I)");
+  if (err & ERR_NONFINITE) return fail(COPA_E_NONFINITE, "non-finite FIT");
+  return COPA_OK;
+}
+
+__global__ void k_srow_smooth(int64_t K, int l, int64_t* srow) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k <= K) srow[k] = k * l;
+}
+
+__global__ void k_rank_deficient(const int32_t* m, const int32_t* rank, int64_t K, int R, unsigned long long* out) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  int q = m[k] < R ? m[k] : R;
+  if (rank[k] < q) atomicAdd(out, 1ull);
+}
+
+}  // namespace
+
+struct copa_handle {
+  Handle h;
+};
+
+extern "C" {
+
+void copa_get_limits(copa_limits* out) {
+  if (!out) return;
+  out->max_R = kMaxR;
+  out->max_q = kMaxQ;
+  out->max_smooth_l = kMaxL;
+  out->max_J = kMaxJ;
+}
+
+const char* copa_last_error(void) { return g_last_error.c_str(); }
+
+copa_status copa_workspace_size(const copa_problem* p, const copa_options* o, size_t* bytes) {
+  copa_status st = check_args(p, o);
+  if (st != COPA_OK) return st;
+  if (!bytes) return fail(COPA_E_ARG, "null bytes");
+  Handle h{};
+  fill_sizes(h, p, o);
+  st = count_fibers(h, &h.F, &h.cub_temp_bytes);
+  if (st != COPA_OK) return st;
+  *bytes = carve(h, nullptr);
+  return COPA_OK;
+}
+
+copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out) {
+  copa_status st = check_args(p, o);
+  if (st != COPA_OK) return st;
+  if (!out || !ws) return fail(COPA_E_ARG, "null workspace/out");
+  if (((uintptr_t)ws & 255) != 0) return fail(COPA_E_WORKSPACE, "workspace must be 256-byte aligned");
+  copa_handle* H = new (std::nothrow) copa_handle();
+  if (!H) return fail(COPA_E_ARG, "out of host memory");
+  Handle& h = H->h;
+  fill_sizes(h, p, o);
+  st = count_fibers(h, &h.F, &h.cub_temp_bytes);
+  if (st != COPA_OK) { delete H; return st; }
+  size_t need = carve(h, nullptr);
+  if (bytes < need) { delete H; return fail(COPA_E_WORKSPACE, "workspace too small: need " + std::to_string(need)); }
+  carve(h, (char*)ws);
+  cudaStream_t s = h.stream;
+  const size_t RR = (size_t)h.R * h.R;
+  cudaMemsetAsync(h.err, 0, 16 * sizeof(int), s);
+  cudaMemsetAsync(h.scal, 0, S_COUNT * sizeof(double), s);
+  cudaMemsetAsync(h.Pp, 0, sizeof(double) * (size_t)(h.S * h.R), s);
+  cudaMemsetAsync(h.Qt, 0, sizeof(double) * (size_t)(h.S * h.R), s);
+  cudaMemsetAsync(h.Nst, 0, sizeof(double) * (size_t)(h.S * h.R), s);
+  cudaMemsetAsync(h.rank, 0, sizeof(int32_t) * (size_t)(h.K > 0 ? h.K : 1), s);
+  launch_validate(h);
+  st = check_err(h);
+  if (st != COPA_OK) { delete H; return st; }
+  if (h.smooth) {
+    if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
+    launch_count_fibers(h, h.fiber_ptr);
+    size_t tb = h.cub_temp_bytes;
+    if (h.K > 0) cub::DeviceScan::InclusiveSum(h.cub_temp, tb, h.fiber_ptr, h.fiber_ptr, (int)(h.K + 1), s);
+    launch_basis(h);
+    launch_build_fibers(h);
+  } else {
+    launch_row_patient(h);
+    if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);
+  }
+  cudaMemcpyAsync(h.H, o->H0, sizeof(double) * RR, cudaMemcpyDefault, s);
+  cudaMemcpyAsync(h.V, o->V0, sizeof(double) * (size_t)(h.J * h.R), cudaMemcpyDefault, s);
+  if (h.K > 0) cudaMemcpyAsync(h.W, o->W0_local, sizeof(double) * (size_t)(h.K * h.R), cudaMemcpyDefault, s);
+  cudaMemsetAsync(h.DH, 0, sizeof(double) * RR, s);
+  cudaMemsetAsync(h.DV, 0, sizeof(double) * (size_t)(h.J * h.R), s);
+  cudaMemsetAsync(h.DW, 0, sizeof(double) * (size_t)(h.K > 0 ? h.K * h.R : 1), s);
+  // normX, W^T W and V^T V of the initial factors (C0: normX and W^T W are summed over ranks)
+  launch_sumsq(h, h.scal + S_NORMX);
+  launch_gram(h, h.W, h.W, h.K, 0, h.WtW);
+  launch_gram(h, h.V, h.V, h.J, 0, h.VtV);
+  // C0 payload: [normX] and [WtW]
+  if (h.o.allreduce) {
+    st = allreduce(h, h.scal + S_NORMX, 1);
+    if (st == COPA_OK) st = allreduce(h, h.WtW, (int64_t)RR);
+    if (st != COPA_OK) { delete H; return st; }
+  }
+  st = check_err(h);
+  if (st != COPA_OK) { delete H; return st; }
+  *out = H;
+  return COPA_OK;
+}
+
+static copa_status iterate_once(Handle& h) {
+  copa_status st;
+  const int64_t RR = (int64_t)h.R * h.R;
+  launch_spmm(h);
+  launch_polar(h);
+  launch_fh(h);
+  if ((st = allreduce(h, h.FH, RR)) != COPA_OK) return st;  // C1
+  launch_admm_H(h);
+  launch_passB1(h);
+  launch_gram(h, h.W, h.W, h.K, 0, h.WtW);
+  launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M);
+  launch_scatter(h);
+  if ((st = allreduce(h, h.comm2, h.J * h.R + 2 * RR)) != COPA_OK) return st;  // C2
+  launch_admm_V(h);
+  launch_fit(h);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "iteration launch");
+  return COPA_OK;
+}
+
+copa_status copa_iterate(copa_handle* H, int32_t n_outer, double* fit_host) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  if (n_outer < 0) return fail(COPA_E_ARG, "n_outer < 0");
+  Handle& h = H->h;
+  int32_t done = 0;
+  while (done < n_outer) {
+    int32_t chunk = n_outer - done < 1024 ? n_outer - done : 1024;
+    for (int32_t t = 0; t < chunk; ++t) {
+      copa_status st = iterate_once(h);
+      if (st != COPA_OK) return st;
+      cudaMemcpyAsync(h.host_fit + t, h.scal + S_FIT, sizeof(double), cudaMemcpyDeviceToDevice, h.stream);
+      ++h.iterations;
+    }
+    if (fit_host)
+      CUDA_TRY(cudaMemcpyAsync(fit_host + done, h.host_fit, sizeof(double) * chunk, cudaMemcpyDefault, h.stream),
+               "fit copy");
+    copa_status st = check_err(h);
+    if (st != COPA_OK) return st;
+    done += chunk;
+  }
+  return COPA_OK;
+}
+
+copa_status copa_get_factors(copa_handle* H, double* Hout, double* Vout, double* Wout) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  Handle& h = H->h;
+  if (Hout) CUDA_TRY(cudaMemcpyAsync(Hout, h.H, sizeof(double) * h.R * h.R, cudaMemcpyDefault, h.stream), "get H");
+  if (Vout) CUDA_TRY(cudaMemcpyAsync(Vout, h.V, sizeof(double) * h.J * h.R, cudaMemcpyDefault, h.stream), "get V");
+  if (Wout && h.K > 0)
+    CUDA_TRY(cudaMemcpyAsync(Wout, h.W, sizeof(double) * h.K * h.R, cudaMemcpyDefault, h.stream), "get W");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "get sync");
+  return COPA_OK;
+}
+
+copa_status copa_get_duals(copa_handle* H, double* DH, double* DV, double* DW) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  Handle& h = H->h;
+  if (DH) CUDA_TRY(cudaMemcpyAsync(DH, h.DH, sizeof(double) * h.R * h.R, cudaMemcpyDefault, h.stream), "get DH");
+  if (DV) CUDA_TRY(cudaMemcpyAsync(DV, h.DV, sizeof(double) * h.J * h.R, cudaMemcpyDefault, h.stream), "get DV");
+  if (DW && h.K > 0)
+    CUDA_TRY(cudaMemcpyAsync(DW, h.DW, sizeof(double) * h.K * h.R, cudaMemcpyDefault, h.stream), "get DW");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "get sync");
+  return COPA_OK;
+}
+
+copa_status copa_get_U(copa_handle* H, double* U) {
+  if (!H || !U) return fail(COPA_E_ARG, "null handle/U");
+  Handle& h = H->h;
+  cudaPointerAttributes attr{};
+  cudaError_t e = cudaPointerGetAttributes(&attr, U);
+  if (e != cudaSuccess) cudaGetLastError();
+  if (e == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)) {
+    launch_U(h, U);
+  } else {
+    // host destination: stage through the state buffer N (overwritten; rebuilt by the next iteration)
+    if (h.rows > h.S) return fail(COPA_E_UNSUPPORTED, "host U needs a device buffer when rows > state rows");
+    launch_U(h, h.Nst);
+    CUDA_TRY(cudaMemcpyAsync(U, h.Nst, sizeof(double) * h.rows * h.R, cudaMemcpyDefault, h.stream), "get U");
+  }
+  return check_err(h);
+}
+
+copa_status copa_get_stats(copa_handle* H, copa_stats* out) {
+  if (!H || !out) return fail(COPA_E_ARG, "null handle/out");
+  Handle& h = H->h;
+  double sc[S_COUNT];
+  CUDA_TRY(cudaMemcpyAsync(sc, h.scal, sizeof(sc), cudaMemcpyDeviceToHost, h.stream), "stats copy");
+  unsigned long long* cnt = (unsigned long long*)(h.partial);
+  cudaMemsetAsync(cnt, 0, sizeof(*cnt), h.stream);
+  if (h.K > 0)
+    k_rank_deficient<<<(unsigned)((h.K + 255) / 256), 256, 0, h.stream>>>(h.m, h.rank, h.K, h.R, cnt);
+  unsigned long long rd = 0;
+  CUDA_TRY(cudaMemcpyAsync(&rd, cnt, sizeof(rd), cudaMemcpyDeviceToHost, h.stream), "stats copy");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "stats sync");
+  out->fit = sc[S_FIT];
+  out->rho[0] = sc[S_RHO_H];
+  out->rho[1] = sc[S_RHO_W];
+  out->rho[2] = sc[S_RHO_V];
+  out->normX = sc[S_NORMX];
+  out->iterations = h.iterations;
+  out->fibers = h.F;
+  out->state_rows = h.S;
+  out->rank_deficient = (int64_t)rd;
+  return COPA_OK;
+}
+
+copa_status copa_debug_state(copa_handle* H, double* Pp, double* Qt, int32_t* m, int64_t* srow, int32_t* rank) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  Handle& h = H->h;
+  size_t SR = sizeof(double) * (size_t)(h.S * h.R);
+  if (Pp) CUDA_TRY(cudaMemcpyAsync(Pp, h.Pp, SR, cudaMemcpyDefault, h.stream), "dbg Pp");
+  if (Qt) CUDA_TRY(cudaMemcpyAsync(Qt, h.Qt, SR, cudaMemcpyDefault, h.stream), "dbg Qt");
+  if (m && h.K) CUDA_TRY(cudaMemcpyAsync(m, h.m, sizeof(int32_t) * h.K, cudaMemcpyDefault, h.stream), "dbg m");
+  if (srow) CUDA_TRY(cudaMemcpyAsync(srow, h.srow, sizeof(int64_t) * (h.K + 1), cudaMemcpyDefault, h.stream), "dbg srow");
+  if (rank && h.K) CUDA_TRY(cudaMemcpyAsync(rank, h.rank, sizeof(int32_t) * h.K, cudaMemcpyDefault, h.stream), "dbg rank");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "dbg sync");
+  return COPA_OK;
+}
+
+void copa_destroy(copa_handle* H) { delete H; }
+
+// ---------------------------------------------------------------- end-to-end with host inputs
+static size_t input_bytes(const copa_problem* p) {
+  size_t b = 0;
+  b += align_up(sizeof(int64_t) * (size_t)(p->K_local + 1));
+  b += align_up(sizeof(int64_t) * (size_t)(p->rows + 1));
+  b += align_up(sizeof(int32_t) * (size_t)(p->nnz > 0 ? p->nnz : 1));
+  b += align_up(sizeof(double) * (size_t)(p->nnz > 0 ? p->nnz : 1));
+  b += align_up(sizeof(double) * (size_t)(p->rows > 0 ? p->rows : 1));
+  b += 3 * align_up(sizeof(double) * 1);  // placeholders
+  return b;
+}
+
+copa_status copa_fit_workspace_size(const copa_problem* p, const copa_options* o, size_t* bytes) {
+  copa_status st = check_args(p, o);
+  if (st != COPA_OK) return st;
+  if (!bytes) return fail(COPA_E_ARG, "null bytes");
+  Handle h{};
+  fill_sizes(h, p, o);
+  // upper bound on fibers from the host CSR: sum_k min(J, nnz_k)
+  int64_t F = 0;
+  if (h.smooth) {
+    for (int64_t k = 0; k < p->K_local; ++k) {
+      int64_t nk = p->row_ptr[p->patient_row_ptr[k + 1]] - p->row_ptr[p->patient_row_ptr[k]];
+      F += nk < p->J ? nk : p->J;
+    }
+    cub::DeviceScan::InclusiveSum(nullptr, h.cub_temp_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(h.K + 1));
+  }
+  h.F = F;
+  size_t need = carve(h, nullptr) + input_bytes(p) + align_up(sizeof(double) * ((size_t)p->J * p->R * 2 +
+                                                                               (size_t)p->R * p->R +
+                                                                               (size_t)p->K_local * p->R)) + 4096;
+  *bytes = need;
+  return COPA_OK;
+}
+
+copa_status copa_fit(const copa_problem* hp, const copa_options* ho, void* ws, size_t bytes, int32_t n_outer,
+                     double* fit_host, double* H_out, double* V_out, double* W_out) {
+  copa_status st = check_args(hp, ho);
+  if (st != COPA_OK) return st;
+  if (!ws || ((uintptr_t)ws & 255)) return fail(COPA_E_WORKSPACE, "workspace null or misaligned");
+  cudaStream_t s = (cudaStream_t)ho->stream;
+  Carver c{(char*)ws};
+  copa_problem dp = *hp;
+  int64_t* prp = c.take<int64_t>(hp->K_local + 1);
+  int64_t* rp = c.take<int64_t>(hp->rows + 1);
+  int32_t* col = c.take<int32_t>(hp->nnz);
+  double* val = c.take<double>(hp->nnz);
+  double* tim = c.take<double>(hp->rows);
+  double* H0 = c.take<double>((int64_t)hp->R * hp->R);
+  double* V0 = c.take<double>(hp->J * hp->R);
+  double* W0 = c.take<double>(hp->K_local * hp->R);
+  if (c.off > bytes) return fail(COPA_E_WORKSPACE, "workspace too small for the inputs");
+  CUDA_TRY(cudaMemcpyAsync(prp, hp->patient_row_ptr, sizeof(int64_t) * (hp->K_local + 1), cudaMemcpyDefault, s), "h2d");
+  CUDA_TRY(cudaMemcpyAsync(rp, hp->row_ptr, sizeof(int64_t) * (hp->rows + 1), cudaMemcpyDefault, s), "h2d");
+  if (hp->nnz > 0) {
+    CUDA_TRY(cudaMemcpyAsync(col, hp->col, sizeof(int32_t) * hp->nnz, cudaMemcpyDefault, s), "h2d");
+    CUDA_TRY(cudaMemcpyAsync(val, hp->val, sizeof(double) * hp->nnz, cudaMemcpyDefault, s), "h2d");
+  }
+  if (hp->visit_time && hp->rows > 0)
+    CUDA_TRY(cudaMemcpyAsync(tim, hp->visit_time, sizeof(double) * hp->rows, cudaMemcpyDefault, s), "h2d");
+  copa_options dopt = *ho;
+  CUDA_TRY(cudaMemcpyAsync(H0, ho->H0, sizeof(double) * hp->R * hp->R, cudaMemcpyDefault, s), "h2d");
+  CUDA_TRY(cudaMemcpyAsync(V0, ho->V0, sizeof(double) * hp->J * hp->R, cudaMemcpyDefault, s), "h2d");
+  if (hp->K_local > 0)
+    CUDA_TRY(cudaMemcpyAsync(W0, ho->W0_local, sizeof(double) * hp->K_local * hp->R, cudaMemcpyDefault, s), "h2d");
+  dopt.H0 = H0; dopt.V0 = V0; dopt.W0_local = W0;
+  dp.patient_row_ptr = prp; dp.row_ptr = rp; dp.col = col; dp.val = val;
+  dp.visit_time = hp->visit_time ? tim : nullptr;
+  copa_handle* h = nullptr;
+  st = copa_init(&dp, &dopt, (char*)ws + c.off, bytes - c.off, &h);
+  if (st != COPA_OK) return st;
+  st = copa_iterate(h, n_outer, fit_host);
+  if (st == COPA_OK) st = copa_get_factors(h, H_out, V_out, W_out);
+  copa_destroy(h);
+  return st;
+}
+
+}  // extern "C"

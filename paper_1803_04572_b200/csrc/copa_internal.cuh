@@ -1,0 +1,182 @@
+// copa_internal.cuh — internal types, device helpers and kernel launchers of libcopa.so.
+// Product path (CUDA, sm_100a, FP64). Shares no code with oracle/ (see DESIGN.md §1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/copa.h"
+
+namespace copa {
+
+constexpr int kMaxR = 64;       // rank limit (local arrays in the per-patient kernels)
+constexpr int kMaxQ = 16;       // q = min(m_k, R) limit of the thread-per-patient polar
+constexpr int kMaxL = 16;       // smooth_l limit
+constexpr int kMaxDeg = 7;      // spline degree limit
+constexpr int64_t kMaxJ = 65535;
+constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
+
+enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
+
+// Scalar slots in Handle::scal
+enum Scal : int { S_NORMX = 0, S_RHO_H, S_RHO_W, S_RHO_V, S_FIT, S_CROSS, S_QUAD, S_E, S_COUNT = 16 };
+
+struct Handle {
+  copa_problem p;      // device pointers of the CSR input
+  copa_options o;
+  cudaStream_t stream;
+  int smooth;          // smooth_l > 0
+  int l, d;            // basis size / degree (smooth)
+  int64_t K, J, rows, nnz;
+  int R;
+  int64_t S;           // state rows
+  int64_t F;           // fibers (smooth)
+  int64_t iterations;
+  // workspace segments (device)
+  int* err;
+  double* scal;
+  double *H, *DH, *FH, *HtH, *VtV, *LW, *partial;
+  double *comm2;       // [FV (J R) | WtW (R R) | M (R R)]
+  double *FV, *WtW, *M;
+  double *V, *DV;
+  double *W, *DW;
+  int32_t *m, *rank;
+  int64_t* srow;
+  double *Pp, *Qt, *Nst;
+  double* Bk;          // smooth: K x l x l basis coefficients (C_k = M_k B_k)
+  int64_t* fiber_ptr;  // smooth: [K+1]
+  int32_t* fiber_col;  // smooth: [F]
+  double* fiber_val;   // smooth: [F x l]
+  int32_t* row_patient;  // non-smooth: [rows]
+  void* cub_temp;
+  size_t cub_temp_bytes;
+  int64_t* counts_scratch;
+  double* host_fit;    // pinned staging for FIT
+  int own_inputs;      // copa_fit: CSR copied into the workspace
+};
+
+// ------------------------------------------------------------------ device helpers
+// Proximal maps (readings R-l1, R-l0, R-admm-sign). x = Z - D.
+__device__ __forceinline__ double prox(int kind, double param, double rho, double x) {
+  switch (kind) {
+    case COPA_NONNEG: return x > 0.0 ? x : 0.0;
+    case COPA_L1: {
+      double a = fabs(x) - param / rho;
+      return a > 0.0 ? copysign(a, x) : 0.0;
+    }
+    case COPA_NONNEG_L1: {
+      double a = x - param / rho;
+      return a > 0.0 ? a : 0.0;
+    }
+    case COPA_L0: return (x * x >= param) ? x : 0.0;
+    default: return x;
+  }
+}
+
+// Insert row a[0..q) into the upper-triangular Rf (q x q, row-major, stride ld) with Givens
+// rotations, so that Rf^T Rf accumulates a a^T without ever forming a Gram matrix.
+__device__ __forceinline__ void givens_insert(double* Rf, int ld, double* a, int q) {
+  for (int j = 0; j < q; ++j) {
+    double aj = a[j];
+    if (aj == 0.0) continue;
+    double r = Rf[j * ld + j];
+    double h = hypot(r, aj);
+    double c = r / h, s = aj / h;
+    Rf[j * ld + j] = h;
+    for (int t = j + 1; t < q; ++t) {
+      double x = Rf[j * ld + t], y = a[t];
+      Rf[j * ld + t] = c * x + s * y;
+      a[t] = c * y - s * x;
+    }
+  }
+}
+
+// One-sided (Hestenes) Jacobi on the q row-vectors of Wm (q x q, stride ld): rotates pairs of
+// rows until mutually orthogonal. Afterwards row j = sigma_j v_j where v_j are the right singular
+// vectors of the upper-triangular factor whose rows were given (polar kernel).
+__device__ __forceinline__ void jacobi_rows(double* Wm, int ld, int q) {
+  const double tol = 2.220446049250313e-16 * (double)q;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int p = 0; p < q - 1; ++p) {
+      for (int r = p + 1; r < q; ++r) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = 0; i < q; ++i) {
+          double x = Wm[p * ld + i], y = Wm[r * ld + i];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          c = fma(x, y, c);
+        }
+        if (a == 0.0 || b == 0.0) continue;
+        if (fabs(c) <= tol * sqrt(a * b)) continue;
+        rotated = 1;
+        double zeta = (b - a) / (2.0 * c);
+        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+        double cs = rsqrt(fma(t, t, 1.0));
+        double sn = cs * t;
+        for (int i = 0; i < q; ++i) {
+          double x = Wm[p * ld + i], y = Wm[r * ld + i];
+          Wm[p * ld + i] = cs * x - sn * y;
+          Wm[r * ld + i] = sn * x + cs * y;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+}
+
+// Uniform knot beta_idx of the gap-aware knot vector on [t1, tn] (reading R-spline-1).
+__device__ __forceinline__ double knot(double t1, double tn, int l, int d, int idx) {
+  if (idx <= d) return t1;
+  if (idx >= l) return tn;
+  int i = idx - d;
+  return t1 + (tn - t1) * (double)i / (double)(l - d);
+}
+
+// The d+1 non-zero B-spline values N[0..d] of basis functions mu-d..mu at t (de Boor triangle;
+// same functions as the paper's recursion P:358). Returns mu (the knot interval index).
+__device__ __forceinline__ int spline_eval(double t, double t1, double tn, int l, int d, double* N) {
+  int mu = d + (int)floor((t - t1) / (tn - t1) * (double)(l - d));
+  if (mu < d) mu = d;
+  if (mu > l - 1) mu = l - 1;
+  while (mu > d && t < knot(t1, tn, l, d, mu)) --mu;
+  while (mu < l - 1 && t >= knot(t1, tn, l, d, mu + 1)) ++mu;
+  double left[kMaxDeg + 1], right[kMaxDeg + 1];
+  N[0] = 1.0;
+  for (int j = 1; j <= d; ++j) {
+    left[j] = t - knot(t1, tn, l, d, mu + 1 - j);
+    right[j] = knot(t1, tn, l, d, mu + j) - t;
+    double saved = 0.0;
+    for (int r = 0; r < j; ++r) {
+      double tmp = N[r] / (right[r + 1] + left[j - r]);
+      N[r] = saved + right[r + 1] * tmp;
+      saved = left[j - r] * tmp;
+    }
+    N[j] = saved;
+  }
+  return mu;
+}
+
+__device__ __forceinline__ void set_err(int* err, int bit) { atomicOr(err, bit); }
+
+// ------------------------------------------------------------------ launchers
+// init
+void launch_validate(Handle& h);
+void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/);
+void launch_basis(Handle& h);
+void launch_build_fibers(Handle& h);
+void launch_row_patient(Handle& h);
+void launch_sumsq(Handle& h, double* out);
+// iteration
+void launch_spmm(Handle& h);
+void launch_polar(Handle& h);
+void launch_fh(Handle& h);
+void launch_admm_H(Handle& h);
+void launch_passB1(Handle& h);
+void launch_scatter(Handle& h);
+void launch_admm_V(Handle& h);
+void launch_fit(Handle& h);
+// reductions: C (R x R) = sum_s A(s,:)^T (B(s,:) * w(s,:)); wsrc: 0 none, 1 W rows by patient of s
+void launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
+void launch_U(Handle& h, double* U);
+
+}  // namespace copa

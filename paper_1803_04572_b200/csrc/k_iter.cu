@@ -1,0 +1,596 @@
+// k_iter.cu — kernels of one COPA outer iteration (Alg.1 l.3-l.20 + FIT), FP64, sm_100a.
+//
+// Pass A   spmm    P'_k = X'_k V̄                 (smooth: fibers of X'_k = C_k^T X_k; plain: CSR rows)
+//          polar   Q~_k = polar(P'_k S_k H̄^T)   (Givens QR of the tall side + one-sided Jacobi)
+//          fh      F_H = sum_k Q~_k^T P'_k S_k   (= Y_(1)(W ⊙ V), Y never formed)          -> C1
+// H-ADMM   admm_H  G_H, rho_H, chol, n_inner steps; then H̄^T H̄, G_W, rho_W, chol(G_W + rho_W I)
+// Pass B   passB1  F_W(k,:) = colsum((Q~_k H̄) ∘ P'_k) (= Y_(3)(V ⊙ H)), W-row ADMM, N_k = Q~_k H̄ S_k
+//          scatter F_V = sum_k X'_k^T N_k         (= Y_(2)(W ⊙ H))                        -> C2
+// V-ADMM   admm_V  G_V, rho_V, chol, n_inner steps per row of V̄
+// FIT      fit     E = normX - 2<F_V, V̄> + <sum_k N_k^T N_k, V̄^T V̄>
+#include "copa_internal.cuh"
+
+namespace copa {
+
+__device__ __forceinline__ int64_t patient_of(int64_t s, const int32_t* row_pat, int l) {
+  return row_pat ? (int64_t)row_pat[s] : s / l;
+}
+
+// ------------------------------------------------------------------ pass A: SpMM
+// Smooth: warp per patient; lane owns (a, r) pairs of P'_k (m_k x R); loops over the patient's fibers.
+constexpr int kSpmmU = 16;  // pairs per lane: m_k * R <= 512
+__global__ void k_spmm_fibers(const int64_t* fiber_ptr, const int32_t* fiber_col, const double* fiber_val,
+                              const int32_t* m, const int64_t* srow, int64_t K, int l, int R, const double* V,
+                              double* Pp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += nwarps) {
+    const int mk = m[k];
+    const int pairs = mk * R;
+    double acc[kSpmmU];
+#pragma unroll
+    for (int u = 0; u < kSpmmU; ++u) acc[u] = 0.0;
+    const int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
+    for (int64_t f = f0; f < f1; ++f) {
+      const int64_t j = fiber_col[f];
+      const double* xv = fiber_val + f * l;
+#pragma unroll
+      for (int u = 0; u < kSpmmU; ++u) {
+        int p = lane + 32 * u;
+        if (p < pairs) {
+          int a = p / R, r = p - a * R;
+          acc[u] = fma(xv[a], V[j * R + r], acc[u]);
+        }
+      }
+    }
+    double* out = Pp + srow[k] * R;
+#pragma unroll
+    for (int u = 0; u < kSpmmU; ++u) {
+      int p = lane + 32 * u;
+      if (p < pairs) out[p] = acc[u];
+    }
+  }
+}
+
+// Plain (no smoothness): P_k = X_k V̄, thread per (row, r).
+__global__ void k_spmm_rows(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int R,
+                            const double* V, double* Pp) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * R) return;
+  int64_t i = t / R;
+  int r = (int)(t - i * R);
+  double acc = 0.0;
+  for (int64_t e = rp[i]; e < rp[i + 1]; ++e) acc = fma(val[e], V[(int64_t)col[e] * R + r], acc);
+  Pp[t] = acc;
+}
+
+void launch_spmm(Handle& h) {
+  if (h.K == 0) return;
+  if (h.smooth) {
+    int64_t blocks = (h.K + 7) / 8;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_spmm_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow, h.K,
+                                                          h.l, h.R, h.V, h.Pp);
+  } else {
+    int64_t n = h.rows * h.R;
+    k_spmm_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R, h.V,
+                                                                   h.Pp);
+  }
+}
+
+// ------------------------------------------------------------------ pass A: polar (thread per patient)
+// A_k = P'_k S_k H̄^T (m x R). Tall (m >= R): Givens-QR of the rows of A into Rf (R x R).
+// Wide (m < R): Givens-QR of the rows of A^T (= columns of A) into Rf (m x m).
+// One-sided Jacobi on the rows of Rf -> rows sigma_j v_j, v_j right singular vectors of the
+// tall side T. K = sum_{sigma_j > tau sigma_max} v_j v_j^T / sigma_j  (= (T^T T)^{-1/2} on the range);
+// polar(T) = T K, so Q~ = A K (tall) or K A (wide): the partial isometry U_r V_r^T (reading R-polar-2).
+__global__ void __launch_bounds__(64) k_polar(const int32_t* m, const int64_t* srow, int64_t K, int R,
+                                              const double* Pp, const double* W, const double* Hg, double tau,
+                                              double* Qt, int32_t* rank) {
+  __shared__ double Hs[kMaxR * kMaxR];
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) Hs[i] = Hg[i];
+  __syncthreads();
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const int mk = m[k];
+  if (mk == 0) { rank[k] = 0; return; }
+  const double* P = Pp + srow[k] * R;
+  double* Q = Qt + srow[k] * R;
+  double w[kMaxR];
+  for (int r = 0; r < R; ++r) w[r] = W[k * R + r];
+  const int tall = mk >= R;
+  const int q = tall ? R : mk;
+  double Rf[kMaxQ * kMaxQ];
+  for (int i = 0; i < q * kMaxQ; ++i) Rf[i] = 0.0;
+  double a[kMaxR];
+  double A[kMaxQ * kMaxR];  // wide case only: A (mk x R)
+  if (tall) {
+    for (int i = 0; i < mk; ++i) {
+      double pw[kMaxR];
+      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
+      for (int s = 0; s < R; ++s) {
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
+        a[s] = acc;
+      }
+      givens_insert(Rf, kMaxQ, a, R);
+    }
+  } else {
+    for (int i = 0; i < mk; ++i) {
+      double pw[kMaxR];
+      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
+      for (int s = 0; s < R; ++s) {
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
+        A[i * R + s] = acc;
+      }
+    }
+    for (int s = 0; s < R; ++s) {
+      for (int i = 0; i < mk; ++i) a[i] = A[i * R + s];
+      givens_insert(Rf, kMaxQ, a, mk);
+    }
+  }
+  jacobi_rows(Rf, kMaxQ, q);
+  double sig[kMaxQ], smax = 0.0;
+  for (int j = 0; j < q; ++j) {
+    double s = 0.0;
+    for (int i = 0; i < q; ++i) s = fma(Rf[j * kMaxQ + i], Rf[j * kMaxQ + i], s);
+    sig[j] = sqrt(s);
+    smax = fmax(smax, sig[j]);
+  }
+  double Km[kMaxQ * kMaxQ];
+  for (int i = 0; i < q * q; ++i) Km[i] = 0.0;
+  int r_k = 0;
+  for (int j = 0; j < q; ++j) {
+    if (!(smax > 0.0) || !(sig[j] > tau * smax)) continue;
+    ++r_k;
+    double inv3 = 1.0 / (sig[j] * sig[j] * sig[j]);
+    for (int x = 0; x < q; ++x) {
+      double vx = Rf[j * kMaxQ + x] * inv3;
+      for (int y = 0; y < q; ++y) Km[x * q + y] = fma(vx, Rf[j * kMaxQ + y], Km[x * q + y]);
+    }
+  }
+  rank[k] = r_k;
+  if (tall) {
+    for (int i = 0; i < mk; ++i) {
+      double pw[kMaxR];
+      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
+      for (int s = 0; s < R; ++s) {
+        double acc = 0.0;
+        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
+        a[s] = acc;
+      }
+      for (int s = 0; s < R; ++s) {
+        double acc = 0.0;
+        for (int x = 0; x < R; ++x) acc = fma(a[x], Km[x * q + s], acc);
+        Q[(int64_t)i * R + s] = acc;
+      }
+    }
+  } else {
+    for (int i = 0; i < mk; ++i)
+      for (int s = 0; s < R; ++s) {
+        double acc = 0.0;
+        for (int x = 0; x < mk; ++x) acc = fma(Km[i * q + x], A[x * R + s], acc);
+        Q[(int64_t)i * R + s] = acc;
+      }
+  }
+}
+
+void launch_polar(Handle& h) {
+  if (h.K == 0) return;
+  k_polar<<<(unsigned)((h.K + 63) / 64), 64, 0, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol,
+                                                            h.Qt, h.rank);
+}
+
+// ------------------------------------------------------------------ R x R reductions
+// partial[b] = sum over block b's rows s of A(s,:)^T (B(s,:) * w(s,:)); then a fixed-order sum.
+constexpr int kGramRows = 32;
+__global__ void __launch_bounds__(256) k_gram(const double* A, const double* B, int64_t n, int R,
+                                              const double* Wrows, const int32_t* row_pat, int lstride,
+                                              double* partial) {
+  __shared__ double As[kGramRows * kMaxR];
+  __shared__ double Bs[kGramRows * kMaxR];
+  const int RR = R * R;
+  double acc[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+  int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  int64_t s0 = blockIdx.x * per, s1 = s0 + per;
+  if (s1 > n) s1 = n;
+  for (int64_t c0 = s0; c0 < s1; c0 += kGramRows) {
+    int nr = (int)((s1 - c0) < kGramRows ? (s1 - c0) : kGramRows);
+    for (int x = threadIdx.x; x < nr * R; x += blockDim.x) {
+      int rr = x / R, c = x - rr * R;
+      int64_t s = c0 + rr;
+      As[rr * R + c] = A[s * R + c];
+      double b = B[s * R + c];
+      if (Wrows) b *= Wrows[patient_of(s, row_pat, lstride) * R + c];
+      Bs[rr * R + c] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      int p = threadIdx.x + 256 * u;
+      if (p < RR) {
+        int r = p / R, c = p - r * R;
+        double s = acc[u];
+        for (int rr = 0; rr < nr; ++rr) s = fma(As[rr * R + r], Bs[rr * R + c], s);
+        acc[u] = s;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    int p = threadIdx.x + 256 * u;
+    if (p < RR) partial[(int64_t)blockIdx.x * RR + p] = acc[u];
+  }
+}
+
+__global__ void k_reduce_partials(const double* partial, int nb, int RR, double* C) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= RR) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += partial[(int64_t)b * RR + p];
+  C[p] = s;
+}
+
+void launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C) {
+  int RR = h.R * h.R;
+  int nb = kPartBlocks;
+  if (nrows < (int64_t)nb * kGramRows) nb = (int)((nrows + kGramRows - 1) / kGramRows);
+  if (nb < 1) nb = 1;
+  k_gram<<<nb, 256, 0, h.stream>>>(A, B, nrows, h.R, wmode ? h.W : nullptr, h.smooth ? nullptr : h.row_patient,
+                                   h.smooth ? h.l : 1, h.partial);
+  k_reduce_partials<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, nb, RR, C);
+}
+
+void launch_fh(Handle& h) { launch_gram(h, h.Qt, h.Pp, h.S, 1, h.FH); }
+
+// ------------------------------------------------------------------ small dense: chol + ADMM
+// Cholesky of Ls (R x R in shared memory, lower, in place) by the whole block; returns 0 or 1 on failure.
+__device__ int block_chol(double* Ls, int R, int* fail) {
+  for (int j = 0; j < R; ++j) {
+    if (threadIdx.x == 0) {
+      double d = Ls[j * R + j];
+      for (int k = 0; k < j; ++k) d -= Ls[j * R + k] * Ls[j * R + k];
+      if (!(d > 0.0)) *fail = 1;
+      Ls[j * R + j] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < R; i += blockDim.x) {
+      double v = Ls[i * R + j];
+      for (int k = 0; k < j; ++k) v -= Ls[i * R + k] * Ls[j * R + k];
+      Ls[i * R + j] = v / Ls[j * R + j];
+    }
+    __syncthreads();
+  }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    int i = x / R, j = x - i * R;
+    if (j > i) Ls[x] = 0.0;
+  }
+  __syncthreads();
+  return *fail;
+}
+
+__device__ __forceinline__ void chol_solve(const double* L, int R, double* x) {
+  for (int i = 0; i < R; ++i) {
+    double v = x[i];
+    for (int k = 0; k < i; ++k) v -= L[i * R + k] * x[k];
+    x[i] = v / L[i * R + i];
+  }
+  for (int i = R - 1; i >= 0; --i) {
+    double v = x[i];
+    for (int k = i + 1; k < R; ++k) v -= L[k * R + i] * x[k];
+    x[i] = v / L[i * R + i];
+  }
+}
+
+// Builds G = G1 ∘ G2 and rho (fixed or trace/R) into shared memory; returns rho (<= 0: degenerate).
+__device__ double block_G_rho(const double* G1, const double* G2, int R, double rho_fixed, double* Gs) {
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Gs[x] = G1[x] * G2[x];
+  __syncthreads();
+  if (rho_fixed > 0.0) return rho_fixed;
+  double tr = 0.0;
+  for (int i = 0; i < R; ++i) tr += Gs[i * R + i];
+  return tr / R;
+}
+
+// One row of Alg.1 l.15-l.18 repeated n_inner times: z = (f + rho (zb + d)) (G + rho I)^-1;
+// zb = prox(z - d); d += zb - z.
+__device__ __forceinline__ void admm_row(const double* L, int R, const double* f, double* zb, double* dd, double rho,
+                                         int n_inner, int kind, double param) {
+  double z[kMaxR];
+  for (int it = 0; it < n_inner; ++it) {
+    for (int r = 0; r < R; ++r) z[r] = f[r] + rho * (zb[r] + dd[r]);
+    chol_solve(L, R, z);
+    for (int r = 0; r < R; ++r) {
+      double nb = prox(kind, param, rho, z[r] - dd[r]);
+      dd[r] += nb - z[r];
+      zb[r] = nb;
+    }
+  }
+}
+
+// H-mode (1 block) + the W-mode setup that depends only on the new H̄.
+__global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const double* VtV, const double* WtW,
+                                                double rho_fixed, int n_inner, int kind, double param, double* H,
+                                                double* DH, double* HtH, double* LW, double* scal, int* err) {
+  extern __shared__ double dyn_smem[];
+  double* Gs = dyn_smem;
+  double* Ls = dyn_smem + R * R;
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  double rho = block_G_rho(VtV, WtW, R, rho_fixed, Gs);
+  if (!(rho > 0.0)) { if (threadIdx.x == 0) set_err(err, ERR_DEGEN); return; }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Ls[x] = Gs[x] + ((x / R == x % R) ? rho : 0.0);
+  __syncthreads();
+  if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0) set_err(err, ERR_CHOL); return; }
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    double zb[kMaxR], dd[kMaxR], f[kMaxR];
+    for (int r = 0; r < R; ++r) { zb[r] = H[i * R + r]; dd[r] = DH[i * R + r]; f[r] = FH[i * R + r]; }
+    admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param);
+    for (int r = 0; r < R; ++r) { H[i * R + r] = zb[r]; DH[i * R + r] = dd[r]; }
+  }
+  __syncthreads();
+  // H̄^T H̄ (new), then G_W = (H̄^T H̄) ∘ (V̄^T V̄), rho_W, chol -> LW
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    int a = x / R, b = x - a * R;
+    double s = 0.0;
+    for (int i = 0; i < R; ++i) s = fma(H[i * R + a], H[i * R + b], s);
+    Gs[x] = s;
+    HtH[x] = s;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Gs[x] *= VtV[x];
+  __syncthreads();
+  double rho_w = rho_fixed;
+  if (!(rho_w > 0.0)) {
+    double tr = 0.0;
+    for (int i = 0; i < R; ++i) tr += Gs[i * R + i];
+    rho_w = tr / R;
+  }
+  if (!(rho_w > 0.0)) { if (threadIdx.x == 0) set_err(err, ERR_DEGEN); return; }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Ls[x] = Gs[x] + ((x / R == x % R) ? rho_w : 0.0);
+  __syncthreads();
+  if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0) set_err(err, ERR_CHOL); return; }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) LW[x] = Ls[x];
+  if (threadIdx.x == 0) { scal[S_RHO_H] = rho; scal[S_RHO_W] = rho_w; }
+}
+
+static size_t small_smem(Handle& h) { return sizeof(double) * 2 * (size_t)h.R * h.R; }
+template <class F>
+static void set_smem_attr(F* fn) {
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 2 * kMaxR * kMaxR));
+}
+
+void launch_admm_H(Handle& h) {
+  static bool once = (set_smem_attr(k_admm_H), true);
+  (void)once;
+  k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind, h.o.on_H.param,
+                                    h.H, h.DH, h.HtH, h.LW, h.scal, h.err);
+}
+
+// ------------------------------------------------------------------ pass B1: F_W, W-rows, N_k
+__global__ void __launch_bounds__(128) k_passB1(const int32_t* m, const int64_t* srow, int64_t K, int R,
+                                                const double* Pp, const double* Qt, const double* Hg,
+                                                const double* LWg, const double* scal, int n_inner, int kind,
+                                                double param, double* W, double* DW, double* Nst) {
+  extern __shared__ double dyn_smem[];
+  double* Hs = dyn_smem;
+  double* Ls = dyn_smem + R * R;
+  for (int i = threadIdx.x; i < R * R; i += blockDim.x) { Hs[i] = Hg[i]; Ls[i] = LWg[i]; }
+  __syncthreads();
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const double rho = scal[S_RHO_W];
+  const int mk = m[k];
+  const double* P = Pp + srow[k] * R;
+  const double* Q = Qt + srow[k] * R;
+  double fw[kMaxR], t[kMaxR];
+  for (int r = 0; r < R; ++r) fw[r] = 0.0;
+  for (int a = 0; a < mk; ++a) {  // F_W(k, r) = sum_a (Q~ H̄)(a, r) P'(a, r)
+    for (int r = 0; r < R; ++r) t[r] = 0.0;
+    for (int i = 0; i < R; ++i) {
+      double qa = Q[(int64_t)a * R + i];
+      for (int r = 0; r < R; ++r) t[r] = fma(qa, Hs[i * R + r], t[r]);
+    }
+    for (int r = 0; r < R; ++r) fw[r] = fma(t[r], P[(int64_t)a * R + r], fw[r]);
+  }
+  double zb[kMaxR], dd[kMaxR];
+  for (int r = 0; r < R; ++r) { zb[r] = W[k * R + r]; dd[r] = DW[k * R + r]; }
+  admm_row(Ls, R, fw, zb, dd, rho, n_inner, kind, param);
+  for (int r = 0; r < R; ++r) { W[k * R + r] = zb[r]; DW[k * R + r] = dd[r]; }
+  double* N = Nst + srow[k] * R;
+  for (int a = 0; a < mk; ++a) {  // N_k = Q~_k H̄ S_k (new w̄_k)
+    for (int r = 0; r < R; ++r) t[r] = 0.0;
+    for (int i = 0; i < R; ++i) {
+      double qa = Q[(int64_t)a * R + i];
+      for (int r = 0; r < R; ++r) t[r] = fma(qa, Hs[i * R + r], t[r]);
+    }
+    for (int r = 0; r < R; ++r) N[(int64_t)a * R + r] = t[r] * zb[r];
+  }
+}
+
+void launch_passB1(Handle& h) {
+  if (h.K == 0) return;
+  static bool once = (set_smem_attr(k_passB1), true);
+  (void)once;
+  k_passB1<<<(unsigned)((h.K + 127) / 128), 128, small_smem(h), h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.LW, h.scal,
+                                                                h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W,
+                                                                h.DW, h.Nst);
+}
+
+// ------------------------------------------------------------------ pass B2: F_V scatter
+__global__ void k_scatter_fibers(const int64_t* fiber_ptr, const int32_t* fiber_col, const double* fiber_val,
+                                 const int32_t* m, const int64_t* srow, int64_t K, int l, int R, const double* Nst,
+                                 double* FV) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += nwarps) {
+    const int mk = m[k];
+    const double* N = Nst + srow[k] * R;
+    double n0[kMaxL], n1[kMaxL];
+    const int r0 = lane, r1 = lane + 32;
+    for (int a = 0; a < kMaxL; ++a) {
+      n0[a] = (a < mk && r0 < R) ? N[a * R + r0] : 0.0;
+      n1[a] = (a < mk && r1 < R) ? N[a * R + r1] : 0.0;
+    }
+    const int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
+    for (int64_t f = f0; f < f1; ++f) {
+      const int64_t j = fiber_col[f];
+      const double* xv = fiber_val + f * l;
+      double s0 = 0.0, s1 = 0.0;
+      for (int a = 0; a < mk; ++a) {
+        double x = xv[a];
+        s0 = fma(x, n0[a], s0);
+        s1 = fma(x, n1[a], s1);
+      }
+      if (r0 < R) atomicAdd(&FV[j * R + r0], s0);
+      if (r1 < R) atomicAdd(&FV[j * R + r1], s1);
+    }
+  }
+}
+
+__global__ void k_scatter_rows(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int R,
+                               const double* Nst, double* FV) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= rows * R) return;
+  int64_t i = t / R;
+  int r = (int)(t - i * R);
+  double z = Nst[t];
+  if (z == 0.0) return;
+  for (int64_t e = rp[i]; e < rp[i + 1]; ++e) atomicAdd(&FV[(int64_t)col[e] * R + r], val[e] * z);
+}
+
+void launch_scatter(Handle& h) {
+  cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
+  if (h.K == 0) return;
+  if (h.smooth) {
+    int64_t blocks = (h.K + 7) / 8;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow,
+                                                             h.K, h.l, h.R, h.Nst, h.FV);
+  } else {
+    int64_t n = h.rows * h.R;
+    k_scatter_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R,
+                                                                      h.Nst, h.FV);
+  }
+}
+
+// ------------------------------------------------------------------ V-mode ADMM (rows independent)
+__global__ void __launch_bounds__(128) k_admm_V(int64_t J, int R, const double* FV, const double* HtH,
+                                                const double* WtW, double rho_fixed, int n_inner, int kind,
+                                                double param, double* V, double* DV, double* scal, int* err) {
+  extern __shared__ double dyn_smem[];
+  double* Gs = dyn_smem;
+  double* Ls = dyn_smem + R * R;
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  double rho = block_G_rho(HtH, WtW, R, rho_fixed, Gs);
+  if (!(rho > 0.0)) { if (threadIdx.x == 0 && blockIdx.x == 0) set_err(err, ERR_DEGEN); return; }
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Ls[x] = Gs[x] + ((x / R == x % R) ? rho : 0.0);
+  __syncthreads();
+  if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0 && blockIdx.x == 0) set_err(err, ERR_CHOL); return; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) scal[S_RHO_V] = rho;
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= J) return;
+  double zb[kMaxR], dd[kMaxR], f[kMaxR];
+  for (int r = 0; r < R; ++r) { zb[r] = V[j * R + r]; dd[r] = DV[j * R + r]; f[r] = FV[j * R + r]; }
+  admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param);
+  for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r]; DV[j * R + r] = dd[r]; }
+}
+
+void launch_admm_V(Handle& h) {
+  static bool once = (set_smem_attr(k_admm_V), true);
+  (void)once;
+  k_admm_V<<<(unsigned)((h.J + 127) / 128), 128, small_smem(h), h.stream>>>(h.J, h.R, h.FV, h.HtH, h.WtW, h.o.rho,
+                                                                 h.o.admm_inner, h.o.on_V.kind, h.o.on_V.param, h.V,
+                                                                 h.DV, h.scal, h.err);
+}
+
+// ------------------------------------------------------------------ FIT
+__global__ void k_fit(int64_t JR, int RR, const double* FV, const double* V, const double* M, const double* VtV,
+                      double* scal, int* err) {
+  __shared__ double red[2][256];
+  double c = 0.0, q = 0.0;
+  for (int64_t x = threadIdx.x; x < JR; x += blockDim.x) c = fma(FV[x], V[x], c);
+  for (int x = threadIdx.x; x < RR; x += blockDim.x) q = fma(M[x], VtV[x], q);
+  red[0][threadIdx.x] = c;
+  red[1][threadIdx.x] = q;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) { red[0][threadIdx.x] += red[0][threadIdx.x + o]; red[1][threadIdx.x] += red[1][threadIdx.x + o]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double normX = scal[S_NORMX];
+    double E = normX - 2.0 * red[0][0] + red[1][0];
+    double fit = 1.0 - E / normX;
+    scal[S_CROSS] = red[0][0];
+    scal[S_QUAD] = red[1][0];
+    scal[S_E] = E;
+    scal[S_FIT] = fit;
+    if (!isfinite(fit)) set_err(err, ERR_NONFINITE);
+  }
+}
+
+void launch_fit(Handle& h) {
+  launch_gram(h, h.V, h.V, h.J, 0, h.VtV);
+  k_fit<<<1, 256, 0, h.stream>>>(h.J * h.R, h.R * h.R, h.FV, h.V, h.M, h.VtV, h.scal, h.err);
+}
+
+// ------------------------------------------------------------------ U_k = C_k Q~_k H̄ (output)
+__global__ void k_U(const int64_t* prp, const double* times, int64_t K, int l, int d, const double* Bk,
+                    const int32_t* m, const int64_t* srow, int R, const double* Qt, const double* H, double* U) {
+  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  int64_t r0 = prp[k], r1 = prp[k + 1];
+  const int mk = m[k];
+  const double* Q = Qt + srow[k] * R;
+  for (int64_t i = r0; i < r1; ++i) {
+    double c[kMaxL];
+    int mrows;
+    if (l > 0) {
+      for (int a = 0; a < kMaxL; ++a) c[a] = 0.0;
+      if (mk > 0) {
+        double N[kMaxDeg + 1];
+        double t1 = times[r0], tn = times[r1 - 1];
+        int mu = spline_eval(times[i], t1, tn, l, d, N);
+        const double* B = Bk + k * (int64_t)l * l;
+        for (int a = 0; a < mk; ++a) {
+          double s = 0.0;
+          for (int r = 0; r <= d; ++r) s = fma(N[r], B[(mu - d + r) * l + a], s);
+          c[a] = s;
+        }
+      }
+      mrows = mk;
+    } else {
+      mrows = 0;
+    }
+    for (int s = 0; s < R; ++s) {
+      double acc = 0.0;
+      if (l > 0) {
+        for (int a = 0; a < mrows; ++a) {
+          double qh = 0.0;
+          for (int x = 0; x < R; ++x) qh = fma(Q[a * R + x], H[x * R + s], qh);
+          acc = fma(c[a], qh, acc);
+        }
+      } else {
+        for (int x = 0; x < R; ++x) acc = fma(Q[(i - r0) * R + x], H[x * R + s], acc);
+      }
+      U[i * R + s] = acc;
+    }
+  }
+}
+
+void launch_U(Handle& h, double* U) {
+  if (h.K == 0) return;
+  k_U<<<(unsigned)((h.K + 127) / 128), 128, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K,
+                                                           h.smooth ? h.l : 0, h.d, h.Bk, h.m, h.srow, h.R, h.Qt,
+                                                           h.H, U);
+}
+
+}  // namespace copa
