@@ -164,6 +164,16 @@ const char* copa_last_error(void);
  * m (K_local int32), srow (K_local+1 int64 state-row offsets), rank (K_local int32). */
 copa_status copa_debug_state(copa_handle* h, double* Pp, double* Qt, int32_t* m, int64_t* srow, int32_t* rank);
 
+/* Phase timing for measurement (bench.py): when on, copa_iterate records CUDA events around
+ * each phase of the iteration on the library stream. Turning it on resets the accumulators. */
+copa_status copa_set_profiling(copa_handle* h, int32_t on);
+/* Accumulated milliseconds and call counts per phase (arrays of n entries, NULL to skip),
+ * the number of phases, and the number of kernels the iterations launched while profiling.
+ * Synchronises the handle's stream. */
+copa_status copa_get_phase_times(copa_handle* h, double* ms, int64_t* calls, int32_t n, int32_t* n_phases,
+                                 int64_t* launches);
+const char* copa_phase_name(int32_t i);
+
 #ifdef __cplusplus
 }
 #endif

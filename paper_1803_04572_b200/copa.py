@@ -84,10 +84,15 @@ def lib() -> ctypes.CDLL:
         L.copa_destroy.restype = None
         L.copa_last_error.restype = ctypes.c_char_p
         L.copa_debug_state.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.copa_set_profiling.argtypes = [vp, i32]
+        L.copa_get_phase_times.argtypes = [vp, vp, vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i64)]
+        L.copa_phase_name.argtypes = [i32]
+        L.copa_phase_name.restype = ctypes.c_char_p
         L.copa_get_limits.argtypes = [ctypes.POINTER(_Limits)]
         L.copa_get_limits.restype = None
         for f in ("copa_workspace_size", "copa_init", "copa_iterate", "copa_get_factors", "copa_get_duals",
-                  "copa_get_U", "copa_get_stats", "copa_fit_workspace_size", "copa_fit", "copa_debug_state"):
+                  "copa_get_U", "copa_get_stats", "copa_fit_workspace_size", "copa_fit", "copa_debug_state",
+                  "copa_set_profiling", "copa_get_phase_times"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
@@ -243,6 +248,21 @@ class Copa:
         return {"fit": s.fit, "rho": list(s.rho), "normX": s.normX, "iterations": s.iterations, "fibers": s.fibers,
                 "state_rows": s.state_rows, "rank_deficient": s.rank_deficient}
 
+    def set_profiling(self, on: bool = True):
+        """Record CUDA events around each phase of the iteration (on the library's stream)."""
+        _check(lib().copa_set_profiling(self.h, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """{phase: (total_ms, calls)} accumulated since set_profiling(True), plus '_launches'."""
+        ms = (ctypes.c_double * 32)()
+        calls = (ctypes.c_int64 * 32)()
+        n = ctypes.c_int32(0)
+        launches = ctypes.c_int64(0)
+        _check(lib().copa_get_phase_times(self.h, ms, calls, 32, ctypes.byref(n), ctypes.byref(launches)))
+        out = {lib().copa_phase_name(i).decode(): (ms[i], int(calls[i])) for i in range(n.value)}
+        out["_launches"] = int(launches.value)
+        return out
+
     def debug_state(self):
         t = self.torch
         st = self.stats()
@@ -269,7 +289,8 @@ class Copa:
             pass
 
 
-def fit_host(prob, options: Options, n_outer: int, R: Optional[int] = None, stream=None, workspace=None):
+def fit_host(prob, options: Options, n_outer: int, R: Optional[int] = None, stream=None, workspace=None,
+             allreduce: Optional[Callable] = None):
     """End-to-end call with HOST inputs (copa_fit): H2D copies, init, n_outer iterations and D2H of
     the factors all happen inside the library. Returns (fits, H, V, W) as numpy arrays."""
     torch = _torch()
@@ -291,11 +312,12 @@ def fit_host(prob, options: Options, n_outer: int, R: Optional[int] = None, stre
                  val=hp(prob.val, np.float64),
                  visit_time=hp(prob.times, np.float64) if options.smooth_l > 0 else None)
     stream = stream if stream is not None else torch.cuda.current_stream()
+    cb = ALLREDUCE_FN(allreduce) if allreduce is not None else ALLREDUCE_FN()
     o = _Options(on_H=_Constraint(*options.con_H), on_W=_Constraint(*options.con_W), on_V=_Constraint(*options.con_V),
                  smooth_l=options.smooth_l, smooth_degree=options.smooth_degree, rho=options.rho,
                  admm_inner=options.admm_inner, rank_tol=options.rank_tol, basis_tol=options.basis_tol,
                  H0=hp(np.asarray(prob.H0)[:R, :R], np.float64), V0=hp(prob.V0, np.float64),
-                 W0_local=hp(prob.W0, np.float64), allreduce=ALLREDUCE_FN(), allreduce_ctx=None,
+                 W0_local=hp(prob.W0, np.float64), allreduce=cb, allreduce_ctx=None,
                  stream=stream.cuda_stream)
     if workspace is None:
         nbytes = ctypes.c_size_t(0)

@@ -68,7 +68,7 @@ size_t carve(Handle& h, char* base) {
   h.Qt = c.take<double>(h.S * R);
   h.Nst = c.take<double>(h.S * R);
   h.partial = c.take<double>((int64_t)kPartBlocks * RR);
-  h.host_fit = c.take<double>(1024);  // device ring of per-iteration FIT values
+  h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   if (h.smooth) {
     h.Bk = c.take<double>(h.K * h.l * h.l);
     h.fiber_ptr = c.take<int64_t>(h.K + 1);
@@ -271,21 +271,63 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   return COPA_OK;
 }
 
+// Phase timing (copa_set_profiling): event pairs around each phase of the iteration, on the
+// library's stream, summed at the next synchronisation point.
+static const char* kPhaseNames[kPhases] = {"spmm", "polar", "fh", "allreduce_c1", "admm_H", "passB1",
+                                           "grams_B", "scatter", "allreduce_c2", "admm_V", "fit"};
+
+static void phase_begin(Handle& h, int ph) {
+  if (!h.profiling) return;
+  if (h.ev_used + 2 > (int)h.events.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    h.events.push_back(a);
+    h.events.push_back(b);
+  }
+  h.ev_phase.push_back(ph);
+  cudaEventRecord(h.events[h.ev_used], h.stream);
+}
+static void phase_end(Handle& h) {
+  if (!h.profiling) return;
+  cudaEventRecord(h.events[h.ev_used + 1], h.stream);
+  h.ev_used += 2;
+}
+static void phase_collect(Handle& h) {
+  for (int i = 0; i < h.ev_used; i += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, h.events[i], h.events[i + 1]) == cudaSuccess) {
+      h.phase_ms[h.ev_phase[i / 2]] += ms;
+      h.phase_calls[h.ev_phase[i / 2]] += 1;
+    }
+  }
+  h.ev_used = 0;
+  h.ev_phase.clear();
+}
+
+#define PHASE(ph, expr)  \
+  do {                   \
+    phase_begin(h, ph);  \
+    h.launches += (expr); \
+    phase_end(h);        \
+  } while (0)
+
 static copa_status iterate_once(Handle& h) {
-  copa_status st;
+  copa_status st = COPA_OK;
   const int64_t RR = (int64_t)h.R * h.R;
-  launch_spmm(h);
-  launch_polar(h);
-  launch_fh(h);
-  if ((st = allreduce(h, h.FH, RR)) != COPA_OK) return st;  // C1
-  launch_admm_H(h);
-  launch_passB1(h);
-  launch_gram(h, h.W, h.W, h.K, 0, h.WtW);
-  launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M);
-  launch_scatter(h);
-  if ((st = allreduce(h, h.comm2, h.J * h.R + 2 * RR)) != COPA_OK) return st;  // C2
-  launch_admm_V(h);
-  launch_fit(h);
+  PHASE(0, launch_spmm(h));
+  PHASE(1, launch_polar(h));
+  PHASE(2, launch_fh(h));
+  PHASE(3, (st = allreduce(h, h.FH, RR), 0));  // C1
+  if (st != COPA_OK) return st;
+  PHASE(4, launch_admm_H(h));
+  PHASE(5, launch_passB1(h));
+  PHASE(6, launch_gram(h, h.W, h.W, h.K, 0, h.WtW) + launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M));
+  PHASE(7, launch_scatter(h));
+  PHASE(8, (st = allreduce(h, h.comm2, h.J * h.R + 2 * RR), 0));  // C2
+  if (st != COPA_OK) return st;
+  PHASE(9, launch_admm_V(h));
+  PHASE(10, launch_fit(h));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "iteration launch");
   return COPA_OK;
@@ -301,14 +343,15 @@ copa_status copa_iterate(copa_handle* H, int32_t n_outer, double* fit_host) {
     for (int32_t t = 0; t < chunk; ++t) {
       copa_status st = iterate_once(h);
       if (st != COPA_OK) return st;
-      cudaMemcpyAsync(h.host_fit + t, h.scal + S_FIT, sizeof(double), cudaMemcpyDeviceToDevice, h.stream);
+      cudaMemcpyAsync(h.fit_ring + t, h.scal + S_FIT, sizeof(double), cudaMemcpyDeviceToDevice, h.stream);
       ++h.iterations;
     }
     if (fit_host)
-      CUDA_TRY(cudaMemcpyAsync(fit_host + done, h.host_fit, sizeof(double) * chunk, cudaMemcpyDefault, h.stream),
+      CUDA_TRY(cudaMemcpyAsync(fit_host + done, h.fit_ring, sizeof(double) * chunk, cudaMemcpyDefault, h.stream),
                "fit copy");
     copa_status st = check_err(h);
     if (st != COPA_OK) return st;
+    phase_collect(h);
     done += chunk;
   }
   return COPA_OK;
@@ -390,7 +433,37 @@ copa_status copa_debug_state(copa_handle* H, double* Pp, double* Qt, int32_t* m,
   return COPA_OK;
 }
 
-void copa_destroy(copa_handle* H) { delete H; }
+void copa_destroy(copa_handle* H) {
+  if (!H) return;
+  for (auto e : H->h.events) cudaEventDestroy(e);
+  delete H;
+}
+
+copa_status copa_set_profiling(copa_handle* H, int32_t on) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  Handle& h = H->h;
+  h.profiling = on != 0;
+  for (int i = 0; i < kPhases; ++i) { h.phase_ms[i] = 0; h.phase_calls[i] = 0; }
+  h.launches = 0;
+  return COPA_OK;
+}
+
+copa_status copa_get_phase_times(copa_handle* H, double* ms, int64_t* calls, int32_t n, int32_t* n_phases,
+                                 int64_t* launches) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  Handle& h = H->h;
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "phase sync");
+  phase_collect(h);
+  for (int i = 0; i < n && i < kPhases; ++i) {
+    if (ms) ms[i] = h.phase_ms[i];
+    if (calls) calls[i] = h.phase_calls[i];
+  }
+  if (n_phases) *n_phases = kPhases;
+  if (launches) *launches = h.launches;
+  return COPA_OK;
+}
+
+const char* copa_phase_name(int32_t i) { return (i >= 0 && i < kPhases) ? kPhaseNames[i] : ""; }
 
 // ---------------------------------------------------------------- end-to-end with host inputs
 static size_t input_bytes(const copa_problem* p) {

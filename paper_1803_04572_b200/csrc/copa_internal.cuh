@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/copa.h"
 
 namespace copa {
@@ -14,6 +16,7 @@ constexpr int kMaxL = 16;       // smooth_l limit
 constexpr int kMaxDeg = 7;      // spline degree limit
 constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
+constexpr int kPhases = 11;       // timed phases of one outer iteration (copa_get_phase_times)
 
 enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
 
@@ -50,8 +53,16 @@ struct Handle {
   void* cub_temp;
   size_t cub_temp_bytes;
   int64_t* counts_scratch;
-  double* host_fit;    // pinned staging for FIT
+  double* fit_ring;    // device ring of per-iteration FIT values
   int own_inputs;      // copa_fit: CSR copied into the workspace
+  // phase profiling (copa_set_profiling)
+  bool profiling = false;
+  std::vector<cudaEvent_t> events;
+  std::vector<int> ev_phase;
+  int ev_used = 0;
+  double phase_ms[kPhases] = {0};
+  int64_t phase_calls[kPhases] = {0};
+  int64_t launches = 0;  // kernels launched by the iteration (counted while profiling)
 };
 
 // ------------------------------------------------------------------ device helpers
@@ -167,16 +178,16 @@ void launch_build_fibers(Handle& h);
 void launch_row_patient(Handle& h);
 void launch_sumsq(Handle& h, double* out);
 // iteration
-void launch_spmm(Handle& h);
-void launch_polar(Handle& h);
-void launch_fh(Handle& h);
-void launch_admm_H(Handle& h);
-void launch_passB1(Handle& h);
-void launch_scatter(Handle& h);
-void launch_admm_V(Handle& h);
-void launch_fit(Handle& h);
+int launch_spmm(Handle& h);
+int launch_polar(Handle& h);
+int launch_fh(Handle& h);
+int launch_admm_H(Handle& h);
+int launch_passB1(Handle& h);
+int launch_scatter(Handle& h);
+int launch_admm_V(Handle& h);
+int launch_fit(Handle& h);
 // reductions: C (R x R) = sum_s A(s,:)^T (B(s,:) * w(s,:)); wsrc: 0 none, 1 W rows by patient of s
-void launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
+int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
 void launch_U(Handle& h, double* U);
 
 }  // namespace copa

@@ -64,8 +64,8 @@ __global__ void k_spmm_rows(const int64_t* rp, const int32_t* col, const double*
   Pp[t] = acc;
 }
 
-void launch_spmm(Handle& h) {
-  if (h.K == 0) return;
+int launch_spmm(Handle& h) {
+  if (h.K == 0) return 0;
   if (h.smooth) {
     int64_t blocks = (h.K + 7) / 8;
     if (blocks > 148 * 32) blocks = 148 * 32;
@@ -76,6 +76,7 @@ void launch_spmm(Handle& h) {
     k_spmm_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R, h.V,
                                                                    h.Pp);
   }
+  return 1;
 }
 
 // ------------------------------------------------------------------ pass A: polar (thread per patient)
@@ -176,10 +177,11 @@ __global__ void __launch_bounds__(64) k_polar(const int32_t* m, const int64_t* s
   }
 }
 
-void launch_polar(Handle& h) {
-  if (h.K == 0) return;
+int launch_polar(Handle& h) {
+  if (h.K == 0) return 0;
   k_polar<<<(unsigned)((h.K + 63) / 64), 64, 0, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol,
                                                             h.Qt, h.rank);
+  return 1;
 }
 
 // ------------------------------------------------------------------ R x R reductions
@@ -235,7 +237,7 @@ __global__ void k_reduce_partials(const double* partial, int nb, int RR, double*
   C[p] = s;
 }
 
-void launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C) {
+int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C) {
   int RR = h.R * h.R;
   int nb = kPartBlocks;
   if (nrows < (int64_t)nb * kGramRows) nb = (int)((nrows + kGramRows - 1) / kGramRows);
@@ -243,9 +245,10 @@ void launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int
   k_gram<<<nb, 256, 0, h.stream>>>(A, B, nrows, h.R, wmode ? h.W : nullptr, h.smooth ? nullptr : h.row_patient,
                                    h.smooth ? h.l : 1, h.partial);
   k_reduce_partials<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, nb, RR, C);
+  return 2;
 }
 
-void launch_fh(Handle& h) { launch_gram(h, h.Qt, h.Pp, h.S, 1, h.FH); }
+int launch_fh(Handle& h) { return launch_gram(h, h.Qt, h.Pp, h.S, 1, h.FH); }
 
 // ------------------------------------------------------------------ small dense: chol + ADMM
 // Cholesky of Ls (R x R in shared memory, lower, in place) by the whole block; returns 0 or 1 on failure.
@@ -365,11 +368,12 @@ static void set_smem_attr(F* fn) {
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 2 * kMaxR * kMaxR));
 }
 
-void launch_admm_H(Handle& h) {
+int launch_admm_H(Handle& h) {
   static bool once = (set_smem_attr(k_admm_H), true);
   (void)once;
   k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind, h.o.on_H.param,
                                     h.H, h.DH, h.HtH, h.LW, h.scal, h.err);
+  return 1;
 }
 
 // ------------------------------------------------------------------ pass B1: F_W, W-rows, N_k
@@ -413,13 +417,14 @@ __global__ void __launch_bounds__(128) k_passB1(const int32_t* m, const int64_t*
   }
 }
 
-void launch_passB1(Handle& h) {
-  if (h.K == 0) return;
+int launch_passB1(Handle& h) {
+  if (h.K == 0) return 0;
   static bool once = (set_smem_attr(k_passB1), true);
   (void)once;
   k_passB1<<<(unsigned)((h.K + 127) / 128), 128, small_smem(h), h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.LW, h.scal,
                                                                 h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W,
                                                                 h.DW, h.Nst);
+  return 1;
 }
 
 // ------------------------------------------------------------------ pass B2: F_V scatter
@@ -464,9 +469,9 @@ __global__ void k_scatter_rows(const int64_t* rp, const int32_t* col, const doub
   for (int64_t e = rp[i]; e < rp[i + 1]; ++e) atomicAdd(&FV[(int64_t)col[e] * R + r], val[e] * z);
 }
 
-void launch_scatter(Handle& h) {
+int launch_scatter(Handle& h) {
   cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
-  if (h.K == 0) return;
+  if (h.K == 0) return 0;
   if (h.smooth) {
     int64_t blocks = (h.K + 7) / 8;
     if (blocks > 148 * 32) blocks = 148 * 32;
@@ -477,6 +482,7 @@ void launch_scatter(Handle& h) {
     k_scatter_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R,
                                                                       h.Nst, h.FV);
   }
+  return 1;
 }
 
 // ------------------------------------------------------------------ V-mode ADMM (rows independent)
@@ -503,12 +509,13 @@ __global__ void __launch_bounds__(128) k_admm_V(int64_t J, int R, const double* 
   for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r]; DV[j * R + r] = dd[r]; }
 }
 
-void launch_admm_V(Handle& h) {
+int launch_admm_V(Handle& h) {
   static bool once = (set_smem_attr(k_admm_V), true);
   (void)once;
   k_admm_V<<<(unsigned)((h.J + 127) / 128), 128, small_smem(h), h.stream>>>(h.J, h.R, h.FV, h.HtH, h.WtW, h.o.rho,
                                                                  h.o.admm_inner, h.o.on_V.kind, h.o.on_V.param, h.V,
                                                                  h.DV, h.scal, h.err);
+  return 1;
 }
 
 // ------------------------------------------------------------------ FIT
@@ -537,9 +544,10 @@ __global__ void k_fit(int64_t JR, int RR, const double* FV, const double* V, con
   }
 }
 
-void launch_fit(Handle& h) {
-  launch_gram(h, h.V, h.V, h.J, 0, h.VtV);
+int launch_fit(Handle& h) {
+  int n = launch_gram(h, h.V, h.V, h.J, 0, h.VtV);
   k_fit<<<1, 256, 0, h.stream>>>(h.J * h.R, h.R * h.R, h.FV, h.V, h.M, h.VtV, h.scal, h.err);
+  return n + 1;
 }
 
 // ------------------------------------------------------------------ U_k = C_k Q~_k H̄ (output)

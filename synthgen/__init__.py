@@ -205,6 +205,23 @@ def generate(name_or_cfg, K: Optional[int] = None, k_range: Optional[tuple] = No
     return Problem(cfg, k0, k1, prp, rp, col, val, times, H0, V0, W0)
 
 
+def patient_nnz(name_or_cfg, K: Optional[int] = None) -> np.ndarray:
+    """nnz per patient of a workload without generating columns/values (for nnz-balanced sharding)."""
+    cfg = CONFIGS[name_or_cfg] if isinstance(name_or_cfg, str) else name_or_cfg
+    lib = _load()
+    Kfull = cfg.K if K is None else int(K)
+    cs = _cstruct(cfg, Kfull)
+    I = np.empty(Kfull, dtype=np.int32)
+    lib.gen_patient_rows(ctypes.byref(cs), 0, Kfull, _ptr(I))
+    prp = np.zeros(Kfull + 1, dtype=np.int64)
+    np.cumsum(I, out=prp[1:])
+    rn = np.empty(int(prp[-1]), dtype=np.int32)
+    lib.gen_row_sizes(ctypes.byref(cs), 0, Kfull, _ptr(prp), _ptr(rn))
+    c = np.zeros(len(rn) + 1, dtype=np.int64)
+    np.cumsum(rn, out=c[1:])
+    return np.diff(c[prp])
+
+
 def shard_bounds(patient_nnz: np.ndarray, world: int) -> np.ndarray:
     """Contiguous patient ranges with nonzeros balanced: bounds[r]..bounds[r+1].
 
