@@ -75,6 +75,14 @@ size_t carve(Handle& h, char* base) {
     h.fiber_col = c.take<int32_t>(h.F);
     h.fiber_val = c.take<double>(h.F * h.l);
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
+    h.counter = c.take<int>(64);
+    h.order = c.take<int32_t>(h.K);
+    h.woff = c.take<uint16_t>(h.K * (h.sc_warps + 1));
+    h.jlo = c.take<int32_t>(h.sc_warps + 1);
+    h.block_k = c.take<int64_t>(h.sc_blocks + 1);
+    h.fv_part = c.take<double>((int64_t)h.sc_blocks * h.J * R);
+    h.layout_tmp_bytes = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 8 * (size_t)h.J + 4096;
+    h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     h.row_patient = c.take<int32_t>(h.rows);
   }
@@ -125,6 +133,15 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   h.nnz = p->nnz;
   h.R = p->R;
   h.S = h.smooth ? h.K * h.l : h.rows;
+  h.sc_warps = 16;
+  h.sc_blocks = 148;
+  if (h.smooth) {
+    size_t smem = sizeof(double) * (size_t)(h.J * h.R);
+    int per_sm = smem > 0 ? (int)((220 * 1024) / (smem + 1024)) : 1;
+    if (per_sm < 1) per_sm = 1;
+    if (per_sm > 2) per_sm = 2;
+    h.sc_blocks = 148 * per_sm;
+  }
 }
 
 copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
@@ -245,6 +262,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     if (h.K > 0) cub::DeviceScan::InclusiveSum(h.cub_temp, tb, h.fiber_ptr, h.fiber_ptr, (int)(h.K + 1), s);
     launch_basis(h);
     launch_build_fibers(h);
+    build_fiber_layout(h, h.layout_tmp, h.layout_tmp_bytes);
   } else {
     launch_row_patient(h);
     if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);

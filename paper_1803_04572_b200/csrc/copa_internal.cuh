@@ -50,6 +50,16 @@ struct Handle {
   int32_t* fiber_col;  // smooth: [F]
   double* fiber_val;   // smooth: [F x l]
   int32_t* row_patient;  // non-smooth: [rows]
+  // fiber-pass layout (smooth): pass A dynamic order, pass B per-CTA patient ranges / per-warp feature ranges
+  int* counter;          // pass A work counter
+  int32_t* order;        // [K] patients by fiber count, descending
+  uint16_t* woff;        // [K x (sc_warps+1)] fiber offsets of each scatter warp's feature range
+  int32_t* jlo;          // [sc_warps+1] feature range boundaries
+  int64_t* block_k;      // [sc_blocks+1] patient range of each scatter CTA
+  double* fv_part;       // [sc_blocks x J x R] per-CTA F_V partials
+  int sc_blocks = 0, sc_warps = 16;
+  void* layout_tmp;
+  size_t layout_tmp_bytes = 0;
   void* cub_temp;
   size_t cub_temp_bytes;
   int64_t* counts_scratch;
@@ -189,5 +199,11 @@ int launch_fit(Handle& h);
 // reductions: C (R x R) = sum_s A(s,:)^T (B(s,:) * w(s,:)); wsrc: 0 none, 1 W rows by patient of s
 int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
 void launch_U(Handle& h, double* U);
+// fiber passes (k_fibers.cu)
+void launch_spmm_fibers(Handle& h);
+int launch_scatter_fibers(Handle& h);
+bool scatter_smem_ok(const Handle& h);
+size_t fiber_layout_temp_bytes(int64_t K);
+void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes);
 
 }  // namespace copa

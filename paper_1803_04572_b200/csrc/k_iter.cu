@@ -67,10 +67,7 @@ __global__ void k_spmm_rows(const int64_t* rp, const int32_t* col, const double*
 int launch_spmm(Handle& h) {
   if (h.K == 0) return 0;
   if (h.smooth) {
-    int64_t blocks = (h.K + 7) / 8;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    k_spmm_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow, h.K,
-                                                          h.l, h.R, h.V, h.Pp);
+    launch_spmm_fibers(h);
   } else {
     int64_t n = h.rows * h.R;
     k_spmm_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R, h.V,
@@ -472,7 +469,9 @@ __global__ void k_scatter_rows(const int64_t* rp, const int32_t* col, const doub
 int launch_scatter(Handle& h) {
   cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
   if (h.K == 0) return 0;
-  if (h.smooth) {
+  if (h.smooth && scatter_smem_ok(h)) {
+    return launch_scatter_fibers(h);
+  } else if (h.smooth) {
     int64_t blocks = (h.K + 7) / 8;
     if (blocks > 148 * 32) blocks = 148 * 32;
     k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow,
