@@ -6,6 +6,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "copa_internal.cuh"
 
@@ -67,7 +68,7 @@ size_t carve(Handle& h, char* base) {
   h.Pp = c.take<double>(h.S * R);
   h.Qt = c.take<double>(h.S * R);
   h.Nst = c.take<double>(h.S * R);
-  h.partial = c.take<double>((int64_t)kPartBlocks * RR);
+  h.partial = c.take<double>(2 * (int64_t)kPartBlocks * RR);
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   if (h.smooth) {
     h.Bk = c.take<double>(h.K * h.l * h.l);
@@ -77,11 +78,13 @@ size_t carve(Handle& h, char* base) {
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
     h.counter = c.take<int>(64);
     h.order = c.take<int32_t>(h.K);
-    h.woff = c.take<uint16_t>(h.K * (h.sc_warps + 1));
-    h.jlo = c.take<int32_t>(h.sc_warps + 1);
-    h.block_k = c.take<int64_t>(h.sc_blocks + 1);
-    h.fv_part = c.take<double>((int64_t)h.sc_blocks * h.J * R);
-    h.layout_tmp_bytes = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 8 * (size_t)h.J + 4096;
+    h.perm = c.take<int32_t>(h.J);
+    h.inv = c.take<int32_t>(h.Jl);
+    h.woff = c.take<uint16_t>(h.K * h.sc_G * 16);
+    h.block_k = c.take<int64_t>(h.sc_ranges + 1);
+    h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
+    h.fhist = c.take<unsigned long long>(h.J);
+    h.layout_tmp_bytes = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 4096;
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     h.row_patient = c.take<int32_t>(h.rows);
@@ -133,15 +136,8 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   h.nnz = p->nnz;
   h.R = p->R;
   h.S = h.smooth ? h.K * h.l : h.rows;
-  h.sc_warps = 16;
-  h.sc_blocks = 148;
-  if (h.smooth) {
-    size_t smem = sizeof(double) * (size_t)(h.J * h.R);
-    int per_sm = smem > 0 ? (int)((220 * 1024) / (smem + 1024)) : 1;
-    if (per_sm < 1) per_sm = 1;
-    if (per_sm > 2) per_sm = 2;
-    h.sc_blocks = 148 * per_sm;
-  }
+  h.Jl = h.J;
+  if (h.smooth) plan_scatter(h);
 }
 
 copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
@@ -156,7 +152,7 @@ copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
   void* tmp = nullptr;
   CUDA_TRY(cudaMallocAsync(&counts, sizeof(int64_t) * (size_t)(h.K + 2), h.stream), "cudaMallocAsync(count)");
   CUDA_TRY(cudaMallocAsync(&tmp, tb + 256, h.stream), "cudaMallocAsync(scan)");
-  launch_count_fibers(h, counts);
+  launch_count_fibers(h, counts, nullptr);
   cub::DeviceScan::InclusiveSum(tmp, tb, counts, counts, (int)(h.K + 1), h.stream);
   int64_t F = 0;
   CUDA_TRY(cudaMemcpyAsync(&F, counts + h.K, sizeof(int64_t), cudaMemcpyDeviceToHost, h.stream), "count copy");
@@ -257,9 +253,21 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   if (st != COPA_OK) { delete H; return st; }
   if (h.smooth) {
     if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
-    launch_count_fibers(h, h.fiber_ptr);
+    launch_count_fibers(h, h.fiber_ptr, h.fhist);
     size_t tb = h.cub_temp_bytes;
     if (h.K > 0) cub::DeviceScan::InclusiveSum(h.cub_temp, tb, h.fiber_ptr, h.fiber_ptr, (int)(h.K + 1), s);
+    {  // feature relabeling by fiber mass (host, J <= 65535)
+      std::vector<unsigned long long> hist((size_t)h.J);
+      std::vector<int32_t> perm((size_t)h.J), inv((size_t)h.Jl);
+      CUDA_TRY(cudaMemcpyAsync(hist.data(), h.fhist, sizeof(unsigned long long) * (size_t)h.J, cudaMemcpyDeviceToHost,
+                               s), "hist copy");
+      CUDA_TRY(cudaStreamSynchronize(s), "hist sync");
+      int64_t Js = 0;
+      compute_relabel(h.J, h.sc_G * kScatterWarps, hist.data(), perm.data(), inv.data(), &Js);
+      CUDA_TRY(cudaMemcpyAsync(h.perm, perm.data(), sizeof(int32_t) * (size_t)h.J, cudaMemcpyHostToDevice, s), "perm");
+      CUDA_TRY(cudaMemcpyAsync(h.inv, inv.data(), sizeof(int32_t) * (size_t)h.Jl, cudaMemcpyHostToDevice, s), "inv");
+      CUDA_TRY(cudaStreamSynchronize(s), "perm sync");
+    }
     launch_basis(h);
     launch_build_fibers(h);
     build_fiber_layout(h, h.layout_tmp, h.layout_tmp_bytes);
@@ -333,14 +341,19 @@ static void phase_collect(Handle& h) {
 static copa_status iterate_once(Handle& h) {
   copa_status st = COPA_OK;
   const int64_t RR = (int64_t)h.R * h.R;
+  const bool wide = polar_wide_ok(h);
   PHASE(0, launch_spmm(h));
-  PHASE(1, launch_polar(h));
-  PHASE(2, launch_fh(h));
+  PHASE(1, wide ? launch_polar_wide(h) : launch_polar(h));  // wide: F_H fused into the polar kernel
+  if (!wide) PHASE(2, launch_fh(h));
   PHASE(3, (st = allreduce(h, h.FH, RR), 0));  // C1
   if (st != COPA_OK) return st;
   PHASE(4, launch_admm_H(h));
-  PHASE(5, launch_passB1(h));
-  PHASE(6, launch_gram(h, h.W, h.W, h.K, 0, h.WtW) + launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M));
+  if (wide) {
+    PHASE(5, launch_passB_wide(h));  // F_W, W rows, N, M and W^T W in one pass
+  } else {
+    PHASE(5, launch_passB1(h));
+    PHASE(6, launch_gram(h, h.W, h.W, h.K, 0, h.WtW) + launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M));
+  }
   PHASE(7, launch_scatter(h));
   PHASE(8, (st = allreduce(h, h.comm2, h.J * h.R + 2 * RR), 0));  // C2
   if (st != COPA_OK) return st;

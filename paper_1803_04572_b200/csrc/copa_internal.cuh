@@ -50,14 +50,18 @@ struct Handle {
   int32_t* fiber_col;  // smooth: [F]
   double* fiber_val;   // smooth: [F x l]
   int32_t* row_patient;  // non-smooth: [rows]
-  // fiber-pass layout (smooth): pass A dynamic order, pass B per-CTA patient ranges / per-warp feature ranges
+  // fiber-pass layout (smooth): relabeled features, pass A order, pass B patient ranges / label ranges
   int* counter;          // pass A work counter
   int32_t* order;        // [K] patients by fiber count, descending
-  uint16_t* woff;        // [K x (sc_warps+1)] fiber offsets of each scatter warp's feature range
-  int32_t* jlo;          // [sc_warps+1] feature range boundaries
-  int64_t* block_k;      // [sc_blocks+1] patient range of each scatter CTA
-  double* fv_part;       // [sc_blocks x J x R] per-CTA F_V partials
-  int sc_blocks = 0, sc_warps = 16;
+  int32_t* perm;         // [J] feature -> label
+  int32_t* inv;          // [Jl] label -> feature (-1: unused label)
+  uint16_t* woff;        // [K x G x 16] fiber offsets of the scatter warps' label ranges
+  int64_t* block_k;      // [sc_ranges+1] patient range of each scatter CTA pair/group
+  double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
+  unsigned long long* fhist;  // [J] fibers per feature (init)
+  int64_t Jl = 0;        // labels = G * Jg >= J
+  int sc_G = 1, sc_CH = 32, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
+  int64_t sc_Js = 0, sc_Jg = 0;
   void* layout_tmp;
   size_t layout_tmp_bytes = 0;
   void* cub_temp;
@@ -182,7 +186,7 @@ __device__ __forceinline__ void set_err(int* err, int bit) { atomicOr(err, bit);
 // ------------------------------------------------------------------ launchers
 // init
 void launch_validate(Handle& h);
-void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/);
+void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/, unsigned long long* hist);
 void launch_basis(Handle& h);
 void launch_build_fibers(Handle& h);
 void launch_row_patient(Handle& h);
@@ -203,7 +207,14 @@ void launch_U(Handle& h, double* U);
 void launch_spmm_fibers(Handle& h);
 int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
+void plan_scatter(Handle& h);
+void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int32_t* perm, int32_t* inv, int64_t* Js);
+constexpr int kScatterWarps = 8;
 size_t fiber_layout_temp_bytes(int64_t K);
 void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes);
+// wide per-patient dense kernels (k_dense.cu)
+bool polar_wide_ok(const Handle& h);
+int launch_polar_wide(Handle& h);
+int launch_passB_wide(Handle& h);
 
 }  // namespace copa

@@ -1,0 +1,626 @@
+// k_dense.cu — per-patient dense work of the smooth ("wide": m_k <= l < R) path, organised in
+// warp rounds of 32 patients: the R-dimension contractions run on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, warp-cooperative, one patient per MMA tile) and the small sequential
+// m_k x m_k algebra (Givens QR, one-sided Jacobi, row ADMM solves) runs one patient per thread.
+//
+//   polar_wide : A_k = P'_k S_k H̄^T (MMA, 8-column slabs) -> Givens QR of A_k^T (thread)
+//                -> Jacobi (thread) -> Q~_k = K_k A_k (thread, K_k = V Σ^-1 V^T on the range)
+//                -> F_H += Q~_k^T P'_k S_k (MMA, per-warp accumulators)        (Alg.1 l.4-6, l.12)
+//   passB_wide : T_k = Q~_k H̄ (MMA) -> F_W(k,:) = colsum(T_k ∘ P'_k) -> W-row ADMM (thread)
+//                -> N_k = T_k S_k (MMA recompute) -> M += N_k^T N_k, W̄^T W̄ (MMA)  (l.12-19, FIT)
+#include <cstdlib>
+
+#include "copa_internal.cuh"
+
+namespace copa {
+
+__device__ __forceinline__ void dmma2(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// Prefetch the byte range [p, p + bytes) with the 32 lanes of a warp (128-byte lines).
+__device__ __forceinline__ void warp_prefetch(const void* p, size_t bytes, bool to_l1) {
+  const int lane = threadIdx.x & 31;
+  const char* c = (const char*)((uintptr_t)p & ~(uintptr_t)127);
+  const char* e = (const char*)p + bytes;
+  for (const char* x = c + 128 * lane; x < e; x += 128 * 32) {
+    if (to_l1) pf_l1(x); else pf_l2(x);
+  }
+}
+
+// Prefetch the state rows of patients [base, base + 32) (srow-contiguous) and their W rows.
+__device__ __forceinline__ void round_prefetch(int64_t base, int64_t K, int R, const int64_t* srow, const double* A,
+                                               const double* B, const double* Wrows, bool to_l1) {
+  if (base >= K) return;
+  int64_t last = base + 32 < K ? base + 32 : K;
+  int64_t s0 = srow[base], s1 = srow[last];
+  warp_prefetch(A + s0 * R, sizeof(double) * (size_t)((s1 - s0) * R), to_l1);
+  if (B) warp_prefetch(B + s0 * R, sizeof(double) * (size_t)((s1 - s0) * R), to_l1);
+  if (Wrows) warp_prefetch(Wrows + base * R, sizeof(double) * (size_t)((last - base) * R), to_l1);
+}
+
+// Givens insert of column vector c[0..L) into the upper-triangular Rf (L x L, registers).
+template <int L>
+__device__ __forceinline__ void givens_insert_reg(double (&Rf)[L][L], double (&c)[L]) {
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const double aj = c[j];
+    if (aj != 0.0) {
+      const double r = Rf[j][j];
+      const double n2 = fma(r, r, aj * aj);
+      const double inv = rsqrt(n2);
+      const double cs = r * inv, sn = aj * inv;
+      Rf[j][j] = n2 * inv;
+#pragma unroll
+      for (int t = j + 1; t < L; ++t) {
+        const double x = Rf[j][t], y = c[t];
+        Rf[j][t] = fma(cs, x, sn * y);
+        c[t] = fma(cs, y, -sn * x);
+      }
+    }
+  }
+}
+
+// One-sided Jacobi on the rows of Wm (L x L, registers) until mutually orthogonal.
+template <int L>
+__device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
+  const double tol = 2.220446049250313e-16 * (double)L;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int rotated = 0;
+#pragma unroll
+    for (int p = 0; p < L - 1; ++p) {
+#pragma unroll
+      for (int q = p + 1; q < L; ++q) {
+        double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+          a = fma(Wm[p][i], Wm[p][i], a);
+          b = fma(Wm[q][i], Wm[q][i], b);
+          c = fma(Wm[p][i], Wm[q][i], c);
+        }
+        if (a != 0.0 && b != 0.0 && fabs(c) > tol * sqrt(a * b)) {
+          rotated = 1;
+          const double zeta = (b - a) / (2.0 * c);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double cs = rsqrt(fma(t, t, 1.0));
+          const double sn = cs * t;
+#pragma unroll
+          for (int i = 0; i < L; ++i) {
+            const double x = Wm[p][i], y = Wm[q][i];
+            Wm[p][i] = fma(cs, x, -sn * y);
+            Wm[q][i] = fma(sn, x, cs * y);
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, rotated == 0)) break;
+  }
+}
+
+// Warp-cooperative A slab: slab[p][a][cc] = A_p(a, s = 8 nt + cc) for the round's patients.
+// A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps).
+template <int MT, int KS>
+__device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int R, const int32_t* m, const int64_t* srow,
+                                       const double* Pp, const double* W, const double* Hs, double* slab) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int p = 0; p < 32; ++p) {
+    const int64_t kp = base + p;
+    if (kp >= K) break;
+    const int mp = m[kp];
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+    if (mp > 0) {
+      const double* P = Pp + srow[kp] * R;
+      const double* w = W + kp * R;
+      const int s = 8 * nt + g;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int r = 4 * ks + t;
+        const double b = (r < R && s < R) ? Hs[s * R + r] : 0.0;  // B[t][g] = H^T(r, s)
+        const double wr = r < R ? w[r] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const int a = 8 * mt + g;
+          const double av = (a < mp && r < R) ? P[a * R + r] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+          dmma2(c[mt][0], c[mt][1], av, b);
+        }
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t] = c[mt][0];
+      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t + 1] = c[mt][1];
+    }
+  }
+}
+
+template <int L, int MT, int NT>
+__global__ void __launch_bounds__(128) k_polar_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
+                                                    int64_t K, int R, const double* __restrict__ Pp,
+                                                    const double* __restrict__ W, const double* __restrict__ Hg,
+                                                    double tau, double* __restrict__ Qt, int32_t* __restrict__ rank,
+                                                    double* __restrict__ FHpart) {
+  constexpr int KS = (NT * 8 + 3) / 4;  // r steps of 4 covering 8 NT >= R
+  extern __shared__ double sm[];
+  const int hoff = ((R * R + 31) / 32) * 32;
+  double* Hs = sm;                                      // R x R
+  const int wib = threadIdx.x >> 5;
+  double* slab = sm + hoff + wib * (32 * MT * 8 * 8);   // per warp: 32 patients x (MT 8) x 8
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Hs[x] = Hg[x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
+  const int64_t rounds = (K + 31) / 32;
+  double fh[NT][NT][2];
+#pragma unroll
+  for (int a = 0; a < NT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
+  for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
+    const int64_t base = rd * 32;
+    round_prefetch(base, K, R, srow, Pp, nullptr, W, true);
+    round_prefetch(base + 32 * (int64_t)nwarps_total, K, R, srow, Pp, nullptr, W, false);
+    const int64_t kme = base + lane;
+    const int mme = kme < K ? m[kme] : 0;
+    // ---- Givens QR of A^T (rows of A^T = columns of A), slab by slab
+    double Rf[L][L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+      for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) {
+      a_slab<MT, KS>(nt, base, K, R, m, srow, Pp, W, Hs, slab);
+      __syncwarp();
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        if (8 * nt + cc < R) {
+          double col[L];
+#pragma unroll
+          for (int a = 0; a < L; ++a) col[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+          givens_insert_reg<L>(Rf, col);
+        }
+      }
+      __syncwarp();
+    }
+    // ---- SVD of the m x m factor: rows of Rf -> sigma_j v_j; u_j = v_j / sqrt(sigma_j) so that
+    //      K = sum_kept u_j u_j^T = V Σ^-1 V^T on the numerical range (reading R-polar-2/3)
+    jacobi_rows_reg<L>(Rf);
+    double sig[L], smax = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
+      sig[j] = sqrt(s);
+      smax = fmax(smax, sig[j]);
+    }
+    int rk = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const bool keep = smax > 0.0 && sig[j] > tau * smax;
+      rk += keep ? 1 : 0;
+      const double sc = keep ? 1.0 / (sig[j] * sqrt(sig[j])) : 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Rf[j][i] *= sc;
+    }
+    if (kme < K) rank[kme] = mme > 0 ? rk : 0;
+    // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
+    for (int nt = 0; nt < NT; ++nt) {
+      a_slab<MT, KS>(nt, base, K, R, m, srow, Pp, W, Hs, slab);
+      __syncwarp();
+      if (kme < K && mme > 0) {
+        double* Q = Qt + srow[kme] * R;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const int s = 8 * nt + cc;
+          if (s < R) {
+            double y[L];
+#pragma unroll
+            for (int a = 0; a < L; ++a) y[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+            double q[L];
+#pragma unroll
+            for (int a = 0; a < L; ++a) q[a] = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+              double d = 0.0;
+#pragma unroll
+              for (int a = 0; a < L; ++a) d = fma(Rf[j][a], y[a], d);
+#pragma unroll
+              for (int a = 0; a < L; ++a) q[a] = fma(Rf[j][a], d, q[a]);
+            }
+#pragma unroll
+            for (int a = 0; a < L; ++a)
+              if (a < mme) Q[a * R + s] = q[a];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // ---- F_H += Q~_p^T (P'_p S_p): MMA with M = r, N = s, K = a
+    for (int p = 0; p < 32; ++p) {
+      const int64_t kp = base + p;
+      if (kp >= K) break;
+      const int mp = m[kp];
+      if (mp == 0) continue;
+      const double* Q = Qt + srow[kp] * R;
+      const double* P = Pp + srow[kp] * R;
+      const double* w = W + kp * R;
+#pragma unroll
+      for (int ks = 0; ks < 2 * MT; ++ks) {
+        const int a = 4 * ks + t;
+        double af[NT], bf[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          const int rr = 8 * i + g;
+          af[i] = (a < mp && rr < R) ? Q[a * R + rr] : 0.0;            // A[g][t] = Q~^T(r, a)
+          bf[i] = (a < mp && rr < R) ? P[a * R + rr] * w[rr] : 0.0;    // B[t][g] = (P'S)(a, s)
+        }
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma2(fh[i][j][0], fh[i][j][1], af[i], bf[j]);
+      }
+    }
+  }
+  // ---- reduce the per-warp F_H accumulators of the block, write the block partial
+  __syncthreads();
+  double* red = sm + hoff;  // reuse the slabs: (warps) x (8 NT)^2
+  const int RP = 8 * NT;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) red[wib * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = fh[i][j][c];
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    const int r = x / R, s = x - r * R;
+    double v = 0.0;
+    for (int ww = 0; ww < nw; ++ww) v += red[ww * RP * RP + r * RP + s];
+    FHpart[(int64_t)blockIdx.x * R * R + x] = v;
+  }
+}
+
+__global__ void k_sum_rr(const double* part, int nb, int n, double* out) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * n + x];
+  out[x] = s;
+}
+
+constexpr int kDenseThreads = 128;
+
+template <int L, int NT>
+static void polar_wide_inst(Handle& h) {
+  constexpr int MT = (L + 7) / 8;
+  auto fn = k_polar_wide<L, MT, NT>;
+  const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
+  const size_t slabs = (size_t)(kDenseThreads / 32) * 32 * MT * 8 * 8;
+  const size_t red = (size_t)(kDenseThreads / 32) * (8 * NT) * (8 * NT);
+  size_t smem = sizeof(double) * (hoff + (slabs > red ? slabs : red));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  int64_t rounds = (h.K + 31) / 32;
+  int64_t blocks = (rounds + 3) / 4;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, smem);
+  if (const char* e = getenv("COPA_POLAR_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
+  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  if (cap > kPartBlocks) cap = kPartBlocks;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt,
+                                                         h.rank, h.partial);
+  const int RR = h.R * h.R;
+  k_sum_rr<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.FH);
+}
+
+template <int L>
+static void polar_wide_n(Handle& h) {
+  switch ((h.R + 7) / 8) {
+    case 1: polar_wide_inst<L, 1>(h); break;
+    case 2: polar_wide_inst<L, 2>(h); break;
+    case 3: polar_wide_inst<L, 3>(h); break;
+    case 4: polar_wide_inst<L, 4>(h); break;
+    case 5: polar_wide_inst<L, 5>(h); break;
+    case 6: polar_wide_inst<L, 6>(h); break;
+    case 7: polar_wide_inst<L, 7>(h); break;
+    default: polar_wide_inst<L, 8>(h); break;
+  }
+}
+
+bool polar_wide_ok(const Handle& h) { return h.smooth && h.l < h.R && h.l <= 12; }
+
+// Polar + F_H for the wide case. Returns kernels launched.
+int launch_polar_wide(Handle& h) {
+  if (h.l <= 4) polar_wide_n<4>(h);
+  else if (h.l <= 7) polar_wide_n<7>(h);
+  else if (h.l <= 8) polar_wide_n<8>(h);
+  else if (h.l <= 9) polar_wide_n<9>(h);
+  else polar_wide_n<12>(h);
+  return 2;
+}
+
+// ------------------------------------------------------------------ pass B (wide): F_W, W ADMM, N, M, W^T W
+// T slab for patient p: T(a, r) = sum_i Q~(a, i) H̄(i, r). MMA: M = a, N = r (NT tiles), K = i.
+template <int MT, int NT>
+__device__ __forceinline__ void t_tiles(int64_t kp, int mp, int R, const int64_t* srow, const double* Qt,
+                                        const double* Hs, double (&c)[MT][NT][2]) {
+  constexpr int KS = (NT * 8 + 3) / 4;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const double* Q = Qt + srow[kp] * R;
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int i = 4 * ks + t;
+    double af[MT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int a = 8 * mt + g;
+      af[mt] = (a < mp && i < R) ? Q[a * R + i] : 0.0;  // A[g][t] = Q~(a, i)
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int r = 8 * nt + g;
+      const double b = (i < R && r < R) ? Hs[i * R + r] : 0.0;  // B[t][g] = H(i, r)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) dmma2(c[mt][nt][0], c[mt][nt][1], af[mt], b);
+    }
+  }
+}
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(128) k_passB_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
+                                                    int64_t K, int R, const double* __restrict__ Pp,
+                                                    const double* __restrict__ Qt, const double* __restrict__ Hg,
+                                                    const double* __restrict__ LWg, const double* __restrict__ scal,
+                                                    int n_inner, int kind, double param, double* __restrict__ W,
+                                                    double* __restrict__ DW, double* __restrict__ Nst,
+                                                    double* __restrict__ part /* [blocks][2][R R] */) {
+  constexpr int RP = 8 * NT;
+  extern __shared__ double sm[];
+  const int hoff = ((R * R + 31) / 32) * 32;
+  double* Hs = sm;                 // R x R
+  double* Ls = sm + hoff;          // R x R (chol of G_W + rho I)
+  const int wib = threadIdx.x >> 5;
+  double* wv = sm + 2 * hoff + wib * (3 * RP * 32);  // per warp: fw, w̄, d as [r][lane]
+  double* fwv = wv;
+  double* wbv = wv + RP * 32;
+  double* dv = wv + 2 * RP * 32;
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Ls[x] = LWg[x]; }
+  __syncthreads();
+  const double rho = scal[S_RHO_W];
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
+  const int64_t rounds = (K + 31) / 32;
+  double macc[NT][NT][2], wacc[NT][NT][2];
+#pragma unroll
+  for (int a = 0; a < NT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) macc[a][b][0] = macc[a][b][1] = wacc[a][b][0] = wacc[a][b][1] = 0.0;
+  for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
+    const int64_t base = rd * 32;
+    round_prefetch(base, K, R, srow, Pp, Qt, W, true);
+    round_prefetch(base + 32 * (int64_t)nwarps_total, K, R, srow, Pp, Qt, W, false);
+    if (base < K) warp_prefetch(DW + base * R, sizeof(double) * 32 * R, true);
+    // ---- F_W rows: F_W(k, r) = sum_a T(a, r) P'(a, r)
+    for (int p = 0; p < 32; ++p) {
+      const int64_t kp = base + p;
+      if (kp >= K) break;
+      const int mp = m[kp];
+      double c[MT][NT][2];
+      t_tiles<MT, NT>(kp, mp, R, srow, Qt, Hs, c);
+      const double* P = Pp + srow[kp] * R;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = 8 * nt + 2 * t + i;
+          double s = 0.0;
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            const int a = 8 * mt + g;
+            s = fma(c[mt][nt][i], (a < mp && r < R) ? P[a * R + r] : 0.0, s);
+          }
+          s += __shfl_xor_sync(0xffffffffu, s, 4);
+          s += __shfl_xor_sync(0xffffffffu, s, 8);
+          s += __shfl_xor_sync(0xffffffffu, s, 16);
+          if (g == 0) fwv[r * 32 + p] = s;
+        }
+    }
+    __syncwarp();
+    // ---- W-row ADMM (thread = patient): z = (f + rho (w̄ + d)) (G + rho I)^-1; w̄ = prox(z - d); d += w̄ - z
+    const int64_t kme = base + lane;
+    if (kme < K) {
+      for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
+      double z[RP];
+      for (int it = 0; it < n_inner; ++it) {
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          z[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
+#pragma unroll
+        for (int i = 0; i < RP; ++i) {
+          if (i < R) {
+            double v = z[i];
+#pragma unroll
+            for (int k2 = 0; k2 < i; ++k2) v = fma(-Ls[i * R + k2], z[k2], v);
+            z[i] = v / Ls[i * R + i];
+          }
+        }
+#pragma unroll
+        for (int i = RP - 1; i >= 0; --i) {
+          if (i < R) {
+            double v = z[i];
+#pragma unroll
+            for (int k2 = i + 1; k2 < RP; ++k2)
+              if (k2 < R) v = fma(-Ls[k2 * R + i], z[k2], v);
+            z[i] = v / Ls[i * R + i];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          if (r < R) {
+            const double d0 = dv[r * 32 + lane];
+            const double nb = prox(kind, param, rho, z[r] - d0);
+            dv[r * 32 + lane] = d0 + nb - z[r];
+            wbv[r * 32 + lane] = nb;
+          }
+        }
+      }
+      for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
+    } else {
+      for (int r = 0; r < R; ++r) wbv[r * 32 + lane] = 0.0;
+    }
+    __syncwarp();
+    // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T  (MMA with K = patients)
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int p = 4 * ks + t;
+      double af[NT];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int r = 8 * i + g;
+        af[i] = r < R ? wbv[r * 32 + p] : 0.0;  // A[g][t] = w̄_p(r) ; B[t][g] = w̄_p(s) (same values)
+      }
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma2(wacc[i][j][0], wacc[i][j][1], af[i], af[j]);
+    }
+    // ---- N_p = T_p S_p (new w̄_p), M += N_p^T N_p
+    for (int p = 0; p < 32; ++p) {
+      const int64_t kp = base + p;
+      if (kp >= K) break;
+      const int mp = m[kp];
+      if (mp == 0) continue;
+      double c[MT][NT][2];
+      t_tiles<MT, NT>(kp, mp, R, srow, Qt, Hs, c);
+      double* N = Nst + srow[kp] * R;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int a = 8 * mt + g;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int r = 8 * nt + 2 * t + i;
+            const double v = r < R ? c[mt][nt][i] * wbv[r * 32 + p] : 0.0;
+            c[mt][nt][i] = v;
+            if (a < mp && r < R) N[a * R + r] = v;
+          }
+      }
+      __syncwarp();
+      // M += N^T N: A[g][t] = N(a = 4ks+t, r = 8i+g), B[t][g] = N(a, s = 8j+g): read back from global (L1)
+#pragma unroll
+      for (int ks = 0; ks < 2 * MT; ++ks) {
+        const int a = 4 * ks + t;
+        double af[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          const int r = 8 * i + g;
+          af[i] = (a < mp && r < R) ? N[a * R + r] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < NT; ++i)
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma2(macc[i][j][0], macc[i][j][1], af[i], af[j]);
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double* red = sm + 2 * hoff;  // reuse: warps x 2 x RP^2
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        red[(wib * 2 + 0) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = macc[i][j][c];
+        red[(wib * 2 + 1) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = wacc[i][j][c];
+      }
+  __syncthreads();
+  for (int x = threadIdx.x; x < 2 * R * R; x += blockDim.x) {
+    const int which = x / (R * R), y = x - which * R * R;
+    const int r = y / R, s = y - r * R;
+    double v = 0.0;
+    for (int ww = 0; ww < nw; ++ww) v += red[(ww * 2 + which) * RP * RP + r * RP + s];
+    part[((int64_t)blockIdx.x * 2 + which) * R * R + y] = v;
+  }
+}
+
+__global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, double* WtW) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 2 * RR) return;
+  int which = x / RR, y = x - which * RR;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[((int64_t)b * 2 + which) * RR + y];
+  (which == 0 ? M : WtW)[y] = s;
+}
+
+template <int MT, int NT>
+static void passB_wide_inst(Handle& h) {
+  constexpr int RP = 8 * NT;
+  auto fn = k_passB_wide<MT, NT>;
+  const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
+  size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32);
+  size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
+  size_t smem = sizeof(double) * 2 * hoff + (per_warp * (kDenseThreads / 32) > red ? per_warp * (kDenseThreads / 32) : red);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  int64_t rounds = (h.K + 31) / 32;
+  int64_t blocks = (rounds + 3) / 4;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, smem);
+  if (const char* e = getenv("COPA_PASSB_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
+  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  if (cap > kPartBlocks) cap = kPartBlocks;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.LW, h.scal,
+                                                         h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
+                                                         h.Nst, h.partial);
+  const int RR = h.R * h.R;
+  k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
+}
+
+template <int MT>
+static void passB_wide_n(Handle& h) {
+  switch ((h.R + 7) / 8) {
+    case 1: passB_wide_inst<MT, 1>(h); break;
+    case 2: passB_wide_inst<MT, 2>(h); break;
+    case 3: passB_wide_inst<MT, 3>(h); break;
+    case 4: passB_wide_inst<MT, 4>(h); break;
+    case 5: passB_wide_inst<MT, 5>(h); break;
+    case 6: passB_wide_inst<MT, 6>(h); break;
+    case 7: passB_wide_inst<MT, 7>(h); break;
+    default: passB_wide_inst<MT, 8>(h); break;
+  }
+}
+
+// F_W + W-ADMM + N + M + W^T W for smooth patients (m_k <= l <= 16). Returns kernels launched.
+int launch_passB_wide(Handle& h) {
+  if (h.l <= 8) passB_wide_n<1>(h);
+  else passB_wide_n<2>(h);
+  return 2;
+}
+
+}  // namespace copa

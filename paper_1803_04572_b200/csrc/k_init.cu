@@ -50,14 +50,19 @@ void launch_validate(Handle& h) {
 }
 
 // ------------------------------------------------------------------ fibers: count
-// Warp per patient; each warp owns a J-bit bitmap in shared memory.
+// Warp per patient; each warp owns a J-bit bitmap in shared memory. Also accumulates the number of
+// fibers per feature (hist, optional) used to relabel features into balanced ranges.
 __global__ void k_count_fibers(const int64_t* prp, const int64_t* rp, const int32_t* col, int64_t K, int words,
-                               int64_t* counts) {
+                               int64_t* counts, unsigned long long* hist, int64_t J) {
   extern __shared__ unsigned smem_bits[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned* bits = smem_bits + wib * words;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib; k < K; k += nwarps) {
+  unsigned* bh = smem_bits + nw * words;  // block histogram [J]
+  if (hist)
+    for (int64_t j = threadIdx.x; j < J; j += blockDim.x) bh[j] = 0u;
+  __syncthreads();
+  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  for (int64_t k = blockIdx.x * (int64_t)nw + wib; k < K; k += nwarps) {
     for (int w = lane; w < words; w += 32) bits[w] = 0u;
     __syncwarp();
     int64_t e0 = rp[prp[k]], e1 = rp[prp[k + 1]];
@@ -67,23 +72,43 @@ __global__ void k_count_fibers(const int64_t* prp, const int64_t* rp, const int3
     }
     __syncwarp();
     int c = 0;
-    for (int w = lane; w < words; w += 32) c += __popc(bits[w]);
+    for (int w = lane; w < words; w += 32) {
+      unsigned b = bits[w];
+      c += __popc(b);
+      if (hist)
+        while (b) {
+          int bit = __ffs(b) - 1;
+          b &= b - 1;
+          atomicAdd(&bh[w * 32 + bit], 1u);
+        }
+    }
     for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) counts[k + 1] = c;
     __syncwarp();
   }
+  if (hist) {
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < J; j += blockDim.x)
+      if (bh[j]) atomicAdd(&hist[j], (unsigned long long)bh[j]);
+  }
 }
 
-void launch_count_fibers(Handle& h, int64_t* counts) {
+void launch_count_fibers(Handle& h, int64_t* counts, unsigned long long* hist) {
   int words = (int)((h.J + 31) / 32);
   int warps = 8;
-  size_t smem = (size_t)warps * words * sizeof(unsigned);
+  size_t smem = (size_t)warps * words * sizeof(unsigned) + (hist ? sizeof(unsigned) * (size_t)h.J : 0);
   cudaMemsetAsync(counts, 0, sizeof(int64_t), h.stream);
+  if (hist) cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * (size_t)h.J, h.stream);
   if (h.K == 0) return;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_count_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
   int64_t blocks = (h.K + warps - 1) / warps;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_count_fibers<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.K,
-                                                                    words, counts);
+                                                                    words, counts, hist, h.J);
 }
 
 // ------------------------------------------------------------------ basis (thread per patient)
@@ -151,7 +176,8 @@ void launch_basis(Handle& h) {
 // fibers), so the accumulation is race-free and its order (ascending row) deterministic.
 __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int32_t* col, const double* val,
                                const double* times, int64_t K, int words, int l, int d, const double* Bk,
-                               const int32_t* m, const int64_t* fiber_ptr, int32_t* fiber_col, double* fiber_val) {
+                               const int32_t* m, const int64_t* fiber_ptr, const int32_t* perm, int32_t* fiber_col,
+                               double* fiber_val) {
   extern __shared__ unsigned smem_b[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
@@ -164,7 +190,7 @@ __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int3
     int64_t r0 = prp[k], r1 = prp[k + 1];
     int64_t e0 = rp[r0], e1 = rp[r1];
     for (int64_t e = e0 + lane; e < e1; e += 32) {
-      int32_t j = col[e];
+      int32_t j = perm[col[e]];  // relabeled feature id (fibers sorted by the new label)
       atomicOr(&bits[j >> 5], 1u << (j & 31));
     }
     __syncwarp();
@@ -211,7 +237,7 @@ __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int3
           c[a] = s;
         }
         for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
-          int32_t j = col[e];
+          int32_t j = perm[col[e]];
           double x = val[e];
           int f = pref[j >> 5] + __popc(bits[j >> 5] & ((1u << (j & 31)) - 1u));
           double* dst = fv + (int64_t)f * l;
@@ -226,14 +252,14 @@ __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int3
 
 void launch_build_fibers(Handle& h) {
   if (h.K == 0) return;
-  int words = (int)((h.J + 31) / 32);
+  int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
   int warps = 8;
   size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
   int64_t blocks = (h.K + warps - 1) / warps;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_build_fibers<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(
       h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m,
-      h.fiber_ptr, h.fiber_col, h.fiber_val);
+      h.fiber_ptr, h.perm, h.fiber_col, h.fiber_val);
 }
 
 // ------------------------------------------------------------------ non-smooth helpers

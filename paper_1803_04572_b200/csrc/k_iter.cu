@@ -17,41 +17,6 @@ __device__ __forceinline__ int64_t patient_of(int64_t s, const int32_t* row_pat,
 }
 
 // ------------------------------------------------------------------ pass A: SpMM
-// Smooth: warp per patient; lane owns (a, r) pairs of P'_k (m_k x R); loops over the patient's fibers.
-constexpr int kSpmmU = 16;  // pairs per lane: m_k * R <= 512
-__global__ void k_spmm_fibers(const int64_t* fiber_ptr, const int32_t* fiber_col, const double* fiber_val,
-                              const int32_t* m, const int64_t* srow, int64_t K, int l, int R, const double* V,
-                              double* Pp) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += nwarps) {
-    const int mk = m[k];
-    const int pairs = mk * R;
-    double acc[kSpmmU];
-#pragma unroll
-    for (int u = 0; u < kSpmmU; ++u) acc[u] = 0.0;
-    const int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
-    for (int64_t f = f0; f < f1; ++f) {
-      const int64_t j = fiber_col[f];
-      const double* xv = fiber_val + f * l;
-#pragma unroll
-      for (int u = 0; u < kSpmmU; ++u) {
-        int p = lane + 32 * u;
-        if (p < pairs) {
-          int a = p / R, r = p - a * R;
-          acc[u] = fma(xv[a], V[j * R + r], acc[u]);
-        }
-      }
-    }
-    double* out = Pp + srow[k] * R;
-#pragma unroll
-    for (int u = 0; u < kSpmmU; ++u) {
-      int p = lane + 32 * u;
-      if (p < pairs) out[p] = acc[u];
-    }
-  }
-}
-
 // Plain (no smoothness): P_k = X_k V̄, thread per (row, r).
 __global__ void k_spmm_rows(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int R,
                             const double* V, double* Pp) {
@@ -427,7 +392,7 @@ int launch_passB1(Handle& h) {
 // ------------------------------------------------------------------ pass B2: F_V scatter
 __global__ void k_scatter_fibers(const int64_t* fiber_ptr, const int32_t* fiber_col, const double* fiber_val,
                                  const int32_t* m, const int64_t* srow, int64_t K, int l, int R, const double* Nst,
-                                 double* FV) {
+                                 const int32_t* inv, double* FV) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += nwarps) {
@@ -441,7 +406,7 @@ __global__ void k_scatter_fibers(const int64_t* fiber_ptr, const int32_t* fiber_
     }
     const int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
     for (int64_t f = f0; f < f1; ++f) {
-      const int64_t j = fiber_col[f];
+      const int64_t j = inv[fiber_col[f]];  // fibers carry relabeled feature ids
       const double* xv = fiber_val + f * l;
       double s0 = 0.0, s1 = 0.0;
       for (int a = 0; a < mk; ++a) {
@@ -475,7 +440,7 @@ int launch_scatter(Handle& h) {
     int64_t blocks = (h.K + 7) / 8;
     if (blocks > 148 * 32) blocks = 148 * 32;
     k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow,
-                                                             h.K, h.l, h.R, h.Nst, h.FV);
+                                                             h.K, h.l, h.R, h.Nst, h.inv, h.FV);
   } else {
     int64_t n = h.rows * h.R;
     k_scatter_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R,
