@@ -141,15 +141,23 @@ class _CAI:
                                          "stream": None}
 
 
-def torch_allreduce(group=None) -> Callable:
-    """Allreduce callback over torch.distributed (NCCL on GPUs). The library calls it on its own
-    stream, which is torch's current stream, so no host synchronisation is needed."""
+def torch_allreduce(group=None, device: str = "cuda") -> Callable:
+    """Allreduce(sum) callback over torch.distributed for copa_options.allreduce.
+
+    device="cuda": the library passes a device pointer and its stream, which is torch's current
+    stream, so NCCL's all_reduce is ordered after the producing kernels without a host sync.
+    device="cpu": host buffers (gloo), used by the multi-rank host-logic tests.
+    """
     torch = _torch()
     import torch.distributed as dist
 
     def fn(ptr, n, stream, ctx):
         try:
-            t = torch.as_tensor(_CAI(ptr, n), device="cuda")
+            if device == "cpu":
+                arr = np.ctypeslib.as_array((ctypes.c_double * int(n)).from_address(int(ptr)))
+                t = torch.from_numpy(arr)
+            else:
+                t = torch.as_tensor(_CAI(ptr, n), device="cuda")
             dist.all_reduce(t, group=group)
             return 0
         except Exception:  # noqa: BLE001 - reported to the library as a status

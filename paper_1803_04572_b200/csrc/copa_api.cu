@@ -114,7 +114,6 @@ copa_status check_args(const copa_problem* p, const copa_options* o) {
     if (o->smooth_degree < 0 || o->smooth_degree > kMaxDeg || o->smooth_degree >= o->smooth_l)
       return fail(COPA_E_ARG, "smooth_degree must be in [0, min(7, l-1)]");
     if (p->K_local > 0 && !p->visit_time) return fail(COPA_E_ARG, "smoothness requires visit times");
-    if (o->smooth_l * p->R > 32 * 16) return fail(COPA_E_UNSUPPORTED, "smooth_l * R > 512 not supported");
   } else if (p->R > kMaxQ) {
     // plain path: tall patients have q = R; this build's thread-per-patient polar needs q <= 16
     return fail(COPA_E_UNSUPPORTED, "R > 16 without smoothness not supported by this build");
