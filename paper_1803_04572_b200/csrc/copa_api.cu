@@ -65,26 +65,35 @@ size_t carve(Handle& h, char* base) {
   h.m = c.take<int32_t>(h.K);
   h.rank = c.take<int32_t>(h.K);
   h.srow = c.take<int64_t>(h.K + 1);
-  h.Pp = c.take<double>(h.S * R);
-  h.Qt = c.take<double>(h.S * R);
-  h.Nst = c.take<double>(h.S * R);
+  h.Pp = c.take<double>(h.S * R + 4);   // +4: bulk copies round up to 16 bytes
+  h.Qt = c.take<double>(h.S * R + 4);
+  h.Nst = c.take<double>(h.S * R + 4);
   h.partial = c.take<double>(2 * (int64_t)kPartBlocks * RR);
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   if (h.smooth) {
+    const int G = h.sc_G;
+    h.Fcap = h.F + 8;
     h.Bk = c.take<double>(h.K * h.l * h.l);
     h.fiber_ptr = c.take<int64_t>(h.K + 1);
-    h.fiber_col = c.take<int32_t>(h.F);
-    h.fiber_val = c.take<double>(h.F * h.l);
+    h.gptr = c.take<int64_t>((int64_t)G * (h.K + 1) + 2);  // +2: bulk copies round up to 16 bytes
+    h.fiber_col = c.take<int32_t>(h.Fcap);
+    h.fiber_val = c.take<double>(h.Fcap * h.l);
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
     h.counter = c.take<int>(64);
     h.order = c.take<int32_t>(h.K);
     h.perm = c.take<int32_t>(h.J);
     h.inv = c.take<int32_t>(h.Jl);
-    h.woff = c.take<uint16_t>(h.K * h.sc_G * 16);
+    h.Vl = c.take<double>(h.Jl * R);
     h.block_k = c.take<int64_t>(h.sc_ranges + 1);
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
-    h.layout_tmp_bytes = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 4096;
+    h.nst_cap = stage_cap(h);
+    h.st_f = c.take<int64_t>(2 * h.nst_cap);
+    h.st_k = c.take<int32_t>(2 * h.nst_cap);
+    h.cta_st = c.take<int32_t>((int64_t)h.sc_ranges * G + 1);
+    size_t lt = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 4096;
+    size_t gc = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;
+    h.layout_tmp_bytes = lt > gc ? lt : gc;
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     h.row_patient = c.take<int32_t>(h.rows);
@@ -262,10 +271,39 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
                                s), "hist copy");
       CUDA_TRY(cudaStreamSynchronize(s), "hist sync");
       int64_t Js = 0;
-      compute_relabel(h.J, h.sc_G * kScatterWarps, hist.data(), perm.data(), inv.data(), &Js);
+      compute_relabel(h.J, h.sc_G * h.sc_W, hist.data(), perm.data(), inv.data(), &Js);
       CUDA_TRY(cudaMemcpyAsync(h.perm, perm.data(), sizeof(int32_t) * (size_t)h.J, cudaMemcpyHostToDevice, s), "perm");
       CUDA_TRY(cudaMemcpyAsync(h.inv, inv.data(), sizeof(int32_t) * (size_t)h.Jl, cudaMemcpyHostToDevice, s), "inv");
       CUDA_TRY(cudaStreamSynchronize(s), "perm sync");
+    }
+    {  // g-stream layout: per-group run lengths (device) -> offsets and pass-B stage table (host)
+      const int G = h.sc_G;
+      int32_t* gcnt_dev = (int32_t*)h.layout_tmp;
+      launch_count_groups(h, gcnt_dev);
+      std::vector<int32_t> gcnt((size_t)G * (size_t)h.K);
+      std::vector<int64_t> gptr((size_t)G * (size_t)(h.K + 1));
+      if (h.K > 0)
+        CUDA_TRY(cudaMemcpyAsync(gcnt.data(), gcnt_dev, sizeof(int32_t) * gcnt.size(), cudaMemcpyDeviceToHost, s),
+                 "gcnt copy");
+      CUDA_TRY(cudaStreamSynchronize(s), "gcnt sync");
+      std::vector<int64_t> st_f, block_k;
+      std::vector<int32_t> st_k, cta_st;
+      plan_streams(h, gcnt.data(), gptr.data(), st_f, st_k, cta_st, block_k);
+      h.nst = (int64_t)st_k.size() / 2;
+      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F) {
+        delete H;
+        return fail(COPA_E_WORKSPACE, "internal: stage table exceeds its bound");
+      }
+      CUDA_TRY(cudaMemcpyAsync(h.gptr, gptr.data(), sizeof(int64_t) * gptr.size(), cudaMemcpyHostToDevice, s), "gptr");
+      if (h.nst > 0) {
+        CUDA_TRY(cudaMemcpyAsync(h.st_f, st_f.data(), sizeof(int64_t) * st_f.size(), cudaMemcpyHostToDevice, s), "st_f");
+        CUDA_TRY(cudaMemcpyAsync(h.st_k, st_k.data(), sizeof(int32_t) * st_k.size(), cudaMemcpyHostToDevice, s), "st_k");
+      }
+      CUDA_TRY(cudaMemcpyAsync(h.cta_st, cta_st.data(), sizeof(int32_t) * cta_st.size(), cudaMemcpyHostToDevice, s),
+               "cta_st");
+      CUDA_TRY(cudaMemcpyAsync(h.block_k, block_k.data(), sizeof(int64_t) * block_k.size(), cudaMemcpyHostToDevice, s),
+               "block_k");
+      CUDA_TRY(cudaStreamSynchronize(s), "layout sync");  // host vectors go out of scope
     }
     launch_basis(h);
     launch_build_fibers(h);

@@ -17,6 +17,7 @@ constexpr int kMaxDeg = 7;      // spline degree limit
 constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
 constexpr int kPhases = 11;       // timed phases of one outer iteration (copa_get_phase_times)
+constexpr int kMaxGroups = 8;     // label groups (fiber streams) of the smooth path
 
 enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
 
@@ -46,24 +47,32 @@ struct Handle {
   int64_t* srow;
   double *Pp, *Qt, *Nst;
   double* Bk;          // smooth: K x l x l basis coefficients (C_k = M_k B_k)
-  int64_t* fiber_ptr;  // smooth: [K+1]
-  int32_t* fiber_col;  // smooth: [F]
-  double* fiber_val;   // smooth: [F x l]
-  int32_t* row_patient;  // non-smooth: [rows]
-  // fiber-pass layout (smooth): relabeled features, pass A order, pass B patient ranges / label ranges
+  int64_t* fiber_ptr;  // smooth: [K+1] fibers per patient (prefix), all groups
+  int32_t* fiber_col;  // smooth: [Fcap] label of each fiber (g-stream layout, see k_fibers.cu)
+  double* fiber_val;   // smooth: [Fcap x l]
+  int64_t* gptr;       // smooth: [G x (K+1)] absolute offset of patient k's run in stream g
+  int64_t Fcap = 0;    // fiber slots incl. stream padding
+  // fiber-pass layout (smooth): relabeled features, pass A order, pass B CTAs and stage table
   int* counter;          // pass A work counter
   int32_t* order;        // [K] patients by fiber count, descending
   int32_t* perm;         // [J] feature -> label
   int32_t* inv;          // [Jl] label -> feature (-1: unused label)
-  uint16_t* woff;        // [K x G x 16] fiber offsets of the scatter warps' label ranges
-  int64_t* block_k;      // [sc_ranges+1] patient range of each scatter CTA pair/group
+  double* Vl;            // [Jl x R] V̄ in label order (pass A gathers when V̄ does not fit in smem)
+  int64_t* block_k;      // [sc_ranges+1] patient range of each pass-B range
   double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
   unsigned long long* fhist;  // [J] fibers per feature (init)
+  int64_t* st_f;         // [nst_cap x 2] pass-B stage: logical fiber range [f0, f1) in its stream
+  int32_t* st_k;         // [nst_cap x 2] pass-B stage: patient range [k0, k1)
+  int32_t* cta_st;       // [sc_ranges x G + 1] first stage of each pass-B CTA
+  int64_t nst = 0, nst_cap = 0;
   int64_t Jl = 0;        // labels = G * Jg >= J
-  int sc_G = 1, sc_CH = 32, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
+  int sc_G = 1, sc_W = 4, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
+  int sc_FB = 256, sc_PB = 16, sc_NS = 3;
   int64_t sc_Js = 0, sc_Jg = 0;
+  size_t sc_slot = 0, sc_smem = 0;
   void* layout_tmp;
   size_t layout_tmp_bytes = 0;
+  int32_t* row_patient;  // non-smooth: [rows]
   void* cub_temp;
   size_t cub_temp_bytes;
   int64_t* counts_scratch;
@@ -189,6 +198,7 @@ void launch_validate(Handle& h);
 void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/, unsigned long long* hist);
 void launch_basis(Handle& h);
 void launch_build_fibers(Handle& h);
+void launch_count_groups(Handle& h, int32_t* gcnt /*[G][K]*/);
 void launch_row_patient(Handle& h);
 void launch_sumsq(Handle& h, double* out);
 // iteration
@@ -209,9 +219,12 @@ int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
 void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int32_t* perm, int32_t* inv, int64_t* Js);
-constexpr int kScatterWarps = 8;
 size_t fiber_layout_temp_bytes(int64_t K);
-void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes);
+void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes);  // pass A order (device)
+int64_t stage_cap(const Handle& h);                                // pass-B stage table bound
+// host: gptr (G x (K+1), absolute) from per-group counts; stage table; pass-B patient ranges
+void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::vector<int64_t>& st_f,
+                  std::vector<int32_t>& st_k, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k);
 // wide per-patient dense kernels (k_dense.cu)
 bool polar_wide_ok(const Handle& h);
 int launch_polar_wide(Handle& h);

@@ -66,34 +66,55 @@ __device__ __forceinline__ void givens_insert_reg(double (&Rf)[L][L], double (&c
   }
 }
 
-// One-sided Jacobi on the rows of Wm (L x L, registers) until mutually orthogonal.
+// One-sided Jacobi on the rows of Wm (L x L, registers) until mutually orthogonal. Round-robin
+// (tournament) ordering: every round rotates floor(L/2) disjoint row pairs, whose dot products and
+// rotation parameters are independent (instruction-level parallelism in the thread-per-patient
+// layout); a sweep (L-1 or L rounds) meets every pair once. Rotation of rows x, y with a = x.x,
+// b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
+// sn = cs t; x <- cs x - sn y, y <- sn x + cs y (the classical zeta = d/c form, Hestenes).
 template <int L>
 __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
-  const double tol = 2.220446049250313e-16 * (double)L;
+  constexpr int N = (L % 2) ? L + 1 : L;  // players, with a dummy (index L) when L is odd
+  constexpr double eps = 2.220446049250313e-16 * (double)L;
+  constexpr double tol2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
 #pragma unroll
-    for (int p = 0; p < L - 1; ++p) {
+    for (int rd = 0; rd < N - 1; ++rd) {
+      double cs[N / 2], sn[N / 2];
 #pragma unroll
-      for (int q = p + 1; q < L; ++q) {
-        double a = 0.0, b = 0.0, c = 0.0;
+      for (int i = 0; i < N / 2; ++i) {
+        const int p = i == 0 ? 0 : 1 + (i - 1 + rd) % (N - 1);
+        const int q = 1 + (N - 2 - i + rd) % (N - 1);
+        cs[i] = 1.0;
+        sn[i] = 0.0;
+        if (p < L && q < L) {
+          double a = 0.0, b = 0.0, c = 0.0;
 #pragma unroll
-        for (int i = 0; i < L; ++i) {
-          a = fma(Wm[p][i], Wm[p][i], a);
-          b = fma(Wm[q][i], Wm[q][i], b);
-          c = fma(Wm[p][i], Wm[q][i], c);
+          for (int x = 0; x < L; ++x) {
+            a = fma(Wm[p][x], Wm[p][x], a);
+            b = fma(Wm[q][x], Wm[q][x], b);
+            c = fma(Wm[p][x], Wm[q][x], c);
+          }
+          if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+            rotated = 1;
+            const double d = 0.5 * (b - a);
+            const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
+            cs[i] = rsqrt(fma(t, t, 1.0));
+            sn[i] = cs[i] * t;
+          }
         }
-        if (a != 0.0 && b != 0.0 && fabs(c) > tol * sqrt(a * b)) {
-          rotated = 1;
-          const double zeta = (b - a) / (2.0 * c);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double cs = rsqrt(fma(t, t, 1.0));
-          const double sn = cs * t;
+      }
 #pragma unroll
-          for (int i = 0; i < L; ++i) {
-            const double x = Wm[p][i], y = Wm[q][i];
-            Wm[p][i] = fma(cs, x, -sn * y);
-            Wm[q][i] = fma(sn, x, cs * y);
+      for (int i = 0; i < N / 2; ++i) {
+        const int p = i == 0 ? 0 : 1 + (i - 1 + rd) % (N - 1);
+        const int q = 1 + (N - 2 - i + rd) % (N - 1);
+        if (p < L && q < L) {
+#pragma unroll
+          for (int x = 0; x < L; ++x) {
+            const double u = Wm[p][x], v = Wm[q][x];
+            Wm[p][x] = fma(cs[i], u, -sn[i] * v);
+            Wm[q][x] = fma(sn[i], u, cs[i] * v);
           }
         }
       }
@@ -103,46 +124,68 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
 }
 
 // Warp-cooperative A slab: slab[p][a][cc] = A_p(a, s = 8 nt + cc) for the round's patients.
-// A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps).
+// A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps). Rows a >= m_p of
+// P'_p are zero (never written), so only a < l is checked; the next patient's (P'S) fragments are
+// loaded while the current patient's MMAs run.
 template <int MT, int KS>
-__device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int R, const int32_t* m, const int64_t* srow,
-                                       const double* Pp, const double* W, const double* Hs, double* slab) {
+__device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, int R, const double* Pp,
+                                       const double* W, const double* Hs, double* slab) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  for (int p = 0; p < 32; ++p) {
-    const int64_t kp = base + p;
-    if (kp >= K) break;
-    const int mp = m[kp];
+  const int s = 8 * nt + g;
+  double hb[KS];
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int r = 4 * ks + t;
+    hb[ks] = (r < R && s < R) ? Hs[s * R + r] : 0.0;  // B[t][g] = H^T(r, s)
+  }
+  const int np = (int)(K - base < 32 ? K - base : 32);
+  auto load = [&](int64_t kp, double (&f)[KS][MT]) {
+    const double* P = Pp + kp * l * R;
+    const double* w = W + kp * R;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int r = 4 * ks + t;
+      const double wr = r < R ? w[r] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const int a = 8 * mt + g;
+        f[ks][mt] = (a < l && r < R) ? P[a * R + r] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+      }
+    }
+  };
+  double cur[KS][MT];
+  if (np > 0) load(base, cur);
+  for (int p = 0; p < np; ++p) {
+    double nxt[KS][MT];
+    if (p + 1 < np) load(base + p + 1, nxt);
     double c[MT][2];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
-    if (mp > 0) {
-      const double* P = Pp + srow[kp] * R;
-      const double* w = W + kp * R;
-      const int s = 8 * nt + g;
+    for (int mt = 0; mt < MT; ++mt) {
+      c[mt][0] = c[mt][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) {
-        const int r = 4 * ks + t;
-        const double b = (r < R && s < R) ? Hs[s * R + r] : 0.0;  // B[t][g] = H^T(r, s)
-        const double wr = r < R ? w[r] : 0.0;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int a = 8 * mt + g;
-          const double av = (a < mp && r < R) ? P[a * R + r] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
-          dmma2(c[mt][0], c[mt][1], av, b);
-        }
-      }
+      for (int ks = 0; ks < KS; ++ks) dmma2(c[mt][0], c[mt][1], cur[ks][mt], hb[ks]);
     }
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t] = c[mt][0];
       slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t + 1] = c[mt][1];
     }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) cur[ks][mt] = nxt[ks][mt];
   }
+  for (int p = np; p < 32; ++p)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t] = 0.0;
+      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t + 1] = 0.0;
+    }
 }
 
 template <int L, int MT, int NT>
-__global__ void __launch_bounds__(128) k_polar_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
-                                                    int64_t K, int R, const double* __restrict__ Pp,
+__global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
+                                                    int64_t K, int R, int l, const double* __restrict__ Pp,
                                                     const double* __restrict__ W, const double* __restrict__ Hg,
                                                     double tau, double* __restrict__ Qt, int32_t* __restrict__ rank,
                                                     double* __restrict__ FHpart) {
@@ -175,7 +218,7 @@ __global__ void __launch_bounds__(128) k_polar_wide(const int32_t* __restrict__ 
 #pragma unroll
       for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS>(nt, base, K, R, m, srow, Pp, W, Hs, slab);
+      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab);
       __syncwarp();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
@@ -212,7 +255,7 @@ __global__ void __launch_bounds__(128) k_polar_wide(const int32_t* __restrict__ 
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS>(nt, base, K, R, m, srow, Pp, W, Hs, slab);
+      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab);
       __syncwarp();
       if (kme < K && mme > 0) {
         double* Q = Qt + srow[kme] * R;
@@ -320,7 +363,7 @@ static void polar_wide_inst(Handle& h) {
   if (cap > kPartBlocks) cap = kPartBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt,
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt,
                                                          h.rank, h.partial);
   const int RR = h.R * h.R;
   k_sum_rr<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.FH);

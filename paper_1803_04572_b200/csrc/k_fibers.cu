@@ -1,24 +1,32 @@
 // k_fibers.cu — the two streaming passes over the projected fibers X'_k (smooth path), FP64 on
-// the tensor cores (mma.sync m8n8k4 f64 = SASS DMMA; 36.9 TFLOP/s measured, DESIGN.md §5).
+// the tensor cores (mma.sync m8n8k4 f64 = SASS DMMA; 36.9 TFLOP/s measured, DESIGN.md §4).
 //
-// Fiber (k, j): the l-vector x'_kj = X'_k(:, j) = C_k^T X_k(:, j). Fibers of a patient are
-// contiguous and sorted by the RELABELED feature id j' = perm[j]: features are dealt round-robin
-// by fiber mass into G x W equal-size label ranges, so every range carries about the same work.
+// Fiber (k, j): the l-vector x'_kj = X'_k(:, j) = C_k^T X_k(:, j).
 //
-// Pass A  P'_k = X'_k V(cols_k, :)  (m_k x R) — warp per patient, dynamic scheduling over patients
-//         sorted by fiber count, V staged (relabeled) in shared memory, fiber loads software-
-//         pipelined one 8-fiber tile ahead across patient boundaries.
+// g-stream layout. Features are relabeled by fiber mass and dealt into G x W equal-mass label
+// sub-ranges of Js labels each; label group g = sub-ranges [g W, (g+1) W) = labels [g Jg, (g+1) Jg).
+// Stream g holds, patient after patient, the fibers of that patient whose label is in group g,
+// sorted by label: patient k's run in stream g is [gptr[g][k], gptr[g][k+1]). Within a run, the
+// fibers of sub-range (g, w) are a contiguous sub-run.
+//
+// Pass A  P'_k = X'_k V(cols_k, :)  (m_k x R) — warp per patient (dynamic scheduling over patients
+//         sorted by fiber count), the patient's G runs one after the other, fiber tiles loaded one
+//         tile ahead, the next patient's runs bulk-prefetched into L2 (cp.async.bulk.prefetch.L2).
 //         MMA per 4 fibers: M = basis index a (8/tile), N = r (8/tile), K = fibers.
-// Pass B  F_V(j, :) += x'_kj^T N_k  (J x R) — CTA (range p, group g) owns the F_V rows of label group
-//         g in shared memory for patient range p; warp w owns label sub-range (g, w) so no two warps
-//         ever update the same row (no atomics). N_k of 32-patient chunks is staged into shared
-//         memory with cp.async (double buffer), the chunk metadata one chunk further ahead, so
-//         each warp prefetches its next fiber tile across patient and chunk boundaries.
-//         MMA per 8 fibers: M = fibers, N = r (8/tile), K = a (4/step). Per-CTA F_V partials are
-//         summed in a fixed order (deterministic) and un-relabeled.
+// Pass B  F_V(j, :) += x'_kj^T N_k  (J x R) — CTA = (patient range, label group g) owns the F_V rows
+//         of group g in shared memory. One producer warp streams the range's run of stream g in
+//         stages (<= FB fibers, <= PB patients) into an NS-deep shared-memory ring with 1-D TMA bulk
+//         copies (cp.async.bulk + mbarrier complete_tx): fiber labels, fiber values and the N_k rows
+//         of the stage's patients. W consumer warps: warp w owns label sub-range (g, w), so no two
+//         warps ever update the same F_V row (no atomics); it finds its sub-run of every patient of
+//         the stage with two warp ballots and runs MMA tiles of 8 fibers: M = fibers, N = r (8/tile),
+//         K = a (4/step). Per-CTA F_V partials are summed in a fixed order (deterministic) and
+//         un-relabeled.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <numeric>
 
 #include "copa_internal.cuh"
@@ -30,17 +38,51 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+
+// Bulk-prefetch [p, p + bytes) into L2 (16-byte aligned outward).
+__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
+  const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
+  const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+  if (e > a)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)(e - a)) : "memory");
 }
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+
+// ------------------------------------------------------------------ mbarrier / bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE%=;\n bra WAIT%=;\n"
+      "DONE%=:\n}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// Copy [src, src + bytes) with a 16-byte aligned bulk copy that starts at or before src; returns
+// the byte offset of src inside dst. dst must have 16 bytes of slack.
+__device__ __forceinline__ uint32_t bulk_g2s_span(void* dst, const void* src, size_t bytes, uint64_t* bar,
+                                                  uint32_t* tx) {
+  const uintptr_t a = (uintptr_t)src & ~(uintptr_t)15;
+  const uint32_t shift = (uint32_t)((uintptr_t)src - a);
+  const uint32_t nb = (uint32_t)((shift + bytes + 15) & ~(size_t)15);
+  if (nb) bulk_g2s(dst, (const void*)a, nb, bar);
+  *tx += nb;
+  return shift;
+}
 
 // ------------------------------------------------------------------ pass A
 template <int MT>
@@ -57,22 +99,23 @@ __device__ __forceinline__ void load_tile_a(TileA<MT>& T, int64_t fb, int64_t f1
   for (int s = 0; s < 2; ++s) {
     const int64_t f = fb + 4 * s + t;
     const bool ok = f < f1;
-    T.col[s] = ok ? fiber_col[f] : -1;
+    T.col[s] = ok ? __ldg(fiber_col + f) : -1;
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) {
       const int a = mt * 8 + g;
-      T.a[s][mt] = (ok && a < l) ? fiber_val[f * l + a] : 0.0;
+      T.a[s][mt] = (ok && a < l) ? __ldg(fiber_val + f * l + a) : 0.0;
     }
   }
 }
 
 template <int MT, int NT, bool VSMEM>
-__global__ void __launch_bounds__(512) k_spmm_mma(const int64_t* __restrict__ fiber_ptr,
+__global__ void __launch_bounds__(512) k_spmm_mma(const int64_t* __restrict__ gptr, int G,
                                                   const int32_t* __restrict__ fiber_col,
                                                   const double* __restrict__ fiber_val, const int32_t* __restrict__ m,
                                                   const int32_t* __restrict__ order, const int32_t* __restrict__ inv,
                                                   int64_t K, int l, int R, int64_t Jl, const double* __restrict__ Vg,
-                                                  double* __restrict__ Pp, int* counter) {
+                                                  const double* __restrict__ Vl, double* __restrict__ Pp,
+                                                  int* counter) {
   extern __shared__ double smem_v[];
   if (VSMEM) {
     for (int64_t x = threadIdx.x; x < Jl * R; x += blockDim.x) {
@@ -82,48 +125,58 @@ __global__ void __launch_bounds__(512) k_spmm_mma(const int64_t* __restrict__ fi
     }
     __syncthreads();
   }
+  const double* Vs = VSMEM ? smem_v : Vl;
   const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  // current patient and the one grabbed ahead
-  int idx = 0;
-  if (lane == 0) idx = atomicAdd(counter, 1);
-  idx = __shfl_sync(0xffffffffu, idx, 0);
-  int64_t k = idx < K ? order[idx] : -1;
-  int64_t f0 = k >= 0 ? fiber_ptr[k] : 0, f1 = k >= 0 ? fiber_ptr[k + 1] : 0;
-  TileA<MT> cur;
-  if (k >= 0) load_tile_a<MT>(cur, f0, f1, l, fiber_col, fiber_val);
+  const int64_t K1 = K + 1;
+  // lanes < G hold [start, end) of the current / next patient's run in stream `lane`
+  auto grab = [&](int64_t& kk, int64_t& s0, int64_t& s1) {
+    int idx = 0;
+    if (lane == 0) idx = atomicAdd(counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    kk = idx < K ? order[idx] : -1;
+    s0 = s1 = 0;
+    if (kk >= 0 && lane < G) {
+      s0 = gptr[lane * K1 + kk];
+      s1 = gptr[lane * K1 + kk + 1];
+      l2_prefetch(fiber_col + s0, sizeof(int32_t) * (size_t)(s1 - s0));
+      l2_prefetch(fiber_val + s0 * l, sizeof(double) * (size_t)((s1 - s0) * l));
+    }
+  };
+  int64_t k, c0, c1;
+  grab(k, c0, c1);
   while (k >= 0) {
-    int nidx = 0;
-    if (lane == 0) nidx = atomicAdd(counter, 1);
-    nidx = __shfl_sync(0xffffffffu, nidx, 0);
-    const int64_t kn = nidx < K ? order[nidx] : -1;
-    const int64_t g0 = kn >= 0 ? fiber_ptr[kn] : 0, g1 = kn >= 0 ? fiber_ptr[kn + 1] : 0;
+    int64_t kn, n0, n1;
+    grab(kn, n0, n1);
     double acc[MT][NT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    if (f0 >= f1 && kn >= 0) load_tile_a<MT>(cur, g0, g1, l, fiber_col, fiber_val);
-    for (int64_t fb = f0; fb < f1; fb += 8) {
-      // prefetch the next tile (this patient's or the next patient's first)
-      TileA<MT> nxt;
-      if (fb + 8 < f1) load_tile_a<MT>(nxt, fb + 8, f1, l, fiber_col, fiber_val);
-      else if (kn >= 0) load_tile_a<MT>(nxt, g0, g1, l, fiber_col, fiber_val);
+    for (int gg = 0; gg < G; ++gg) {
+      const int64_t f0 = __shfl_sync(0xffffffffu, c0, gg), f1 = __shfl_sync(0xffffffffu, c1, gg);
+      if (f0 >= f1) continue;
+      TileA<MT> cur;
+      load_tile_a<MT>(cur, f0, f1, l, fiber_col, fiber_val);
+      for (int64_t fb = f0; fb < f1; fb += 8) {
+        TileA<MT> nxt;
+        if (fb + 8 < f1) load_tile_a<MT>(nxt, fb + 8, f1, l, fiber_col, fiber_val);
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        double bfr[NT];
-        const int64_t j = cur.col[s];
+        for (int s = 0; s < 2; ++s) {
+          double bfr[NT];
+          const int64_t j = cur.col[s];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int r = nt * 8 + g;
-          bfr[nt] = (j >= 0 && r < R) ? (VSMEM ? smem_v[j * R + r] : Vg[(int64_t)inv[j] * R + r]) : 0.0;
+          for (int nt = 0; nt < NT; ++nt) {
+            const int r = nt * 8 + g;
+            bfr[nt] = (j >= 0 && r < R) ? (VSMEM ? Vs[j * R + r] : __ldg(Vs + j * R + r)) : 0.0;
+          }
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], cur.a[s][mt], bfr[nt]);
         }
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], cur.a[s][mt], bfr[nt]);
+        cur = nxt;
       }
-      cur = nxt;
     }
     const int mk = m[k];
     double* out = Pp + k * l * R;  // smooth state rows: srow[k] = k * l
@@ -139,9 +192,18 @@ __global__ void __launch_bounds__(512) k_spmm_mma(const int64_t* __restrict__ fi
         }
     }
     k = kn;
-    f0 = g0;
-    f1 = g1;
+    c0 = n0;
+    c1 = n1;
   }
+}
+
+// V̄ in label order for the global-gather variant of pass A.
+__global__ void k_relabel_V(const double* V, const int32_t* inv, int64_t Jl, int R, double* Vl) {
+  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= Jl * R) return;
+  const int64_t nj = x / R, r = x - nj * R;
+  const int32_t j = inv[nj];
+  Vl[x] = j >= 0 ? V[(int64_t)j * R + r] : 0.0;
 }
 
 template <int MT, int NT, bool VS>
@@ -155,15 +217,19 @@ static void spmm_inst(Handle& h, int smem_bytes) {
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, smem_bytes);
   if (per_sm < 1) per_sm = 1;
+  if (!VS) {
+    const int64_t n = h.Jl * h.R;
+    k_relabel_V<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.V, h.inv, h.Jl, h.R, h.Vl);
+  }
   cudaMemsetAsync(h.counter, 0, sizeof(int), h.stream);
-  fn<<<148 * per_sm, 512, smem_bytes, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.order, h.inv, h.K,
-                                                   h.l, h.R, h.Jl, h.V, h.Pp, h.counter);
+  fn<<<148 * per_sm, 512, smem_bytes, h.stream>>>(h.gptr, h.sc_G, h.fiber_col, h.fiber_val, h.m, h.order, h.inv,
+                                                   h.K, h.l, h.R, h.Jl, h.V, h.Vl, h.Pp, h.counter);
 }
 
 template <int MT, int NT>
 static void spmm_dispatch_v(Handle& h) {
   size_t vbytes = sizeof(double) * (size_t)(h.Jl * h.R);
-  if (vbytes <= 200 * 1024) spmm_inst<MT, NT, true>(h, (int)vbytes);
+  if (vbytes <= 200 * 1024 && !getenv("COPA_SPMM_VGLOBAL")) spmm_inst<MT, NT, true>(h, (int)vbytes);
   else spmm_inst<MT, NT, false>(h, 0);
 }
 
@@ -186,179 +252,177 @@ void launch_spmm_fibers(Handle& h) {
   else spmm_dispatch_n<2>(h);
 }
 
-// ------------------------------------------------------------------ pass B
-constexpr int kScW = 8;        // warps per scatter CTA = label sub-ranges per group
-constexpr int kWoffStride = 16;  // uint16 entries per (group, patient) row of woff (>= kScW + 1)
-
-struct MetaB {  // per chunk, in shared memory
-  int64_t f0[64];
-  int32_t m[64];
-  uint16_t wo[64][kWoffStride];
+// ------------------------------------------------------------------ pass B (TMA-staged scatter)
+// Stage slot layout (bytes, each part 16-byte aligned):
+//   meta  : int64 f0, f1; int32 k0, k1, shift_col, shift_val, shift_n, shift_gp   (48)
+//   gp    : int64 [PB + 1] + 16  run starts of the stage's patients in stream g (bulk copy, shifted)
+//   col   : int32 [FB] + 16  labels           (bulk copy, shifted)
+//   val   : f64 [FB l] + 16   fiber values     (bulk copy, shifted)
+//   nrows : f64 [PB l R] + 16 N_k rows         (bulk copy, shifted)
+struct SlotGeom {
+  uint32_t gp, col, val, nrows, bytes;
 };
+__host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~(uint64_t)15); }
+__host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
+  SlotGeom s;
+  s.gp = 48;
+  s.col = s.gp + al16(8ull * (PB + 1) + 16);
+  s.val = s.col + al16(4ull * FB + 16);
+  s.nrows = s.val + al16(8ull * FB * l + 16);
+  s.bytes = (s.nrows + al16(8ull * PB * l * R + 16) + 127) & ~127u;
+  return s;
+}
 
-template <int KS>
-struct TileB {
-  double a[KS];
-  int32_t col;   // label of the lane's fiber (-1: none)
-  int p;         // visit (patient index within its chunk), -1 = end
-  int chunk;     // chunk index (relative) of the visit: 0 = current, 1 = next
-  int64_t fb, fz;
-};
-
-template <int KS, int NT>
-__global__ void __launch_bounds__(32 * kScW) k_scatter_grp(
-    const int64_t* __restrict__ fiber_ptr, const int32_t* __restrict__ fiber_col,
-    const double* __restrict__ fiber_val, const int32_t* __restrict__ m, const uint16_t* __restrict__ woff,
-    const int64_t* __restrict__ range_k, int G, int64_t Jg, int l, int R, int RS, int CH,
+template <int KS, int NT, int W>
+__global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
+    const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
+    int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
+    const int32_t* __restrict__ cta_st, int l, int R, int RS, int FB, int PB, int NSt,
     const double* __restrict__ Nst, double* __restrict__ FVpart) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int g = lane >> 2, t = lane & 3;
   const int grp = blockIdx.x % G;
   const int64_t rng = blockIdx.x / G;
-  const int64_t k0 = range_k[rng], k1 = range_k[rng + 1];
-  const int64_t jbase = grp * Jg;
-  double* Fs = sm;                                       // Jg x RS
-  double* Nb = sm + Jg * RS;                             // [2][CH * l * R]
-  MetaB* mb = (MetaB*)(Nb + 2 * (int64_t)CH * l * R);    // [3]
-  const int64_t per = (int64_t)l * R;
+  const SlotGeom sg = slot_geom(FB, PB, l, R);
+  double* Fs = (double*)smraw;  // Jg x RS
+  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + 127) & ~127ull);
+  uint64_t* full = (uint64_t*)(smraw + fs_bytes);
+  uint64_t* empty = full + NSt;
+  unsigned char* slots = smraw + fs_bytes + ((2 * NSt * 8 + 127) & ~127);
   for (int64_t x = threadIdx.x; x < Jg * RS; x += blockDim.x) Fs[x] = 0.0;
-  const int64_t nch = (k1 - k0 + CH - 1) / CH;
-  auto stage_meta = [&](int64_t c) {
-    MetaB& M = mb[c % 3];
-    const int64_t kc = k0 + c * CH;
-    for (int i = threadIdx.x; i < CH; i += blockDim.x) {
-      const int64_t k = kc + i;
-      if (k < k1) {
-        cp_async8(&M.f0[i], fiber_ptr + k);
-        cp_async16(&M.wo[i][0], woff + (k * G + grp) * kWoffStride);
-        cp_async16(&M.wo[i][8], woff + (k * G + grp) * kWoffStride + 8);
-      }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSt; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, W);
     }
-    for (int i = threadIdx.x; i < CH; i += blockDim.x) {
-      const int64_t k = kc + i;
-      if (k < k1) {
-        // m as 4-byte copies (8-byte aligned pairs are not guaranteed)
-        unsigned s = (unsigned)__cvta_generic_to_shared(&M.m[i]);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(m + k));
-      }
-    }
-  };
-  auto stage_n = [&](int64_t c) {
-    double* dst = Nb + (c & 1) * (int64_t)CH * per;
-    const int64_t kc = k0 + c * CH;
-    const int64_t np = (kc + CH < k1 ? CH : k1 - kc) * per;
-    const double* src = Nst + kc * per;
-    for (int64_t x = threadIdx.x; x < np; x += blockDim.x) cp_async8(dst + x, src + x);
-  };
-  // prologue: group 0 = meta(0), group 1 = [N(0), meta(1)]
-  if (nch > 0) stage_meta(0);
-  cp_async_commit();
-  if (nch > 0) stage_n(0);
-  if (nch > 1) stage_meta(1);
-  cp_async_commit();
-  cp_async_wait<0>();
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
-
-  // the warp's tile iterator over (chunk, visit, tile)
-  auto first_visit = [&](int64_t c, int p_start, TileB<KS>& T) {
-    // find the first visit p >= p_start of chunk c with a non-empty range; T.p = -1 if none
-    const MetaB& M = mb[c % 3];
-    const int64_t kc = k0 + c * CH;
-    const int np = (int)(kc + CH < k1 ? CH : k1 - kc);
-    for (int p = p_start; p < np; ++p) {
-      const int64_t fa = M.f0[p] + M.wo[p][w], fz = M.f0[p] + M.wo[p][w + 1];
-      if (fa < fz) { T.p = p; T.fb = fa; T.fz = fz; return; }
+  const int s0 = cta_st[blockIdx.x], ns = cta_st[blockIdx.x + 1] - s0;
+  const int64_t K1 = K + 1;
+  if (w == W) {
+    // ---------------- producer (one lane)
+    if (lane == 0) {
+      // stage metadata is loaded one stage ahead so that its latency overlaps the ring wait
+      int64_t nf0 = 0, nf1 = 0;
+      int32_t nk0 = 0, nk1 = 0;
+      if (ns > 0) {
+        nf0 = st_f[2 * (int64_t)s0]; nf1 = st_f[2 * (int64_t)s0 + 1];
+        nk0 = st_k[2 * (int64_t)s0]; nk1 = st_k[2 * (int64_t)s0 + 1];
+      }
+      for (int i = 0; i < ns; ++i) {
+        const int slot = i % NSt, use = i / NSt;
+        const int64_t f0 = nf0, f1 = nf1;
+        const int32_t k0 = nk0, k1 = nk1;
+        if (i + 1 < ns) {
+          const int64_t st = s0 + i + 1;
+          nf0 = st_f[2 * st]; nf1 = st_f[2 * st + 1];
+          nk0 = st_k[2 * st]; nk1 = st_k[2 * st + 1];
+        }
+        mbar_wait(empty + slot, (use & 1) ^ 1);
+        unsigned char* base = slots + (size_t)slot * sg.bytes;
+        int64_t* meta = (int64_t*)base;
+        int32_t* mi = (int32_t*)(base + 16);
+        meta[0] = f0;
+        meta[1] = f1;
+        mi[0] = k0;
+        mi[1] = k1;
+        const uintptr_t sc = (uintptr_t)(fiber_col + f0), sv = (uintptr_t)(fiber_val + f0 * l),
+                        sn = (uintptr_t)(Nst + (int64_t)k0 * l * R), sp = (uintptr_t)(gptr + grp * K1 + k0);
+        const size_t bc = 4ull * (f1 - f0), bv = 8ull * (f1 - f0) * l, bn = 8ull * (k1 - k0) * l * R,
+                     bp = 8ull * (k1 - k0 + 1);
+        mi[2] = (int32_t)(sc & 15);
+        mi[3] = (int32_t)(sv & 15);
+        mi[4] = (int32_t)(sn & 15);
+        mi[5] = (int32_t)(sp & 15);
+        // expected bytes first (same rounding as bulk_g2s_span), then the copies
+        const uint32_t tx = al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn) + al16((sp & 15) + bp);
+        mbar_arrive_tx(full + slot, tx);
+        uint32_t t2 = 0;
+        bulk_g2s_span(base + sg.gp, (const void*)sp, bp, full + slot, &t2);
+        bulk_g2s_span(base + sg.col, (const void*)sc, bc, full + slot, &t2);
+        bulk_g2s_span(base + sg.val, (const void*)sv, bv, full + slot, &t2);
+        bulk_g2s_span(base + sg.nrows, (const void*)sn, bn, full + slot, &t2);
+      }
     }
-    T.p = -1;
-  };
-  auto load_b = [&](TileB<KS>& T) {
-    const int64_t f = T.fb + g;
-    const bool ok = f < T.fz;
-    T.col = ok ? fiber_col[f] : -1;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int a = 4 * ks + t;
-      T.a[ks] = (ok && a < l) ? fiber_val[f * l + a] : 0.0;
-    }
-  };
-  // next tile after T (same visit, later visit of the same chunk, or first visit of chunk c+1)
-  auto advance = [&](const TileB<KS>& T, int64_t c, TileB<KS>& N) {
-    if (T.fb + 8 < T.fz) { N = T; N.fb = T.fb + 8; load_b(N); return; }
-    int64_t cc = c + T.chunk;
-    first_visit(cc, T.p + 1, N);
-    N.chunk = T.chunk;
-    if (N.p < 0 && T.chunk == 0 && cc + 1 < nch) {
-      first_visit(cc + 1, 0, N);
-      N.chunk = 1;
-    }
-    if (N.p >= 0) load_b(N);
-  };
-
-  TileB<KS> cur;
-  cur.p = -1;
-  cur.chunk = 0;
-  for (int64_t c = 0; c < nch; ++c) {
-    // stage N(c+1) and meta(c+2); wait for N(c)/meta(c+1) (committed one group earlier)
-    if (c + 1 < nch) stage_n(c + 1);
-    if (c + 2 < nch) stage_meta(c + 2);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    if (cur.p < 0) {  // iterator ran dry (no prefetched tile): restart in this chunk
-      first_visit(c, 0, cur);
-      cur.chunk = 0;
-      if (cur.p >= 0) load_b(cur);
-    }
-    const double* Nc = Nb + (c & 1) * (int64_t)CH * per;
-    int curp = -1;
-    double bfr[KS][NT];
-    // process tiles belonging to chunk c (cur.chunk == 0)
-    while (cur.p >= 0 && cur.chunk == 0) {
-      if (cur.p != curp) {  // B fragments of the visit: B[t][g] = N(a = 4 ks + t, r = 8 nt + g)
-        curp = cur.p;
-        const MetaB& M = mb[c % 3];
-        const int mp = M.m[cur.p];
-        const double* Np = Nc + (int64_t)cur.p * per;
+  } else {
+    // ---------------- consumers: warp w owns labels [lw0, lw1) of group grp
+    const int g = lane >> 2, t = lane & 3;
+    const int32_t lw0 = (int32_t)(grp * Jg + (int64_t)w * Js), lw1 = (int32_t)(lw0 + Js);
+    const int64_t jbase = grp * Jg;
+    const int per = l * R;
+    for (int i = 0; i < ns; ++i) {
+      const int slot = i % NSt, use = i / NSt;
+      mbar_wait(full + slot, use & 1);
+      const unsigned char* base = slots + (size_t)slot * sg.bytes;
+      const int64_t f0 = ((const int64_t*)base)[0], f1 = ((const int64_t*)base)[1];
+      const int32_t* mi = (const int32_t*)(base + 16);
+      const int32_t k0 = mi[0], k1 = mi[1];
+      const int64_t* gp = (const int64_t*)(base + sg.gp + mi[5]);
+      const int32_t* colS = (const int32_t*)(base + sg.col + mi[2]);
+      const double* valS = (const double*)(base + sg.val + mi[3]);
+      const double* nS = (const double*)(base + sg.nrows + mi[4]);
+      for (int p = 0; p < k1 - k0; ++p) {
+        const int64_t a0 = max(gp[p], f0) - f0, a1 = min(gp[p + 1], f1) - f0;
+        if (a0 >= a1) continue;
+        // sub-run of labels [lw0, lw1) inside the (label-sorted) run [a0, a1)
+        int c0 = 0, c1 = 0;
+        for (int64_t x0 = a0; x0 < a1; x0 += 32) {
+          const int64_t x = x0 + lane;
+          const int32_t lab = x < a1 ? colS[x] : INT_MAX;
+          c0 += __popc(__ballot_sync(0xffffffffu, lab < lw0));
+          c1 += __popc(__ballot_sync(0xffffffffu, lab < lw1));
+        }
+        const int64_t lo = a0 + c0, hi = a0 + c1;
+        if (lo >= hi) continue;
+        // B fragments of this patient: B[t][g] = N(a = 4 ks + t, r = 8 nt + g)
+        const double* Np = nS + (int64_t)p * per;
+        double bfr[KS][NT];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             const int a = 4 * ks + t, r = 8 * nt + g;
-            bfr[ks][nt] = (a < mp && r < R) ? Np[a * R + r] : 0.0;
+            bfr[ks][nt] = (a < l && r < R) ? Np[a * R + r] : 0.0;
           }
-      }
-      TileB<KS> nxt;
-      advance(cur, c, nxt);
-      double cc[NT][2];
+        for (int64_t tb = lo; tb < hi; tb += 8) {
+          const int64_t f = tb + g;
+          const bool ok = f < hi;
+          const int32_t col = ok ? colS[f] : 0;
+          double av[KS];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        cc[nt][0] = cc[nt][1] = 0.0;
+          for (int ks = 0; ks < KS; ++ks) {
+            const int a = 4 * ks + t;
+            av[ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
+          }
+          double cc[NT][2];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) dmma(cc[nt][0], cc[nt][1], cur.a[ks], bfr[ks][nt]);
-      }
-      if (cur.col >= 0) {
-        double* row = Fs + (cur.col - jbase) * RS;
+          for (int nt = 0; nt < NT; ++nt) {
+            cc[nt][0] = cc[nt][1] = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int r = 8 * nt + 2 * t;
-          if (r < RS) {
-            double2 v = *reinterpret_cast<double2*>(row + r);
-            v.x += cc[nt][0];
-            v.y += cc[nt][1];
-            *reinterpret_cast<double2*>(row + r) = v;
+            for (int ks = 0; ks < KS; ++ks) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
+          }
+          if (ok) {
+            double* row = Fs + (col - jbase) * RS;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              const int r = 8 * nt + 2 * t;
+              if (r < RS) {
+                double2 v = *reinterpret_cast<double2*>(row + r);
+                v.x += cc[nt][0];
+                v.y += cc[nt][1];
+                *reinterpret_cast<double2*>(row + r) = v;
+              }
+            }
           }
         }
       }
-      cur = nxt;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + slot);
     }
-    // tiles of chunk c+1 already prefetched keep chunk = 1 -> becomes the current chunk
-    if (cur.p >= 0) cur.chunk = 0;
-    __syncthreads();  // everyone done with N(c) and meta(c) before they are overwritten
   }
-  cp_async_wait<0>();
   __syncthreads();
-  double* out = FVpart + rng * (G * Jg) * (int64_t)R + jbase * R;
+  double* out = FVpart + rng * (G * Jg) * (int64_t)R + (int64_t)grp * Jg * R;
   for (int64_t x = threadIdx.x; x < Jg * R; x += blockDim.x) {
     const int64_t jj = x / R, r = x - jj * R;
     out[x] = Fs[jj * RS + r];
@@ -378,24 +442,20 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-size_t scatter_smem_bytes(const Handle& h) {
-  return sizeof(double) * (size_t)(h.sc_Jg * h.sc_RS + 2 * (int64_t)h.sc_CH * h.l * h.R) + 3 * sizeof(MetaB);
-}
-
 template <int KS, int NT>
 static void scatter_inst(Handle& h) {
-  auto fn = k_scatter_grp<KS, NT>;
+  auto fn = k_scatter_tma<KS, NT, 4>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  const size_t smem = scatter_smem_bytes(h);
-  const int nr = h.sc_ranges;
-  fn<<<nr * h.sc_G, 32 * kScW, smem, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.woff, h.block_k,
-                                                   h.sc_G, h.sc_Jg, h.l, h.R, h.sc_RS, h.sc_CH, h.Nst, h.fv_part);
+  const int ctas = h.sc_ranges * h.sc_G;
+  fn<<<ctas, 32 * (h.sc_W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js,
+                                                         h.sc_Jg, h.st_f, h.st_k, h.cta_st, h.l, h.R, h.sc_RS,
+                                                         h.sc_FB, h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
   int64_t n = h.Jl * h.R;
-  k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, nr, h.Jl, h.R, h.inv, h.FV);
+  k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
 
 template <int KS>
@@ -422,80 +482,121 @@ int launch_scatter_fibers(Handle& h) {
   return 2;
 }
 
-// Chooses G (label groups), chunk size and label ranges so that a scatter CTA fits in shared memory.
+// Chooses the label groups G (F_V slice of a CTA), stage geometry and the number of pass-B patient
+// ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared memory.
 void plan_scatter(Handle& h) {
-  const size_t budget = 220 * 1024;
+  const size_t budget = 225 * 1024;
+  h.sc_W = 4;  // consumer warps per CTA (template parameter of k_scatter_tma)
   h.sc_RS = (h.R + 1) & ~1;
+  h.sc_FB = 256;
   h.sc_ok = 0;
-  for (int G = 1; G <= 8 && !h.sc_ok; ++G) {
-    const int64_t Js = (h.J + (int64_t)G * kScW - 1) / ((int64_t)G * kScW);
-    const int64_t Jg = Js * kScW;
-    for (int CH = 64; CH >= 8; CH /= 2) {
-      size_t bytes = sizeof(double) * (size_t)(Jg * h.sc_RS + 2 * (int64_t)CH * h.l * h.R) + 3 * sizeof(MetaB);
-      if (bytes <= budget) {
-        h.sc_G = G;
-        h.sc_Js = Js;
-        h.sc_Jg = Jg;
-        h.sc_CH = CH;
-        h.sc_ok = 1;
-        break;
+  const int pbs[3] = {16, 8, 4};
+  for (int G = 1; G <= kMaxGroups && !h.sc_ok; ++G) {
+    const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
+    const int64_t Jg = Js * h.sc_W;
+    const size_t fs = ((size_t)Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
+    for (int NSt = 4; NSt >= 2 && !h.sc_ok; --NSt)
+      for (int pi = 0; pi < 3 && !h.sc_ok; ++pi) {
+        const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
+        const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
+        if (bytes <= budget && (NSt >= 3 || pi == 2)) {
+          h.sc_G = G;
+          h.sc_Js = Js;
+          h.sc_Jg = Jg;
+          h.sc_PB = pbs[pi];
+          h.sc_NS = NSt;
+          h.sc_slot = sg.bytes;
+          h.sc_smem = bytes;
+          h.sc_ok = 1;
+        }
       }
-    }
   }
-  if (!h.sc_ok) {  // fall back: one label range per group of 1 (atomic scatter path handles it)
-    h.sc_G = 1;
-    h.sc_Js = (h.J + kScW - 1) / kScW;
-    h.sc_Jg = h.sc_Js * kScW;
-    h.sc_CH = 8;
+  if (!h.sc_ok) {  // F_V does not fit even split 8 ways: global-atomic fallback (k_iter.cu)
+    h.sc_G = kMaxGroups;
+    h.sc_Js = (h.J + (int64_t)h.sc_G * h.sc_W - 1) / ((int64_t)h.sc_G * h.sc_W);
+    h.sc_Jg = h.sc_Js * h.sc_W;
   }
   h.Jl = (int64_t)h.sc_G * h.sc_Jg;
-  int64_t ranges = (148 + h.sc_G - 1) / h.sc_G;
+  int bps = h.sc_ok ? (int)((228 * 1024) / (h.sc_smem + 1024)) : 1;
+  if (bps < 1) bps = 1;
+  int64_t ranges = (148 * (int64_t)bps + h.sc_G - 1) / h.sc_G;
   if (ranges > h.K) ranges = h.K > 0 ? h.K : 1;
   h.sc_ranges = (int)ranges;
 }
 
 bool scatter_smem_ok(const Handle& h) { return h.sc_ok != 0; }
 
-// ------------------------------------------------------------------ init-time layout for the passes
+int64_t stage_cap(const Handle& h) {
+  return h.F / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
+}
+
+// Host planning from the per-group run lengths gcnt[g][k]: stream offsets gptr (absolute), pass-B
+// patient ranges (balanced by fibers) and the stage table of every (range, group) CTA.
+void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int64_t>& st_f, std::vector<int32_t>& st_k,
+                  std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k) {
+  const int G = h.sc_G;
+  const int64_t K = h.K, K1 = K + 1;
+  int64_t base = 0;
+  for (int g = 0; g < G; ++g) {
+    int64_t* gp = gptr + g * K1;
+    gp[0] = base;
+    for (int64_t k = 0; k < K; ++k) gp[k + 1] = gp[k] + gcnt[g * K + k];
+    base = gp[K];
+  }
+  // balanced patient ranges by total fibers
+  const int nr = h.sc_ranges;
+  block_k.assign((size_t)nr + 1, 0);
+  std::vector<int64_t> tot((size_t)K1, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    int64_t c = 0;
+    for (int g = 0; g < G; ++g) c += gcnt[g * K + k];
+    tot[(size_t)k + 1] = tot[(size_t)k] + c;
+  }
+  for (int b = 0; b <= nr; ++b) {
+    if (b == nr) { block_k[(size_t)b] = K; break; }
+    const int64_t target = (tot[(size_t)K] * b) / nr;
+    block_k[(size_t)b] = std::lower_bound(tot.begin(), tot.end(), target) - tot.begin();
+    if (block_k[(size_t)b] > K) block_k[(size_t)b] = K;
+  }
+  st_f.clear();
+  st_k.clear();
+  cta_st.assign((size_t)nr * G + 1, 0);
+  const int64_t FB = h.sc_FB, PB = h.sc_PB;
+  for (int r = 0; r < nr; ++r)
+    for (int g = 0; g < G; ++g) {
+      cta_st[(size_t)r * G + g] = (int32_t)(st_k.size() / 2);
+      const int64_t* gp = gptr + g * K1;
+      const int64_t kr0 = block_k[(size_t)r], kr1 = block_k[(size_t)r + 1];
+      if (kr0 >= kr1) continue;
+      int64_t f = gp[kr0];
+      const int64_t fend = gp[kr1];
+      int64_t k = kr0;
+      while (f < fend) {
+        while (gp[k + 1] <= f) ++k;  // first patient whose run ends after f
+        int64_t f1 = std::min(f + FB, fend);
+        int64_t kk = k + 1;
+        while (kk < kr1 && gp[kk] < f1) ++kk;
+        if (kk - k > PB) {
+          kk = k + PB;
+          f1 = gp[kk];
+        }
+        st_f.push_back(f);
+        st_f.push_back(f1);
+        st_k.push_back((int32_t)k);
+        st_k.push_back((int32_t)kk);
+        f = f1;
+        k = kk - 1;
+      }
+    }
+  cta_st[(size_t)nr * G] = (int32_t)(st_k.size() / 2);
+}
+
+// ------------------------------------------------------------------ init-time layout for pass A
 __global__ void k_fiber_counts(const int64_t* fiber_ptr, int64_t K, int32_t* cnt, int32_t* idx) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
   cnt[k] = (int32_t)(fiber_ptr[k + 1] - fiber_ptr[k]);
   idx[k] = (int32_t)k;
-}
-
-// woff[(k G + grp) 16 + w] = lower_bound(label (grp W + w) * Js) within the patient's sorted labels
-__global__ void k_warp_offsets(const int64_t* fiber_ptr, const int32_t* fiber_col, int64_t K, int G, int64_t Js,
-                               uint16_t* woff) {
-  int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int per = G * (kScW + 1);
-  if (x >= K * per) return;
-  int64_t k = x / per;
-  int rem = (int)(x - k * per);
-  int grp = rem / (kScW + 1), w = rem - grp * (kScW + 1);
-  int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
-  int64_t key = ((int64_t)grp * kScW + w) * Js;
-  int64_t lo = f0, hi = f1;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (fiber_col[mid] < key) lo = mid + 1; else hi = mid;
-  }
-  woff[(k * G + grp) * kWoffStride + w] = (uint16_t)(lo - f0);
-}
-
-// range_k[b] = first patient whose fiber start >= b F / nb (balanced patient ranges)
-__global__ void k_block_ranges(const int64_t* fiber_ptr, int64_t K, int nb, int64_t* block_k) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b > nb) return;
-  if (b == nb) { block_k[nb] = K; return; }
-  int64_t F = fiber_ptr[K];
-  int64_t target = (F * b) / nb;
-  int64_t lo = 0, hi = K;
-  while (lo < hi) {
-    int64_t mid = (lo + hi) >> 1;
-    if (fiber_ptr[mid] < target) lo = mid + 1; else hi = mid;
-  }
-  block_k[b] = lo;
 }
 
 size_t fiber_layout_temp_bytes(int64_t K) {
@@ -506,8 +607,8 @@ size_t fiber_layout_temp_bytes(int64_t K) {
 }
 
 // Feature relabeling from the per-feature fiber counts: features sorted by count (descending,
-// ties by id) are dealt round-robin over the G*W label ranges of Js labels each; perm[j] = new label,
-// inv[new] = j. Host-side (J <= 65535).
+// ties by id) are dealt serpentine over the G*W label sub-ranges of Js labels each; perm[j] = new
+// label, inv[new] = j. Host-side (J <= 65535).
 void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int32_t* perm, int32_t* inv, int64_t* Js) {
   std::vector<int32_t> idx((size_t)J);
   std::iota(idx.begin(), idx.end(), 0);
@@ -527,8 +628,9 @@ void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int3
   *Js = js;
 }
 
-// Builds order (pass A), woff / range_k (pass B). tmp: >= fiber_layout_temp_bytes(K) + 12 K bytes.
+// Pass A patient order (by fiber count, descending). tmp: >= fiber_layout_temp_bytes(K) + 12 K bytes.
 void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes) {
+  (void)tmp_bytes;
   cudaStream_t s = h.stream;
   char* p = (char*)tmp;
   auto take = [&](size_t n) { char* r = p; p += (n + 255) & ~(size_t)255; return (void*)r; };
@@ -540,11 +642,7 @@ void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes) {
   if (h.K > 0) {
     k_fiber_counts<<<(unsigned)((h.K + 255) / 256), 256, 0, s>>>(h.fiber_ptr, h.K, cnt, idx);
     cub::DeviceRadixSort::SortPairsDescending(sort_tmp, sort_bytes, cnt, cnt_sorted, idx, h.order, (int)h.K, 0, 32, s);
-    int64_t n = h.K * h.sc_G * (kScW + 1);
-    k_warp_offsets<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(h.fiber_ptr, h.fiber_col, h.K, h.sc_G, h.sc_Js,
-                                                               h.woff);
   }
-  k_block_ranges<<<(h.sc_ranges + 1 + 255) / 256, 256, 0, s>>>(h.fiber_ptr, h.K, h.sc_ranges, h.block_k);
 }
 
 }  // namespace copa

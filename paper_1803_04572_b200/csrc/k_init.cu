@@ -170,66 +170,124 @@ void launch_basis(Handle& h) {
                                                           h.o.basis_tol, h.Bk, h.m);
 }
 
+// ------------------------------------------------------------------ fibers: per-group counts
+// Patient bitmap over the relabeled feature ids (labels); the fibers of group g are the distinct
+// labels in [g Jg, (g+1) Jg). rank(x) = number of the patient's labels below x.
+__device__ __forceinline__ void patient_label_bitmap(const int64_t* prp, const int64_t* rp, const int32_t* col,
+                                                     const int32_t* perm, int64_t k, int words, unsigned* bits,
+                                                     int* pref) {
+  const int lane = threadIdx.x & 31;
+  for (int w = lane; w < words; w += 32) bits[w] = 0u;
+  __syncwarp();
+  const int64_t e0 = rp[prp[k]], e1 = rp[prp[k + 1]];
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const int32_t j = perm[col[e]];
+    atomicOr(&bits[j >> 5], 1u << (j & 31));
+  }
+  __syncwarp();
+  // exclusive prefix of popcounts over words (warp-strided chunks)
+  int carry = 0;
+  for (int w0 = 0; w0 < words; w0 += 32) {
+    const int w = w0 + lane;
+    const int c = w < words ? __popc(bits[w]) : 0;
+    int inc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (w < words) pref[w] = carry + inc - c;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ int label_rank(const unsigned* bits, const int* pref, int words, int64_t x) {
+  const int64_t w = x >> 5;
+  if (w >= words) return pref[words - 1] + __popc(bits[words - 1]);
+  return pref[w] + __popc(bits[w] & ((1u << (x & 31)) - 1u));
+}
+
+__global__ void k_count_groups(const int64_t* prp, const int64_t* rp, const int32_t* col, const int32_t* perm,
+                               int64_t K, int words, int G, int64_t Jg, int32_t* gcnt /*[G][K]*/) {
+  extern __shared__ unsigned smem_g[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  unsigned* bits = smem_g + wib * words;
+  int* pref = (int*)(smem_g + nw * words) + wib * words;
+  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  for (int64_t k = blockIdx.x * (int64_t)nw + wib; k < K; k += nwarps) {
+    patient_label_bitmap(prp, rp, col, perm, k, words, bits, pref);
+    if (lane < G) {
+      const int a = label_rank(bits, pref, words, lane * Jg);
+      const int b = label_rank(bits, pref, words, (lane + 1) * Jg);
+      gcnt[(int64_t)lane * K + k] = b - a;
+    }
+    __syncwarp();
+  }
+}
+
+void launch_count_groups(Handle& h, int32_t* gcnt) {
+  if (h.K == 0) return;
+  const int words = (int)((h.Jl + 31) / 32);
+  const int warps = 8;
+  const size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_count_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  int64_t blocks = (h.K + warps - 1) / warps;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_count_groups<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.perm,
+                                                                    h.K, words, h.sc_G, h.sc_Jg, gcnt);
+}
+
 // ------------------------------------------------------------------ fibers: build X'_k = C_k^T X_k
-// Warp per patient. Fibers of a patient are its distinct columns in ascending order. Rows are
-// processed in order; within a row the lanes own distinct nonzeros (distinct columns => distinct
-// fibers), so the accumulation is race-free and its order (ascending row) deterministic.
+// Warp per patient. The fibers of a patient are its distinct labels; the fiber with label j goes to
+// stream g = j / Jg at gptr[g][k] + (rank(j) - rank(g Jg)), so every stream is sorted by label within
+// each patient. Rows are processed in order; within a row the lanes own distinct nonzeros (distinct
+// columns => distinct fibers), so the accumulation is race-free and its order (ascending row)
+// deterministic.
 __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int32_t* col, const double* val,
                                const double* times, int64_t K, int words, int l, int d, const double* Bk,
-                               const int32_t* m, const int64_t* fiber_ptr, const int32_t* perm, int32_t* fiber_col,
-                               double* fiber_val) {
+                               const int32_t* m, const int64_t* gptr, int G, int64_t Jg, const int32_t* perm,
+                               int32_t* fiber_col, double* fiber_val) {
   extern __shared__ unsigned smem_b[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   unsigned* bits = smem_b + wib * words;
   int* pref = (int*)(smem_b + nw * words) + wib * words;
   const int64_t nwarps = (int64_t)gridDim.x * nw;
+  const int64_t K1 = K + 1;
   for (int64_t k = blockIdx.x * (int64_t)nw + wib; k < K; k += nwarps) {
-    for (int w = lane; w < words; w += 32) bits[w] = 0u;
-    __syncwarp();
-    int64_t r0 = prp[k], r1 = prp[k + 1];
-    int64_t e0 = rp[r0], e1 = rp[r1];
-    for (int64_t e = e0 + lane; e < e1; e += 32) {
-      int32_t j = perm[col[e]];  // relabeled feature id (fibers sorted by the new label)
-      atomicOr(&bits[j >> 5], 1u << (j & 31));
-    }
-    __syncwarp();
-    // exclusive prefix of popcounts over words (warp-strided chunks)
-    int carry = 0;
-    for (int w0 = 0; w0 < words; w0 += 32) {
-      int w = w0 + lane;
-      int c = w < words ? __popc(bits[w]) : 0;
-      int inc = c;
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-      }
-      if (w < words) pref[w] = carry + inc - c;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    __syncwarp();
-    const int64_t f0 = fiber_ptr[k];
-    const int nf = (int)(fiber_ptr[k + 1] - f0);
+    patient_label_bitmap(prp, rp, col, perm, k, words, bits, pref);
+    // per-group destination offset: dst(j) = gptr[g][k] - rank(g Jg) + rank(j)
+    int64_t gdst[kMaxGroups];
+#pragma unroll
+    for (int g = 0; g < kMaxGroups; ++g)
+      gdst[g] = g < G ? gptr[g * K1 + k] - label_rank(bits, pref, words, g * Jg) : 0;
     for (int w = lane; w < words; w += 32) {
       unsigned b = bits[w];
-      int base = pref[w];
+      int rk = pref[w];
       while (b) {
-        int bit = __ffs(b) - 1;
+        const int bit = __ffs(b) - 1;
         b &= b - 1;
-        fiber_col[f0 + base] = w * 32 + bit;
-        ++base;
+        const int64_t j = (int64_t)w * 32 + bit;
+        const int g = (int)(j / Jg);
+        const int64_t dst = gdst[g] + rk;
+        fiber_col[dst] = (int32_t)j;
+        for (int a = 0; a < l; ++a) fiber_val[dst * l + a] = 0.0;
+        ++rk;
       }
     }
-    double* fv = fiber_val + f0 * l;
-    for (int64_t x = lane; x < (int64_t)nf * l; x += 32) fv[x] = 0.0;
     __syncwarp();
     const int mk = m[k];
     const double* B = Bk + k * (int64_t)l * l;
-    double t1 = times[r0], tn = times[r1 - 1];
+    const int64_t r0 = prp[k], r1 = prp[k + 1];
+    const double t1 = times[r0], tn = times[r1 - 1];
     if (mk > 0) {
       for (int64_t i = r0; i < r1; ++i) {
         double N[kMaxDeg + 1];
-        int mu = spline_eval(times[i], t1, tn, l, d, N);
+        const int mu = spline_eval(times[i], t1, tn, l, d, N);
         double c[kMaxL];  // C_k(i, :) = M_k(i, :) B_k
         for (int a = 0; a < mk; ++a) {
           double s = 0.0;
@@ -237,10 +295,10 @@ __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int3
           c[a] = s;
         }
         for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
-          int32_t j = perm[col[e]];
-          double x = val[e];
-          int f = pref[j >> 5] + __popc(bits[j >> 5] & ((1u << (j & 31)) - 1u));
-          double* dst = fv + (int64_t)f * l;
+          const int32_t j = perm[col[e]];
+          const double x = val[e];
+          const int g = (int)(j / Jg);
+          double* dst = fiber_val + (gdst[g] + label_rank(bits, pref, words, j)) * l;
           for (int a = 0; a < mk; ++a) dst[a] = fma(x, c[a], dst[a]);
         }
         __syncwarp();
@@ -252,14 +310,19 @@ __global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int3
 
 void launch_build_fibers(Handle& h) {
   if (h.K == 0) return;
-  int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
-  int warps = 8;
-  size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
+  const int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
+  const int warps = 8;
+  const size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_build_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
   int64_t blocks = (h.K + warps - 1) / warps;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_build_fibers<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(
-      h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m,
-      h.fiber_ptr, h.perm, h.fiber_col, h.fiber_val);
+      h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m, h.gptr,
+      h.sc_G, h.sc_Jg, h.perm, h.fiber_col, h.fiber_val);
 }
 
 // ------------------------------------------------------------------ non-smooth helpers

@@ -390,7 +390,8 @@ int launch_passB1(Handle& h) {
 }
 
 // ------------------------------------------------------------------ pass B2: F_V scatter
-__global__ void k_scatter_fibers(const int64_t* fiber_ptr, const int32_t* fiber_col, const double* fiber_val,
+// Fallback when no F_V slice fits in shared memory: warp per patient, FP64 global atomics.
+__global__ void k_scatter_fibers(const int64_t* gptr, int G, const int32_t* fiber_col, const double* fiber_val,
                                  const int32_t* m, const int64_t* srow, int64_t K, int l, int R, const double* Nst,
                                  const int32_t* inv, double* FV) {
   const int lane = threadIdx.x & 31;
@@ -404,8 +405,8 @@ __global__ void k_scatter_fibers(const int64_t* fiber_ptr, const int32_t* fiber_
       n0[a] = (a < mk && r0 < R) ? N[a * R + r0] : 0.0;
       n1[a] = (a < mk && r1 < R) ? N[a * R + r1] : 0.0;
     }
-    const int64_t f0 = fiber_ptr[k], f1 = fiber_ptr[k + 1];
-    for (int64_t f = f0; f < f1; ++f) {
+    for (int g = 0; g < G; ++g)
+    for (int64_t f = gptr[g * (K + 1) + k]; f < gptr[g * (K + 1) + k + 1]; ++f) {
       const int64_t j = inv[fiber_col[f]];  // fibers carry relabeled feature ids
       const double* xv = fiber_val + f * l;
       double s0 = 0.0, s1 = 0.0;
@@ -439,7 +440,7 @@ int launch_scatter(Handle& h) {
   } else if (h.smooth) {
     int64_t blocks = (h.K + 7) / 8;
     if (blocks > 148 * 32) blocks = 148 * 32;
-    k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.fiber_ptr, h.fiber_col, h.fiber_val, h.m, h.srow,
+    k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.gptr, h.sc_G, h.fiber_col, h.fiber_val, h.m, h.srow,
                                                              h.K, h.l, h.R, h.Nst, h.inv, h.FV);
   } else {
     int64_t n = h.rows * h.R;
