@@ -56,6 +56,7 @@ size_t carve(Handle& h, char* base) {
   h.HtH = c.take<double>(RR);
   h.VtV = c.take<double>(RR);
   h.LW = c.take<double>(RR);
+  h.GWi = c.take<double>(RR);
   h.comm2 = c.take<double>(h.J * R + 2 * RR);
   if (base) { h.FV = h.comm2; h.WtW = h.comm2 + h.J * R; h.M = h.WtW + RR; }
   h.V = c.take<double>(h.J * R);
@@ -69,6 +70,10 @@ size_t carve(Handle& h, char* base) {
   h.Qt = c.take<double>(h.S * R + 4);
   h.Nst = c.take<double>(h.S * R + 4);
   h.partial = c.take<double>(2 * (int64_t)kPartBlocks * RR);
+  {
+    const int64_t RP = 8 * ((R + 7) / 8);
+    h.fh_warp = c.take<double>(h.smooth ? (int64_t)kPartBlocks * 4 * RP * RP : 1);
+  }
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   if (h.smooth) {
     const int G = h.sc_G;
@@ -87,6 +92,7 @@ size_t carve(Handle& h, char* base) {
     h.block_k = c.take<int64_t>(h.sc_ranges + 1);
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
+    h.woff = c.take<uint16_t>((int64_t)G * h.K * kWoS + 16);
     h.nst_cap = stage_cap(h);
     h.st_f = c.take<int64_t>(2 * h.nst_cap);
     h.st_k = c.take<int32_t>(2 * h.nst_cap);

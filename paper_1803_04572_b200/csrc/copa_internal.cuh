@@ -18,6 +18,7 @@ constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
 constexpr int kPhases = 11;       // timed phases of one outer iteration (copa_get_phase_times)
 constexpr int kMaxGroups = 8;     // label groups (fiber streams) of the smooth path
+constexpr int kWoS = 16;          // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
 
 enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
 
@@ -38,7 +39,8 @@ struct Handle {
   // workspace segments (device)
   int* err;
   double* scal;
-  double *H, *DH, *FH, *HtH, *VtV, *LW, *partial;
+  double *H, *DH, *FH, *HtH, *VtV, *LW, *GWi, *partial;  // GWi = (G_W + rho I)^-1
+  double* fh_warp;     // smooth: per-warp F_H partials of the polar kernel [kPartBlocks x 4 x (8 ceil(R/8))^2]
   double *comm2;       // [FV (J R) | WtW (R R) | M (R R)]
   double *FV, *WtW, *M;
   double *V, *DV;
@@ -61,6 +63,7 @@ struct Handle {
   int64_t* block_k;      // [sc_ranges+1] patient range of each pass-B range
   double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
   unsigned long long* fhist;  // [J] fibers per feature (init)
+  uint16_t* woff;        // [G x K x kWoS] label sub-run offsets inside each patient's group run
   int64_t* st_f;         // [nst_cap x 2] pass-B stage: logical fiber range [f0, f1) in its stream
   int32_t* st_k;         // [nst_cap x 2] pass-B stage: patient range [k0, k1)
   int32_t* cta_st;       // [sc_ranges x G + 1] first stage of each pass-B CTA

@@ -133,43 +133,48 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int s = 8 * nt + g;
   double hb[KS];
+  int offp[KS][MT];  // lane's fragment offsets inside a patient's P' block (-1: outside)
+  int offw[KS];
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
     const int r = 4 * ks + t;
     hb[ks] = (r < R && s < R) ? Hs[s * R + r] : 0.0;  // B[t][g] = H^T(r, s)
+    offw[ks] = r < R ? r : -1;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int a = 8 * mt + g;
+      offp[ks][mt] = (a < l && r < R) ? a * R + r : -1;
+    }
   }
   const int np = (int)(K - base < 32 ? K - base : 32);
-  auto load = [&](int64_t kp, double (&f)[KS][MT]) {
-    const double* P = Pp + kp * l * R;
-    const double* w = W + kp * R;
+  const int64_t pstride = (int64_t)l * R;
+  const double* P = Pp + base * pstride;
+  const double* w = W + base * R;
+  auto load = [&](const double* Pk, const double* wk, double (&f)[KS][MT]) {
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      const int r = 4 * ks + t;
-      const double wr = r < R ? w[r] : 0.0;
+      const double wr = offw[ks] >= 0 ? wk[offw[ks]] : 0.0;
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int a = 8 * mt + g;
-        f[ks][mt] = (a < l && r < R) ? P[a * R + r] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
-      }
+      for (int mt = 0; mt < MT; ++mt) f[ks][mt] = offp[ks][mt] >= 0 ? Pk[offp[ks][mt]] * wr : 0.0;
     }
   };
   double cur[KS][MT];
-  if (np > 0) load(base, cur);
+  if (np > 0) load(P, w, cur);
   for (int p = 0; p < np; ++p) {
     double nxt[KS][MT];
-    if (p + 1 < np) load(base + p + 1, nxt);
+    P += pstride;
+    w += R;
+    if (p + 1 < np) load(P, w, nxt);
     double c[MT][2];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      c[mt][0] = c[mt][1] = 0.0;
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < KS; ++ks) dmma2(c[mt][0], c[mt][1], cur[ks][mt], hb[ks]);
-    }
+    for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t] = c[mt][0];
-      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t + 1] = c[mt][1];
-    }
+      for (int mt = 0; mt < MT; ++mt) dmma2(c[mt][0], c[mt][1], cur[ks][mt], hb[ks]);
+    double* sp = slab + (p * MT * 8 + g) * 8 + 2 * t;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) *reinterpret_cast<double2*>(sp + mt * 64) = make_double2(c[mt][0], c[mt][1]);
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
@@ -177,19 +182,20 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
   }
   for (int p = np; p < 32; ++p)
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t] = 0.0;
-      slab[(p * MT * 8 + 8 * mt + g) * 8 + 2 * t + 1] = 0.0;
-    }
+    for (int mt = 0; mt < MT; ++mt)
+      *reinterpret_cast<double2*>(slab + (p * MT * 8 + 8 * mt + g) * 8 + 2 * t) = make_double2(0.0, 0.0);
 }
 
-template <int L, int MT, int NT>
-__global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
-                                                    int64_t K, int R, int l, const double* __restrict__ Pp,
-                                                    const double* __restrict__ W, const double* __restrict__ Hg,
-                                                    double tau, double* __restrict__ Qt, int32_t* __restrict__ rank,
-                                                    double* __restrict__ FHpart) {
+template <int L, int MT, int NT, int RT, int LT>
+__global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict__ m, int64_t K, int R_, int l_,
+                                                       const double* __restrict__ Pp, const double* __restrict__ W,
+                                                       const double* __restrict__ Hg, double tau,
+                                                       double* __restrict__ Qt, int32_t* __restrict__ rank,
+                                                       double* __restrict__ FHwarp) {
   constexpr int KS = (NT * 8 + 3) / 4;  // r steps of 4 covering 8 NT >= R
+  constexpr int RP = 8 * NT;
+  const int R = RT ? RT : R_;           // compile-time for the configured (R, l) pairs
+  const int l = LT ? LT : l_;
   extern __shared__ double sm[];
   const int hoff = ((R * R + 31) / 32) * 32;
   double* Hs = sm;                                      // R x R
@@ -200,15 +206,24 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int nwarps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t rounds = (K + 31) / 32;
-  double fh[NT][NT][2];
+  const int64_t pstride = (int64_t)l * R;
+  // this warp's F_H partial (RP x RP, MMA fragment order), accumulated round by round
+  double* fhw = FHwarp + ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * (RP * RP) + lane;
 #pragma unroll
-  for (int a = 0; a < NT; ++a)
-#pragma unroll
-    for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
+  for (int x = 0; x < NT * NT * 2; ++x) fhw[32 * x] = 0.0;
   for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
     const int64_t base = rd * 32;
-    round_prefetch(base, K, R, srow, Pp, nullptr, W, true);
-    round_prefetch(base + 32 * (int64_t)nwarps_total, K, R, srow, Pp, nullptr, W, false);
+    {  // prefetch this round's P' and W rows into L1 and the next round's into L2
+      const int64_t last = base + 32 < K ? base + 32 : K;
+      warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)((last - base) * pstride), true);
+      warp_prefetch(W + base * R, sizeof(double) * (size_t)((last - base) * R), true);
+      const int64_t nb = base + 32 * (int64_t)nwarps_total;
+      if (nb < K) {
+        const int64_t nl = nb + 32 < K ? nb + 32 : K;
+        warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)((nl - nb) * pstride), false);
+        warp_prefetch(W + nb * R, sizeof(double) * (size_t)((nl - nb) * R), false);
+      }
+    }
     const int64_t kme = base + lane;
     const int mme = kme < K ? m[kme] : 0;
     // ---- Givens QR of A^T (rows of A^T = columns of A), slab by slab
@@ -234,21 +249,25 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     // ---- SVD of the m x m factor: rows of Rf -> sigma_j v_j; u_j = v_j / sqrt(sigma_j) so that
     //      K = sum_kept u_j u_j^T = V Σ^-1 V^T on the numerical range (reading R-polar-2/3)
     jacobi_rows_reg<L>(Rf);
-    double sig[L], smax = 0.0;
+    double smax = 0.0;
 #pragma unroll
     for (int j = 0; j < L; ++j) {
       double s = 0.0;
 #pragma unroll
       for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
-      sig[j] = sqrt(s);
-      smax = fmax(smax, sig[j]);
+      smax = fmax(smax, s);
     }
+    smax = sqrt(smax);
     int rk = 0;
 #pragma unroll
     for (int j = 0; j < L; ++j) {
-      const bool keep = smax > 0.0 && sig[j] > tau * smax;
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
+      const double sg = sqrt(s);
+      const bool keep = smax > 0.0 && sg > tau * smax;
       rk += keep ? 1 : 0;
-      const double sc = keep ? 1.0 / (sig[j] * sqrt(sig[j])) : 0.0;
+      const double sc = keep ? 1.0 / (sg * sqrt(sg)) : 0.0;
 #pragma unroll
       for (int i = 0; i < L; ++i) Rf[j][i] *= sc;
     }
@@ -258,7 +277,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
       a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab);
       __syncwarp();
       if (kme < K && mme > 0) {
-        double* Q = Qt + srow[kme] * R;
+        double* Q = Qt + kme * pstride;
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const int s = 8 * nt + cc;
@@ -285,50 +304,85 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
       }
       __syncwarp();
     }
-    // ---- F_H += Q~_p^T (P'_p S_p): MMA with M = r, N = s, K = a
-    for (int p = 0; p < 32; ++p) {
-      const int64_t kp = base + p;
-      if (kp >= K) break;
-      const int mp = m[kp];
-      if (mp == 0) continue;
-      const double* Q = Qt + srow[kp] * R;
-      const double* P = Pp + srow[kp] * R;
-      const double* w = W + kp * R;
+    // ---- F_H += Q~_p^T (P'_p S_p): MMA with M = r, N = s, K = a (rows a >= m_p are zero)
+    {
+      int offq[2 * MT][NT];
+      int offw[NT];
 #pragma unroll
-      for (int ks = 0; ks < 2 * MT; ++ks) {
-        const int a = 4 * ks + t;
-        double af[NT], bf[NT];
+      for (int ks = 0; ks < 2 * MT; ++ks)
 #pragma unroll
         for (int i = 0; i < NT; ++i) {
-          const int rr = 8 * i + g;
-          af[i] = (a < mp && rr < R) ? Q[a * R + rr] : 0.0;            // A[g][t] = Q~^T(r, a)
-          bf[i] = (a < mp && rr < R) ? P[a * R + rr] * w[rr] : 0.0;    // B[t][g] = (P'S)(a, s)
+          const int a = 4 * ks + t, rr = 8 * i + g;
+          offq[ks][i] = (a < l && rr < R) ? a * R + rr : -1;
         }
 #pragma unroll
-        for (int i = 0; i < NT; ++i)
+      for (int i = 0; i < NT; ++i) offw[i] = 8 * i + g < R ? 8 * i + g : -1;
+      double fh[NT][NT][2];
 #pragma unroll
-          for (int j = 0; j < NT; ++j) dmma2(fh[i][j][0], fh[i][j][1], af[i], bf[j]);
+      for (int a = 0; a < NT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
+      const int np = (int)(K - base < 32 ? K - base : 32);
+      const double* Q = Qt + base * pstride;
+      const double* P = Pp + base * pstride;
+      const double* w = W + base * R;
+      auto load = [&](const double* Qk, const double* Pk, const double* wk, double (&af)[2 * MT][NT],
+                      double (&bf)[2 * MT][NT]) {
+        double wv[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) wv[i] = offw[i] >= 0 ? wk[offw[i]] : 0.0;
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            af[ks][i] = offq[ks][i] >= 0 ? Qk[offq[ks][i]] : 0.0;          // A[g][t] = Q~^T(r, a)
+            bf[ks][i] = offq[ks][i] >= 0 ? Pk[offq[ks][i]] * wv[i] : 0.0;  // B[t][g] = (P'S)(a, s)
+          }
+      };
+      double af[2 * MT][NT], bf[2 * MT][NT];
+      if (np > 0) load(Q, P, w, af, bf);
+      for (int p = 0; p < np; ++p) {
+        double an[2 * MT][NT], bn[2 * MT][NT];
+        Q += pstride;
+        P += pstride;
+        w += R;
+        if (p + 1 < np) load(Q, P, w, an, bn);
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma2(fh[i][j][0], fh[i][j][1], af[ks][i], bf[ks][j]);
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            af[ks][i] = an[ks][i];
+            bf[ks][i] = bn[ks][i];
+          }
       }
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) fhw[32 * ((i * NT + j) * 2 + c)] += fh[i][j][c];
     }
   }
-  // ---- reduce the per-warp F_H accumulators of the block, write the block partial
-  __syncthreads();
-  double* red = sm + hoff;  // reuse the slabs: (warps) x (8 NT)^2
-  const int RP = 8 * NT;
-#pragma unroll
-  for (int i = 0; i < NT; ++i)
-#pragma unroll
-    for (int j = 0; j < NT; ++j)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) red[wib * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = fh[i][j][c];
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
-    const int r = x / R, s = x - r * R;
-    double v = 0.0;
-    for (int ww = 0; ww < nw; ++ww) v += red[ww * RP * RP + r * RP + s];
-    FHpart[(int64_t)blockIdx.x * R * R + x] = v;
-  }
+}
+
+// F_H = sum over warps (fixed order) of the fragment-ordered partials
+__global__ void k_sum_fh(const double* __restrict__ part, int nw, int R, int NT, double* __restrict__ FH) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= R * R) return;
+  const int r = x / R, s = x - r * R;
+  // fragment position of (r, s): tile (i = r/8, j = s/8), lane g = r%8, t = (s%8)/2, c = s%2
+  const int i = r >> 3, j = s >> 3, g = r & 7, t = (s & 7) >> 1, c = s & 1;
+  const int off = 32 * ((i * NT + j) * 2 + c) + g * 4 + t;
+  const int rp2 = 64 * NT * NT;
+  double v = 0.0;
+  for (int w = 0; w < nw; ++w) v += part[(int64_t)w * rp2 + off];
+  FH[x] = v;
 }
 
 __global__ void k_sum_rr(const double* part, int nb, int n, double* out) {
@@ -341,14 +395,13 @@ __global__ void k_sum_rr(const double* part, int nb, int n, double* out) {
 
 constexpr int kDenseThreads = 128;
 
-template <int L, int NT>
+template <int L, int NT, int RT = 0, int LT = 0>
 static void polar_wide_inst(Handle& h) {
   constexpr int MT = (L + 7) / 8;
-  auto fn = k_polar_wide<L, MT, NT>;
+  auto fn = k_polar_wide<L, MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
   const size_t slabs = (size_t)(kDenseThreads / 32) * 32 * MT * 8 * 8;
-  const size_t red = (size_t)(kDenseThreads / 32) * (8 * NT) * (8 * NT);
-  size_t smem = sizeof(double) * (hoff + (slabs > red ? slabs : red));
+  size_t smem = sizeof(double) * (hoff + slabs);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -363,14 +416,18 @@ static void polar_wide_inst(Handle& h) {
   if (cap > kPartBlocks) cap = kPartBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt,
-                                                         h.rank, h.partial);
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt,
+                                                         h.rank, h.fh_warp);
   const int RR = h.R * h.R;
-  k_sum_rr<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.FH);
+  k_sum_fh<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.fh_warp, (int)blocks * (kDenseThreads / 32), h.R, NT, h.FH);
 }
 
 template <int L>
 static void polar_wide_n(Handle& h) {
+  // compile-time (R, l) for the BASELINE configs (Medium, Large, Scale); generic otherwise
+  if (L == 7 && h.l == 7 && h.R == 20) { polar_wide_inst<7, 3, 20, 7>(h); return; }
+  if (L == 7 && h.l == 7 && h.R == 15) { polar_wide_inst<7, 2, 15, 7>(h); return; }
+  if (L == 9 && h.l == 9 && h.R == 40) { polar_wide_inst<9, 5, 40, 9>(h); return; }
   switch ((h.R + 7) / 8) {
     case 1: polar_wide_inst<L, 1>(h); break;
     case 2: polar_wide_inst<L, 2>(h); break;
@@ -396,60 +453,85 @@ int launch_polar_wide(Handle& h) {
 }
 
 // ------------------------------------------------------------------ pass B (wide): F_W, W ADMM, N, M, W^T W
-// T slab for patient p: T(a, r) = sum_i Q~(a, i) H̄(i, r). MMA: M = a, N = r (NT tiles), K = i.
-template <int MT, int NT>
-__device__ __forceinline__ void t_tiles(int64_t kp, int mp, int R, const int64_t* srow, const double* Qt,
-                                        const double* Hs, double (&c)[MT][NT][2]) {
-  constexpr int KS = (NT * 8 + 3) / 4;
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const double* Q = Qt + srow[kp] * R;
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
-#pragma unroll
-  for (int ks = 0; ks < KS; ++ks) {
-    const int i = 4 * ks + t;
-    double af[MT];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int a = 8 * mt + g;
-      af[mt] = (a < mp && i < R) ? Q[a * R + i] : 0.0;  // A[g][t] = Q~(a, i)
-    }
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const int r = 8 * nt + g;
-      const double b = (i < R && r < R) ? Hs[i * R + r] : 0.0;  // B[t][g] = H(i, r)
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) dmma2(c[mt][nt][0], c[mt][nt][1], af[mt], b);
-    }
-  }
-}
-
-template <int MT, int NT>
-__global__ void __launch_bounds__(128) k_passB_wide(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
-                                                    int64_t K, int R, const double* __restrict__ Pp,
+// Per patient p of a warp round (one MMA tile set per patient, the next patient's fragments loaded
+// while the current one's MMAs run):
+//   T_p = Q~_p H̄ (MMA: M = a, N = r, K = i), F_W(p, r) = sum_a T_p(a, r) P'_p(a, r)   (Alg.1 l.12, W mode)
+// thread per patient: 5 ADMM row steps z = Ginv (f + rho (w̄ + d)), w̄ = prox(z - d), d += w̄ - z with
+//   Ginv = (G_W + rho I)^-1 formed once from the cached Cholesky factor (k_admm_H)          (l.13-19)
+//   N_p = T_p S_p (new w̄_p) -> HBM, M += N_p^T N_p (MMA via the warp's smem scratch), W̄^T W̄ += w̄ w̄^T
+template <int MT, int NT, int RT, int LT>
+__global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, const double* __restrict__ Pp,
                                                     const double* __restrict__ Qt, const double* __restrict__ Hg,
-                                                    const double* __restrict__ LWg, const double* __restrict__ scal,
+                                                    const double* __restrict__ GWi, const double* __restrict__ scal,
                                                     int n_inner, int kind, double param, double* __restrict__ W,
                                                     double* __restrict__ DW, double* __restrict__ Nst,
                                                     double* __restrict__ part /* [blocks][2][R R] */) {
   constexpr int RP = 8 * NT;
+  constexpr int KS = (NT * 8 + 3) / 4;  // i steps of 4 covering 8 NT >= R
+  const int R = RT ? RT : R_;
+  const int l = LT ? LT : l_;
   extern __shared__ double sm[];
   const int hoff = ((R * R + 31) / 32) * 32;
   double* Hs = sm;                 // R x R
-  double* Ls = sm + hoff;          // R x R (chol of G_W + rho I)
+  double* Gs = sm + hoff;          // R x R  (G_W + rho I)^-1
   const int wib = threadIdx.x >> 5;
-  double* wv = sm + 2 * hoff + wib * (3 * RP * 32);  // per warp: fw, w̄, d as [r][lane]
+  double* wv = sm + 2 * hoff + wib * (3 * RP * 32 + MT * 8 * RP);  // per warp: fw, w̄, d as [r][lane] + N scratch
   double* fwv = wv;
   double* wbv = wv + RP * 32;
   double* dv = wv + 2 * RP * 32;
-  for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Ls[x] = LWg[x]; }
+  double* ns = wv + 3 * RP * 32;   // N_p (MT 8 x RP)
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Gs[x] = GWi[x]; }
   __syncthreads();
   const double rho = scal[S_RHO_W];
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int nwarps_total = gridDim.x * (blockDim.x >> 5);
   const int64_t rounds = (K + 31) / 32;
+  const int64_t pstride = (int64_t)l * R;
+  // lane-constant fragment offsets (-1: padding)
+  int offq[KS][MT];   // A[g][t] = Q~(a = 8 mt + g, i = 4 ks + t)
+  int offp[MT][NT][2];  // C-layout (a = 8 mt + g, r = 8 nt + 2 t + c)
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int a = 8 * mt + g, i = 4 * ks + t;
+      offq[ks][mt] = (a < l && i < R) ? a * R + i : -1;
+    }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int a = 8 * mt + g, r = 8 * nt + 2 * t + c;
+        offp[mt][nt][c] = (a < l && r < R) ? a * R + r : -1;
+      }
+  double hb[KS][NT];  // B[t][g] = H̄(i = 4 ks + t, r = 8 nt + g), kept in registers
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int i = 4 * ks + t, r = 8 * nt + g;
+      hb[ks][nt] = (i < R && r < R) ? Hs[i * R + r] : 0.0;
+    }
+  auto load_q = [&](const double* Q, double (&f)[KS][MT]) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) f[ks][mt] = offq[ks][mt] >= 0 ? Q[offq[ks][mt]] : 0.0;
+  };
+  auto t_mma = [&](const double (&f)[KS][MT], double (&c)[MT][NT][2]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma2(c[mt][nt][0], c[mt][nt][1], f[ks][mt], hb[ks][nt]);
+  };
   double macc[NT][NT][2], wacc[NT][NT][2];
 #pragma unroll
   for (int a = 0; a < NT; ++a)
@@ -457,69 +539,72 @@ __global__ void __launch_bounds__(128) k_passB_wide(const int32_t* __restrict__ 
     for (int b = 0; b < NT; ++b) macc[a][b][0] = macc[a][b][1] = wacc[a][b][0] = wacc[a][b][1] = 0.0;
   for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
     const int64_t base = rd * 32;
-    round_prefetch(base, K, R, srow, Pp, Qt, W, true);
-    round_prefetch(base + 32 * (int64_t)nwarps_total, K, R, srow, Pp, Qt, W, false);
-    if (base < K) warp_prefetch(DW + base * R, sizeof(double) * 32 * R, true);
-    // ---- F_W rows: F_W(k, r) = sum_a T(a, r) P'(a, r)
-    for (int p = 0; p < 32; ++p) {
-      const int64_t kp = base + p;
-      if (kp >= K) break;
-      const int mp = m[kp];
-      double c[MT][NT][2];
-      t_tiles<MT, NT>(kp, mp, R, srow, Qt, Hs, c);
-      const double* P = Pp + srow[kp] * R;
+    const int np = (int)(K - base < 32 ? K - base : 32);
+    {  // this round's rows into L1, the next round's into L2
+      warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+      warp_prefetch(Qt + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+      warp_prefetch(W + base * R, sizeof(double) * (size_t)(np * R), true);
+      warp_prefetch(DW + base * R, sizeof(double) * (size_t)(np * R), true);
+      const int64_t nb = base + 32 * (int64_t)nwarps_total;
+      if (nb < K) {
+        const int64_t nn = K - nb < 32 ? K - nb : 32;
+        warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
+        warp_prefetch(Qt + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
+      }
+    }
+    // ---- F_W rows: F_W(p, r) = sum_a T_p(a, r) P'_p(a, r)
+    {
+      const double* Q = Qt + base * pstride;
+      const double* P = Pp + base * pstride;
+      double fq[KS][MT];
+      load_q(Q, fq);
+      for (int p = 0; p < np; ++p) {
+        double pv[MT][NT][2];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = 8 * nt + 2 * t + i;
-          double s = 0.0;
+          for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const int a = 8 * mt + g;
-            s = fma(c[mt][nt][i], (a < mp && r < R) ? P[a * R + r] : 0.0, s);
+            for (int c = 0; c < 2; ++c) pv[mt][nt][c] = offp[mt][nt][c] >= 0 ? P[offp[mt][nt][c]] : 0.0;
+        double c[MT][NT][2];
+        t_mma(fq, c);
+        Q += pstride;
+        P += pstride;
+        if (p + 1 < np) load_q(Q, fq);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double sv = 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) sv = fma(c[mt][nt][i], pv[mt][nt][i], sv);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 4);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 8);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 16);
+            if (g == 0) fwv[(8 * nt + 2 * t + i) * 32 + p] = sv;
           }
-          s += __shfl_xor_sync(0xffffffffu, s, 4);
-          s += __shfl_xor_sync(0xffffffffu, s, 8);
-          s += __shfl_xor_sync(0xffffffffu, s, 16);
-          if (g == 0) fwv[r * 32 + p] = s;
-        }
+      }
     }
     __syncwarp();
-    // ---- W-row ADMM (thread = patient): z = (f + rho (w̄ + d)) (G + rho I)^-1; w̄ = prox(z - d); d += w̄ - z
+    // ---- W-row ADMM (thread = patient)
     const int64_t kme = base + lane;
     if (kme < K) {
       for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
-      double z[RP];
       for (int it = 0; it < n_inner; ++it) {
+        double rhs[RP];
 #pragma unroll
         for (int r = 0; r < RP; ++r)
-          z[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
-#pragma unroll
-        for (int i = 0; i < RP; ++i) {
-          if (i < R) {
-            double v = z[i];
-#pragma unroll
-            for (int k2 = 0; k2 < i; ++k2) v = fma(-Ls[i * R + k2], z[k2], v);
-            z[i] = v / Ls[i * R + i];
-          }
-        }
-#pragma unroll
-        for (int i = RP - 1; i >= 0; --i) {
-          if (i < R) {
-            double v = z[i];
-#pragma unroll
-            for (int k2 = i + 1; k2 < RP; ++k2)
-              if (k2 < R) v = fma(-Ls[k2 * R + i], z[k2], v);
-            z[i] = v / Ls[i * R + i];
-          }
-        }
+          rhs[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
 #pragma unroll
         for (int r = 0; r < RP; ++r) {
           if (r < R) {
+            double z = 0.0;
+#pragma unroll
+            for (int q = 0; q < RP; ++q)
+              if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
             const double d0 = dv[r * 32 + lane];
-            const double nb = prox(kind, param, rho, z[r] - d0);
-            dv[r * 32 + lane] = d0 + nb - z[r];
+            const double nb = prox(kind, param, rho, z - d0);
+            dv[r * 32 + lane] = d0 + nb - z;
             wbv[r * 32 + lane] = nb;
           }
         }
@@ -544,45 +629,46 @@ __global__ void __launch_bounds__(128) k_passB_wide(const int32_t* __restrict__ 
 #pragma unroll
         for (int j = 0; j < NT; ++j) dmma2(wacc[i][j][0], wacc[i][j][1], af[i], af[j]);
     }
-    // ---- N_p = T_p S_p (new w̄_p), M += N_p^T N_p
-    for (int p = 0; p < 32; ++p) {
-      const int64_t kp = base + p;
-      if (kp >= K) break;
-      const int mp = m[kp];
-      if (mp == 0) continue;
-      double c[MT][NT][2];
-      t_tiles<MT, NT>(kp, mp, R, srow, Qt, Hs, c);
-      double* N = Nst + srow[kp] * R;
+    // ---- N_p = T_p S_p (new w̄_p) -> HBM; M += N_p^T N_p
+    {
+      const double* Q = Qt + base * pstride;
+      double* Nrow = Nst + base * pstride;
+      double fq[KS][MT];
+      load_q(Q, fq);
+      for (int p = 0; p < np; ++p) {
+        double c[MT][NT][2];
+        t_mma(fq, c);
+        Q += pstride;
+        if (p + 1 < np) load_q(Q, fq);
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const int a = 8 * mt + g;
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
+          for (int nt = 0; nt < NT; ++nt) {
+            double v[2];
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int r = 8 * nt + 2 * t + i;
-            const double v = r < R ? c[mt][nt][i] * wbv[r * 32 + p] : 0.0;
-            c[mt][nt][i] = v;
-            if (a < mp && r < R) N[a * R + r] = v;
+            for (int i = 0; i < 2; ++i) {
+              const int r = 8 * nt + 2 * t + i;
+              v[i] = r < R ? c[mt][nt][i] * wbv[r * 32 + p] : 0.0;
+              if (offp[mt][nt][i] >= 0) Nrow[offp[mt][nt][i]] = v[i];
+            }
+            *reinterpret_cast<double2*>(ns + (8 * mt + g) * RP + 8 * nt + 2 * t) = make_double2(v[0], v[1]);
           }
-      }
-      __syncwarp();
-      // M += N^T N: A[g][t] = N(a = 4ks+t, r = 8i+g), B[t][g] = N(a, s = 8j+g): read back from global (L1)
+        __syncwarp();
+        // M += N^T N: A[g][t] = N(a = 4 ks + t, r = 8 i + g), B[t][g] = N(a, s = 8 j + g)
 #pragma unroll
-      for (int ks = 0; ks < 2 * MT; ++ks) {
-        const int a = 4 * ks + t;
-        double af[NT];
+        for (int ks = 0; ks < 2 * MT; ++ks) {
+          const int a = 4 * ks + t;
+          double af[NT];
 #pragma unroll
-        for (int i = 0; i < NT; ++i) {
-          const int r = 8 * i + g;
-          af[i] = (a < mp && r < R) ? N[a * R + r] : 0.0;
+          for (int i = 0; i < NT; ++i) af[i] = a < l ? ns[a * RP + 8 * i + g] : 0.0;
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma2(macc[i][j][0], macc[i][j][1], af[i], af[j]);
         }
-#pragma unroll
-        for (int i = 0; i < NT; ++i)
-#pragma unroll
-          for (int j = 0; j < NT; ++j) dmma2(macc[i][j][0], macc[i][j][1], af[i], af[j]);
+        __syncwarp();
+        Nrow += pstride;
       }
-      __syncwarp();
     }
   }
   __syncthreads();
@@ -600,9 +686,9 @@ __global__ void __launch_bounds__(128) k_passB_wide(const int32_t* __restrict__ 
   __syncthreads();
   for (int x = threadIdx.x; x < 2 * R * R; x += blockDim.x) {
     const int which = x / (R * R), y = x - which * R * R;
-    const int r = y / R, s = y - r * R;
+    const int r = y / R, s2 = y - r * R;
     double v = 0.0;
-    for (int ww = 0; ww < nw; ++ww) v += red[(ww * 2 + which) * RP * RP + r * RP + s];
+    for (int ww = 0; ww < nw; ++ww) v += red[(ww * 2 + which) * RP * RP + r * RP + s2];
     part[((int64_t)blockIdx.x * 2 + which) * R * R + y] = v;
   }
 }
@@ -616,12 +702,12 @@ __global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, double*
   (which == 0 ? M : WtW)[y] = s;
 }
 
-template <int MT, int NT>
+template <int MT, int NT, int RT = 0, int LT = 0>
 static void passB_wide_inst(Handle& h) {
   constexpr int RP = 8 * NT;
-  auto fn = k_passB_wide<MT, NT>;
+  auto fn = k_passB_wide<MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
-  size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32);
+  size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32 + MT * 8 * RP);
   size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
   size_t smem = sizeof(double) * 2 * hoff + (per_warp * (kDenseThreads / 32) > red ? per_warp * (kDenseThreads / 32) : red);
   static bool attr = false;
@@ -638,7 +724,7 @@ static void passB_wide_inst(Handle& h) {
   if (cap > kPartBlocks) cap = kPartBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.LW, h.scal,
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.K, h.R, h.l, h.Pp, h.Qt, h.H, h.GWi, h.scal,
                                                          h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
                                                          h.Nst, h.partial);
   const int RR = h.R * h.R;
@@ -647,6 +733,9 @@ static void passB_wide_inst(Handle& h) {
 
 template <int MT>
 static void passB_wide_n(Handle& h) {
+  if (MT == 1 && h.l == 7 && h.R == 20) { passB_wide_inst<1, 3, 20, 7>(h); return; }
+  if (MT == 1 && h.l == 7 && h.R == 15) { passB_wide_inst<1, 2, 15, 7>(h); return; }
+  if (MT == 2 && h.l == 9 && h.R == 40) { passB_wide_inst<2, 5, 40, 9>(h); return; }
   switch ((h.R + 7) / 8) {
     case 1: passB_wide_inst<MT, 1>(h); break;
     case 2: passB_wide_inst<MT, 2>(h); break;

@@ -28,6 +28,7 @@
 #include <climits>
 #include <cstdlib>
 #include <numeric>
+#include <type_traits>
 
 #include "copa_internal.cuh"
 
@@ -254,31 +255,37 @@ void launch_spmm_fibers(Handle& h) {
 
 // ------------------------------------------------------------------ pass B (TMA-staged scatter)
 // Stage slot layout (bytes, each part 16-byte aligned):
-//   meta  : int64 f0, f1; int32 k0, k1, shift_col, shift_val, shift_n, shift_gp   (48)
+//   meta  : int64 f0, f1; int32 k0, k1, shift_col, shift_val, shift_n, shift_gp, shift_wo (48)
 //   gp    : int64 [PB + 1] + 16  run starts of the stage's patients in stream g (bulk copy, shifted)
+//   wo    : uint16 [PB][kWoS] + 16  label sub-run offsets inside each run (bulk copy, shifted)
 //   col   : int32 [FB] + 16  labels           (bulk copy, shifted)
 //   val   : f64 [FB l] + 16   fiber values     (bulk copy, shifted)
 //   nrows : f64 [PB l R] + 16 N_k rows         (bulk copy, shifted)
 struct SlotGeom {
-  uint32_t gp, col, val, nrows, bytes;
+  uint32_t gp, wo, col, val, nrows, bytes;
 };
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~(uint64_t)15); }
 __host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
   SlotGeom s;
   s.gp = 48;
-  s.col = s.gp + al16(8ull * (PB + 1) + 16);
+  s.wo = s.gp + al16(8ull * (PB + 1) + 16);
+  s.col = s.wo + al16(2ull * kWoS * PB + 16);
   s.val = s.col + al16(4ull * FB + 16);
   s.nrows = s.val + al16(8ull * FB * l + 16);
   s.bytes = (s.nrows + al16(8ull * PB * l * R + 16) + 127) & ~127u;
   return s;
 }
 
-template <int KS, int NT, int W>
+constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
+constexpr int kPfFibers = 4096;   // pass-B L2 prefetch distance (fibers) ahead of the ring
+constexpr int kPfPatients = 64;   // and patients (N rows)
+
+template <int KS, int NT, int W, int TB>
 __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
-    const int32_t* __restrict__ cta_st, int l, int R, int RS, int FB, int PB, int NSt,
-    const double* __restrict__ Nst, double* __restrict__ FVpart) {
+    const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l, int R, int RS, int FB, int PB,
+    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg) {
   extern __shared__ __align__(128) unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = blockIdx.x % G;
@@ -310,16 +317,39 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         nf0 = st_f[2 * (int64_t)s0]; nf1 = st_f[2 * (int64_t)s0 + 1];
         nk0 = st_k[2 * (int64_t)s0]; nk1 = st_k[2 * (int64_t)s0 + 1];
       }
+      // L2 prefetch frontier: fibers and N rows up to kPfFibers / kPfPatients beyond the stage
+      // being issued, so the bulk copies mostly hit L2 (the ring itself is only NS stages deep)
+      int64_t pf_f = nf0, pf_k = nk0, end_f = 0, end_k = 0;
+      if (ns > 0) {
+        end_f = st_f[2 * (int64_t)(s0 + ns - 1) + 1];
+        end_k = st_k[2 * (int64_t)(s0 + ns - 1) + 1];
+      }
+      int slot = 0, phase = 1;  // the producer's first pass over the ring does not wait
       for (int i = 0; i < ns; ++i) {
-        const int slot = i % NSt, use = i / NSt;
         const int64_t f0 = nf0, f1 = nf1;
         const int32_t k0 = nk0, k1 = nk1;
+        {
+          const int64_t ft = min(f1 + (int64_t)kPfFibers, end_f);
+          while (pf_f < ft) {
+            const int64_t n = min((int64_t)1024, ft - pf_f);
+            l2_prefetch(fiber_col + pf_f, 4ull * n);
+            l2_prefetch(fiber_val + pf_f * l, 8ull * n * l);
+            pf_f += n;
+          }
+          const int64_t kt = min((int64_t)k1 + kPfPatients, end_k);
+          while (pf_k < kt) {
+            const int64_t n = min((int64_t)16, kt - pf_k);
+            l2_prefetch(Nst + pf_k * l * R, 8ull * n * l * R);
+            l2_prefetch(gptr + grp * K1 + pf_k, 8ull * (n + 1));
+            pf_k += n;
+          }
+        }
         if (i + 1 < ns) {
           const int64_t st = s0 + i + 1;
           nf0 = st_f[2 * st]; nf1 = st_f[2 * st + 1];
           nk0 = st_k[2 * st]; nk1 = st_k[2 * st + 1];
         }
-        mbar_wait(empty + slot, (use & 1) ^ 1);
+        mbar_wait(empty + slot, phase);
         unsigned char* base = slots + (size_t)slot * sg.bytes;
         int64_t* meta = (int64_t*)base;
         int32_t* mi = (int32_t*)(base + 16);
@@ -328,52 +358,58 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         mi[0] = k0;
         mi[1] = k1;
         const uintptr_t sc = (uintptr_t)(fiber_col + f0), sv = (uintptr_t)(fiber_val + f0 * l),
-                        sn = (uintptr_t)(Nst + (int64_t)k0 * l * R), sp = (uintptr_t)(gptr + grp * K1 + k0);
+                        sn = (uintptr_t)(Nst + (int64_t)k0 * l * R), sp = (uintptr_t)(gptr + grp * K1 + k0),
+                        sw = (uintptr_t)(woff + ((int64_t)grp * K + k0) * kWoS);
         const size_t bc = 4ull * (f1 - f0), bv = 8ull * (f1 - f0) * l, bn = 8ull * (k1 - k0) * l * R,
-                     bp = 8ull * (k1 - k0 + 1);
+                     bp = 8ull * (k1 - k0 + 1), bw = 2ull * kWoS * (k1 - k0);
         mi[2] = (int32_t)(sc & 15);
         mi[3] = (int32_t)(sv & 15);
         mi[4] = (int32_t)(sn & 15);
         mi[5] = (int32_t)(sp & 15);
+        mi[6] = (int32_t)(sw & 15);
         // expected bytes first (same rounding as bulk_g2s_span), then the copies
-        const uint32_t tx = al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn) + al16((sp & 15) + bp);
+        const uint32_t tx = al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn) +
+                            al16((sp & 15) + bp) + al16((sw & 15) + bw);
+        if (dbg == 2) {  // timing experiment: no copies
+          mbar_arrive(full + slot);
+          if (++slot == NSt) { slot = 0; phase ^= 1; }
+          continue;
+        }
         mbar_arrive_tx(full + slot, tx);
         uint32_t t2 = 0;
         bulk_g2s_span(base + sg.gp, (const void*)sp, bp, full + slot, &t2);
+        bulk_g2s_span(base + sg.wo, (const void*)sw, bw, full + slot, &t2);
         bulk_g2s_span(base + sg.col, (const void*)sc, bc, full + slot, &t2);
         bulk_g2s_span(base + sg.val, (const void*)sv, bv, full + slot, &t2);
         bulk_g2s_span(base + sg.nrows, (const void*)sn, bn, full + slot, &t2);
+        if (++slot == NSt) { slot = 0; phase ^= 1; }
       }
     }
   } else {
-    // ---------------- consumers: warp w owns labels [lw0, lw1) of group grp
+    // ---------------- consumers: warp w owns label sub-range (grp, w) = labels [grp Jg + w Js, + Js),
+    // all R columns of those F_V rows: no two warps write the same row. Its sub-run of each run
+    // comes from the staged offsets; tiles of 8 fibers (one patient, distinct labels) run TB at a
+    // time: loads and MMAs of the batch first, then the read-modify-writes.
     const int g = lane >> 2, t = lane & 3;
-    const int32_t lw0 = (int32_t)(grp * Jg + (int64_t)w * Js), lw1 = (int32_t)(lw0 + Js);
     const int64_t jbase = grp * Jg;
     const int per = l * R;
+    double sink = 0.0;  // timing experiments (dbg 3, 4) only
+    int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
-      const int slot = i % NSt, use = i / NSt;
-      mbar_wait(full + slot, use & 1);
+      mbar_wait(full + slot, phase);
       const unsigned char* base = slots + (size_t)slot * sg.bytes;
       const int64_t f0 = ((const int64_t*)base)[0], f1 = ((const int64_t*)base)[1];
       const int32_t* mi = (const int32_t*)(base + 16);
       const int32_t k0 = mi[0], k1 = mi[1];
       const int64_t* gp = (const int64_t*)(base + sg.gp + mi[5]);
+      const uint16_t* wo = (const uint16_t*)(base + sg.wo + mi[6]);
       const int32_t* colS = (const int32_t*)(base + sg.col + mi[2]);
       const double* valS = (const double*)(base + sg.val + mi[3]);
       const double* nS = (const double*)(base + sg.nrows + mi[4]);
-      for (int p = 0; p < k1 - k0; ++p) {
-        const int64_t a0 = max(gp[p], f0) - f0, a1 = min(gp[p + 1], f1) - f0;
-        if (a0 >= a1) continue;
-        // sub-run of labels [lw0, lw1) inside the (label-sorted) run [a0, a1)
-        int c0 = 0, c1 = 0;
-        for (int64_t x0 = a0; x0 < a1; x0 += 32) {
-          const int64_t x = x0 + lane;
-          const int32_t lab = x < a1 ? colS[x] : INT_MAX;
-          c0 += __popc(__ballot_sync(0xffffffffu, lab < lw0));
-          c1 += __popc(__ballot_sync(0xffffffffu, lab < lw1));
-        }
-        const int64_t lo = a0 + c0, hi = a0 + c1;
+      for (int p = 0; p < (dbg == 1 ? 0 : k1 - k0); ++p) {
+        const int64_t rs = gp[p];
+        const int lo = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
+        const int hi = (int)(min(rs + wo[p * kWoS + w + 1], f1) - f0);
         if (lo >= hi) continue;
         // B fragments of this patient: B[t][g] = N(a = 4 ks + t, r = 8 nt + g)
         const double* Np = nS + (int64_t)p * per;
@@ -385,41 +421,67 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             const int a = 4 * ks + t, r = 8 * nt + g;
             bfr[ks][nt] = (a < l && r < R) ? Np[a * R + r] : 0.0;
           }
-        for (int64_t tb = lo; tb < hi; tb += 8) {
-          const int64_t f = tb + g;
-          const bool ok = f < hi;
-          const int32_t col = ok ? colS[f] : 0;
-          double av[KS];
+        if (dbg == 3) { sink += bfr[0][0]; continue; }
+        // TB tiles at a time while >= TB tiles remain, then single tiles (no MMAs on empty tiles).
+        // Tiles of one sub-run belong to one patient => distinct labels => distinct F_V rows, so
+        // all row loads of a batch may precede its stores.
+        auto run_tiles = [&](int tb, auto tbc) {
+          constexpr int NB = decltype(tbc)::value;
+          int32_t col[NB];
+          double av[NB][KS];
+          double cc[NB][NT][2];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const int a = 4 * ks + t;
-            av[ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
-          }
-          double cc[NT][2];
+          for (int b = 0; b < NB; ++b) {
+            const int f = tb + 8 * b + g;
+            const bool ok = f < hi;
+            col[b] = ok ? colS[f] : -1;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            cc[nt][0] = cc[nt][1] = 0.0;
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
-          }
-          if (ok) {
-            double* row = Fs + (col - jbase) * RS;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const int r = 8 * nt + 2 * t;
-              if (r < RS) {
-                double2 v = *reinterpret_cast<double2*>(row + r);
-                v.x += cc[nt][0];
-                v.y += cc[nt][1];
-                *reinterpret_cast<double2*>(row + r) = v;
-              }
+            for (int ks = 0; ks < KS; ++ks) {
+              const int a = 4 * ks + t;
+              av[b][ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
             }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) cc[b][nt][0] = cc[b][nt][1] = 0.0;
           }
-        }
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) dmma(cc[b][nt][0], cc[b][nt][1], av[b][ks], bfr[ks][nt]);
+          if (dbg == 4) {
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+#pragma unroll
+              for (int nt = 0; nt < NT; ++nt) sink += cc[b][nt][0] + cc[b][nt][1] + (double)col[b];
+            return;
+          }
+          double2 v[NB][NT];
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              if (col[b] >= 0 && 8 * nt + 2 * t < R)
+                v[b][nt] = *reinterpret_cast<const double2*>(Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t);
+#pragma unroll
+          for (int b = 0; b < NB; ++b)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+              if (col[b] >= 0 && 8 * nt + 2 * t < R) {
+                v[b][nt].x += cc[b][nt][0];
+                v[b][nt].y += cc[b][nt][1];
+                *reinterpret_cast<double2*>(Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t) = v[b][nt];
+              }
+        };
+        int tb = lo;
+        for (; tb + 8 * (TB - 1) < hi; tb += 8 * TB) run_tiles(tb, std::integral_constant<int, TB>());
+        for (; tb < hi; tb += 8) run_tiles(tb, std::integral_constant<int, 1>());
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == NSt) { slot = 0; phase ^= 1; }
     }
+    if (dbg >= 3 && sink == 12345.678) Fs[0] += sink;
   }
   __syncthreads();
   double* out = FVpart + rng * (G * Jg) * (int64_t)R + (int64_t)grp * Jg * R;
@@ -444,16 +506,18 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
 
 template <int KS, int NT>
 static void scatter_inst(Handle& h) {
-  auto fn = k_scatter_tma<KS, NT, 4>;
+  constexpr int W = kScW;
+  auto fn = k_scatter_tma<KS, NT, W, 2>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
   const int ctas = h.sc_ranges * h.sc_G;
-  fn<<<ctas, 32 * (h.sc_W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js,
-                                                         h.sc_Jg, h.st_f, h.st_k, h.cta_st, h.l, h.R, h.sc_RS,
-                                                         h.sc_FB, h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
+  fn<<<ctas, 32 * (W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js, h.sc_Jg,
+                                                   h.st_f, h.st_k, h.cta_st, h.woff, h.l, h.R, h.sc_RS, h.sc_FB,
+                                                   h.sc_PB, h.sc_NS, h.Nst, h.fv_part,
+                                                   getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
@@ -486,31 +550,32 @@ int launch_scatter_fibers(Handle& h) {
 // ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared memory.
 void plan_scatter(Handle& h) {
   const size_t budget = 225 * 1024;
-  h.sc_W = 4;  // consumer warps per CTA (template parameter of k_scatter_tma)
+  h.sc_W = kScW;  // label sub-ranges per group = consumer warps of k_scatter_tma
   h.sc_RS = (h.R + 1) & ~1;
   h.sc_FB = 256;
   h.sc_ok = 0;
   const int pbs[3] = {16, 8, 4};
-  for (int G = 1; G <= kMaxGroups && !h.sc_ok; ++G) {
-    const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
-    const int64_t Jg = Js * h.sc_W;
-    const size_t fs = ((size_t)Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
-    for (int NSt = 4; NSt >= 2 && !h.sc_ok; --NSt)
-      for (int pi = 0; pi < 3 && !h.sc_ok; ++pi) {
-        const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
-        const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
-        if (bytes <= budget && (NSt >= 3 || pi == 2)) {
-          h.sc_G = G;
-          h.sc_Js = Js;
-          h.sc_Jg = Jg;
-          h.sc_PB = pbs[pi];
-          h.sc_NS = NSt;
-          h.sc_slot = sg.bytes;
-          h.sc_smem = bytes;
-          h.sc_ok = 1;
+  for (int pass = 0; pass < 2 && !h.sc_ok; ++pass)  // pass 0: >= 3 stages of >= 8 patients
+    for (int G = 1; G <= kMaxGroups && !h.sc_ok; ++G) {
+      const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
+      const int64_t Jg = Js * h.sc_W;
+      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
+      for (int NSt = 4; NSt >= (pass ? 2 : 3) && !h.sc_ok; --NSt)
+        for (int pi = 0; pi < (pass ? 3 : 2) && !h.sc_ok; ++pi) {
+          const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
+          const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
+          if (bytes <= budget) {
+            h.sc_G = G;
+            h.sc_Js = Js;
+            h.sc_Jg = Jg;
+            h.sc_PB = pbs[pi];
+            h.sc_NS = NSt;
+            h.sc_slot = sg.bytes;
+            h.sc_smem = bytes;
+            h.sc_ok = 1;
+          }
         }
-      }
-  }
+    }
   if (!h.sc_ok) {  // F_V does not fit even split 8 ways: global-atomic fallback (k_iter.cu)
     h.sc_G = kMaxGroups;
     h.sc_Js = (h.J + (int64_t)h.sc_G * h.sc_W - 1) / ((int64_t)h.sc_G * h.sc_W);

@@ -207,8 +207,11 @@ __device__ __forceinline__ int label_rank(const unsigned* bits, const int* pref,
   return pref[w] + __popc(bits[w] & ((1u << (x & 31)) - 1u));
 }
 
+// Also writes, per (group, patient), the offsets of the W label sub-runs inside the run:
+// woff[(g K + k) kWoS + w] = rank(g Jg + w Js) - rank(g Jg), w = 0..W (W < kWoS).
 __global__ void k_count_groups(const int64_t* prp, const int64_t* rp, const int32_t* col, const int32_t* perm,
-                               int64_t K, int words, int G, int64_t Jg, int32_t* gcnt /*[G][K]*/) {
+                               int64_t K, int words, int G, int64_t Jg, int W, int64_t Js, int32_t* gcnt /*[G][K]*/,
+                               uint16_t* woff /*[G][K][8]*/) {
   extern __shared__ unsigned smem_g[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned* bits = smem_g + wib * words;
@@ -220,6 +223,12 @@ __global__ void k_count_groups(const int64_t* prp, const int64_t* rp, const int3
       const int a = label_rank(bits, pref, words, lane * Jg);
       const int b = label_rank(bits, pref, words, (lane + 1) * Jg);
       gcnt[(int64_t)lane * K + k] = b - a;
+    }
+    for (int x = lane; x < G * kWoS; x += 32) {
+      const int g = x / kWoS, w = x % kWoS;
+      const int a = label_rank(bits, pref, words, g * Jg);
+      const int v = w <= W ? label_rank(bits, pref, words, g * Jg + (int64_t)w * Js) - a : 0;
+      woff[((int64_t)g * K + k) * kWoS + w] = (uint16_t)v;
     }
     __syncwarp();
   }
@@ -238,7 +247,8 @@ void launch_count_groups(Handle& h, int32_t* gcnt) {
   int64_t blocks = (h.K + warps - 1) / warps;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_count_groups<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.perm,
-                                                                    h.K, words, h.sc_G, h.sc_Jg, gcnt);
+                                                                    h.K, words, h.sc_G, h.sc_Jg, h.sc_W, h.sc_Js, gcnt,
+                                                                    h.woff);
 }
 
 // ------------------------------------------------------------------ fibers: build X'_k = C_k^T X_k

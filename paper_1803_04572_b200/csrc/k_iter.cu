@@ -280,7 +280,8 @@ __device__ __forceinline__ void admm_row(const double* L, int R, const double* f
 // H-mode (1 block) + the W-mode setup that depends only on the new H̄.
 __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const double* VtV, const double* WtW,
                                                 double rho_fixed, int n_inner, int kind, double param, double* H,
-                                                double* DH, double* HtH, double* LW, double* scal, int* err) {
+                                                double* DH, double* HtH, double* LW, double* GWi, double* scal,
+                                                int* err) {
   extern __shared__ double dyn_smem[];
   double* Gs = dyn_smem;
   double* Ls = dyn_smem + R * R;
@@ -321,6 +322,13 @@ __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const d
   __syncthreads();
   if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0) set_err(err, ERR_CHOL); return; }
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) LW[x] = Ls[x];
+  // (G_W + rho I)^-1 from the cached factor: column i solves L L^T x = e_i (used by the wide W pass)
+  for (int i = threadIdx.x; i < R; i += blockDim.x) {
+    double x[kMaxR];
+    for (int r = 0; r < R; ++r) x[r] = r == i ? 1.0 : 0.0;
+    chol_solve(Ls, R, x);
+    for (int r = 0; r < R; ++r) GWi[r * R + i] = x[r];
+  }
   if (threadIdx.x == 0) { scal[S_RHO_H] = rho; scal[S_RHO_W] = rho_w; }
 }
 
@@ -334,7 +342,7 @@ int launch_admm_H(Handle& h) {
   static bool once = (set_smem_attr(k_admm_H), true);
   (void)once;
   k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind, h.o.on_H.param,
-                                    h.H, h.DH, h.HtH, h.LW, h.scal, h.err);
+                                    h.H, h.DH, h.HtH, h.LW, h.GWi, h.scal, h.err);
   return 1;
 }
 
