@@ -1,0 +1,786 @@
+// k_dense.cuh — per-patient dense work of the smooth ("wide": m_k <= l < R) path, organised in
+// warp rounds of 32 patients: the R-dimension contractions run on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, warp-cooperative, one patient per MMA tile) and the small sequential
+// m_k x m_k algebra (Givens QR, one-sided Jacobi, row ADMM solves) runs one patient per thread.
+//
+//   polar_wide : A_k = P'_k S_k H̄^T (MMA, 8-column slabs) -> Givens QR of A_k^T (thread)
+//                -> Jacobi (thread) -> Q~_k = K_k A_k (thread, K_k = V Σ^-1 V^T on the range)
+//                -> F_H += Q~_k^T P'_k S_k (MMA, per-warp accumulators)        (Alg.1 l.4-6, l.12)
+//   passB_wide : T_k = Q~_k H̄ (MMA) -> F_W(k,:) = colsum(T_k ∘ P'_k) -> W-row ADMM (thread)
+//                -> N_k = T_k S_k (MMA recompute) -> M += N_k^T N_k, W̄^T W̄ (MMA)  (l.12-19, FIT)
+// Templates of the wide per-patient kernels; instantiated by k_polar_l*.cu and k_passB_m*.cu
+// (split so that the heavily unrolled instantiations compile in parallel).
+#pragma once
+#include <cstdlib>
+
+#include "copa_internal.cuh"
+
+namespace copa {
+
+__device__ __forceinline__ void dmma2(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// Prefetch the byte range [p, p + bytes) with the 32 lanes of a warp (128-byte lines).
+__device__ __forceinline__ void warp_prefetch(const void* p, size_t bytes, bool to_l1) {
+  const int lane = threadIdx.x & 31;
+  const char* c = (const char*)((uintptr_t)p & ~(uintptr_t)127);
+  const char* e = (const char*)p + bytes;
+  for (const char* x = c + 128 * lane; x < e; x += 128 * 32) {
+    if (to_l1) pf_l1(x); else pf_l2(x);
+  }
+}
+
+// Prefetch the state rows of patients [base, base + 32) (srow-contiguous) and their W rows.
+__device__ __forceinline__ void round_prefetch(int64_t base, int64_t K, int R, const int64_t* srow, const double* A,
+                                               const double* B, const double* Wrows, bool to_l1) {
+  if (base >= K) return;
+  int64_t last = base + 32 < K ? base + 32 : K;
+  int64_t s0 = srow[base], s1 = srow[last];
+  warp_prefetch(A + s0 * R, sizeof(double) * (size_t)((s1 - s0) * R), to_l1);
+  if (B) warp_prefetch(B + s0 * R, sizeof(double) * (size_t)((s1 - s0) * R), to_l1);
+  if (Wrows) warp_prefetch(Wrows + base * R, sizeof(double) * (size_t)((last - base) * R), to_l1);
+}
+
+// Givens insert of column vector c[0..L) into the upper-triangular Rf (L x L, registers).
+template <int L>
+__device__ __forceinline__ void givens_insert_reg(double (&Rf)[L][L], double (&c)[L]) {
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const double aj = c[j];
+    if (aj != 0.0) {
+      const double r = Rf[j][j];
+      const double n2 = fma(r, r, aj * aj);
+      const double inv = rsqrt(n2);
+      const double cs = r * inv, sn = aj * inv;
+      Rf[j][j] = n2 * inv;
+#pragma unroll
+      for (int t = j + 1; t < L; ++t) {
+        const double x = Rf[j][t], y = c[t];
+        Rf[j][t] = fma(cs, x, sn * y);
+        c[t] = fma(cs, y, -sn * x);
+      }
+    }
+  }
+}
+
+// One-sided Jacobi on the rows of Wm (L x L, registers) until mutually orthogonal. Round-robin
+// (tournament) ordering: every round rotates floor(L/2) disjoint row pairs, whose dot products and
+// rotation parameters are independent (instruction-level parallelism in the thread-per-patient
+// layout); a sweep (L-1 or L rounds) meets every pair once. Rotation of rows x, y with a = x.x,
+// b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
+// sn = cs t; x <- cs x - sn y, y <- sn x + cs y (the classical zeta = d/c form, Hestenes).
+template <int L>
+__device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
+  constexpr int N = (L % 2) ? L + 1 : L;  // players, with a dummy (index L) when L is odd
+  constexpr double eps = 2.220446049250313e-16 * (double)L;
+  constexpr double tol2 = eps * eps;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int rotated = 0;
+#pragma unroll
+    for (int rd = 0; rd < N - 1; ++rd) {
+      double cs[N / 2], sn[N / 2];
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const int p = i == 0 ? 0 : 1 + (i - 1 + rd) % (N - 1);
+        const int q = 1 + (N - 2 - i + rd) % (N - 1);
+        cs[i] = 1.0;
+        sn[i] = 0.0;
+        if (p < L && q < L) {
+          double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+          for (int x = 0; x < L; ++x) {
+            a = fma(Wm[p][x], Wm[p][x], a);
+            b = fma(Wm[q][x], Wm[q][x], b);
+            c = fma(Wm[p][x], Wm[q][x], c);
+          }
+          if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+            rotated = 1;
+            const double d = 0.5 * (b - a);
+            const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
+            cs[i] = rsqrt(fma(t, t, 1.0));
+            sn[i] = cs[i] * t;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const int p = i == 0 ? 0 : 1 + (i - 1 + rd) % (N - 1);
+        const int q = 1 + (N - 2 - i + rd) % (N - 1);
+        if (p < L && q < L) {
+#pragma unroll
+          for (int x = 0; x < L; ++x) {
+            const double u = Wm[p][x], v = Wm[q][x];
+            Wm[p][x] = fma(cs[i], u, -sn[i] * v);
+            Wm[q][x] = fma(sn[i], u, cs[i] * v);
+          }
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, rotated == 0)) break;
+  }
+}
+
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int kRing = 4;  // patients staged ahead (per warp) by the cp.async rings of the wide kernels
+
+// Per-warp ring of kRing patient records in shared memory, filled with cp.async (8-byte granules,
+// any alignment): record p holds nseg segments (segment j: len[j] doubles from src[j] + p stride[j]).
+// issue(p) copies record p into slot p % kRing as one commit group; wait() makes the oldest
+// outstanding record visible to the whole warp.
+template <int NSEG>
+struct WarpRing {
+  double* buf;
+  int per;                 // doubles per record
+  const double* src[NSEG];
+  int64_t stride[NSEG];
+  int len[NSEG];
+  __device__ __forceinline__ double* slot(int p) const { return buf + (p % kRing) * per; }
+  __device__ __forceinline__ void issue(int p, int np) {
+    if (p < np) {
+      const int lane = threadIdx.x & 31;
+      double* dst = slot(p);
+#pragma unroll
+      for (int j = 0; j < NSEG; ++j) {
+        const double* sp = src[j] + (int64_t)p * stride[j];
+        for (int x = lane; x < len[j]; x += 32) cpa8(dst + x, sp + x);
+        dst += len[j];
+      }
+    }
+    cpa_commit();
+  }
+};
+
+// Warp-cooperative A slab: slab[p][a][cc] = A_p(a, s = 8 nt + cc) for the round's patients.
+// A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps). Rows a >= m_p of
+// P'_p are zero (never written), so only a < l is checked. P'_p and w̄_p arrive through the warp's
+// cp.async ring, kRing patients ahead of the MMAs.
+template <int MT, int KS>
+__device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, int R, const double* Pp,
+                                       const double* W, const double* Hs, double* slab, double* ringbuf) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int s = 8 * nt + g;
+  double hb[KS];
+  int offp[KS][MT];  // lane's fragment offsets inside a patient's P' block (-1: outside)
+  int offw[KS];
+  const int lR = l * R;
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks) {
+    const int r = 4 * ks + t;
+    hb[ks] = (r < R && s < R) ? Hs[s * R + r] : 0.0;  // B[t][g] = H^T(r, s)
+    offw[ks] = r < R ? lR + r : -1;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int a = 8 * mt + g;
+      offp[ks][mt] = (a < l && r < R) ? a * R + r : -1;
+    }
+  }
+  const int np = (int)(K - base < 32 ? K - base : 32);
+  WarpRing<2> ring;
+  ring.buf = ringbuf;
+  ring.per = lR + R;
+  ring.src[0] = Pp + base * lR;
+  ring.stride[0] = lR;
+  ring.len[0] = lR;
+  ring.src[1] = W + base * R;
+  ring.stride[1] = R;
+  ring.len[1] = R;
+#pragma unroll
+  for (int p = 0; p < kRing; ++p) ring.issue(p, np);
+  for (int p = 0; p < np; ++p) {
+    cpa_wait<kRing - 1>();
+    __syncwarp();
+    const double* rec = ring.slot(p);
+    double c[MT][2];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const double wr = offw[ks] >= 0 ? rec[offw[ks]] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double av = offp[ks][mt] >= 0 ? rec[offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+        dmma2(c[mt][0], c[mt][1], av, hb[ks]);
+      }
+    }
+    double* sp = slab + (p * MT * 8 + g) * 8 + 2 * t;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) *reinterpret_cast<double2*>(sp + mt * 64) = make_double2(c[mt][0], c[mt][1]);
+    __syncwarp();  // slot p fully read before it is refilled
+    ring.issue(p + kRing, np);
+  }
+  cpa_wait<0>();
+  for (int p = np; p < 32; ++p)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+      *reinterpret_cast<double2*>(slab + (p * MT * 8 + 8 * mt + g) * 8 + 2 * t) = make_double2(0.0, 0.0);
+}
+
+template <int L, int MT, int NT, int RT, int LT>
+__global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict__ m, int64_t K, int R_, int l_,
+                                                       const double* __restrict__ Pp, const double* __restrict__ W,
+                                                       const double* __restrict__ Hg, double tau,
+                                                       double* __restrict__ Qt, int32_t* __restrict__ rank,
+                                                       double* __restrict__ FHwarp) {
+  constexpr int KS = (NT * 8 + 3) / 4;  // r steps of 4 covering 8 NT >= R
+  constexpr int RP = 8 * NT;
+  const int R = RT ? RT : R_;           // compile-time for the configured (R, l) pairs
+  const int l = LT ? LT : l_;
+  extern __shared__ double sm[];
+  const int hoff = ((R * R + 31) / 32) * 32;
+  double* Hs = sm;                                      // R x R
+  const int wib = threadIdx.x >> 5;
+  const int ringd = kRing * (2 * l * R + R);           // per warp: cp.async ring (doubles)
+  double* slab = sm + hoff + wib * (32 * MT * 8 * 8 + ringd);  // per warp: 32 patients x (MT 8) x 8
+  double* ringbuf = slab + 32 * MT * 8 * 8;
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) Hs[x] = Hg[x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
+  const int64_t rounds = (K + 31) / 32;
+  const int64_t pstride = (int64_t)l * R;
+  // this warp's F_H partial (RP x RP, MMA fragment order), accumulated round by round
+  double* fhw = FHwarp + ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * (RP * RP) + lane;
+#pragma unroll
+  for (int x = 0; x < NT * NT * 2; ++x) fhw[32 * x] = 0.0;
+  for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
+    const int64_t base = rd * 32;
+    {  // prefetch the next round's P' and W rows into L2
+      const int64_t nb = base + 32 * (int64_t)nwarps_total;
+      if (nb < K) {
+        const int64_t nl = nb + 32 < K ? nb + 32 : K;
+        warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)((nl - nb) * pstride), false);
+        warp_prefetch(W + nb * R, sizeof(double) * (size_t)((nl - nb) * R), false);
+      }
+    }
+    const int64_t kme = base + lane;
+    const int mme = kme < K ? m[kme] : 0;
+    // ---- Givens QR of A^T (rows of A^T = columns of A), slab by slab
+    double Rf[L][L];
+#pragma unroll
+    for (int i = 0; i < L; ++i)
+#pragma unroll
+      for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
+    for (int nt = 0; nt < NT; ++nt) {
+      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf);
+      __syncwarp();
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        if (8 * nt + cc < R) {
+          double col[L];
+#pragma unroll
+          for (int a = 0; a < L; ++a) col[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+          givens_insert_reg<L>(Rf, col);
+        }
+      }
+      __syncwarp();
+    }
+    // ---- SVD of the m x m factor: rows of Rf -> sigma_j v_j; u_j = v_j / sqrt(sigma_j) so that
+    //      K = sum_kept u_j u_j^T = V Σ^-1 V^T on the numerical range (reading R-polar-2/3)
+    jacobi_rows_reg<L>(Rf);
+    double smax = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
+      smax = fmax(smax, s);
+    }
+    smax = sqrt(smax);
+    int rk = 0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
+      const double sg = sqrt(s);
+      const bool keep = smax > 0.0 && sg > tau * smax;
+      rk += keep ? 1 : 0;
+      const double sc = keep ? 1.0 / (sg * sqrt(sg)) : 0.0;
+#pragma unroll
+      for (int i = 0; i < L; ++i) Rf[j][i] *= sc;
+    }
+    if (kme < K) rank[kme] = mme > 0 ? rk : 0;
+    // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
+    for (int nt = 0; nt < NT; ++nt) {
+      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf);
+      __syncwarp();
+      if (kme < K && mme > 0) {
+        double* Q = Qt + kme * pstride;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const int s = 8 * nt + cc;
+          if (s < R) {
+            double y[L];
+#pragma unroll
+            for (int a = 0; a < L; ++a) y[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+            double q[L];
+#pragma unroll
+            for (int a = 0; a < L; ++a) q[a] = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) {
+              double d = 0.0;
+#pragma unroll
+              for (int a = 0; a < L; ++a) d = fma(Rf[j][a], y[a], d);
+#pragma unroll
+              for (int a = 0; a < L; ++a) q[a] = fma(Rf[j][a], d, q[a]);
+            }
+#pragma unroll
+            for (int a = 0; a < L; ++a)
+              if (a < mme) Q[a * R + s] = q[a];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // ---- F_H += Q~_p^T (P'_p S_p): MMA with M = r, N = s, K = a (rows a >= m_p are zero)
+    {
+      int offq[2 * MT][NT];
+      int offw[NT];
+#pragma unroll
+      for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+        for (int i = 0; i < NT; ++i) {
+          const int a = 4 * ks + t, rr = 8 * i + g;
+          offq[ks][i] = (a < l && rr < R) ? a * R + rr : -1;
+        }
+#pragma unroll
+      for (int i = 0; i < NT; ++i) offw[i] = 8 * i + g < R ? 8 * i + g : -1;
+      double fh[NT][NT][2];
+#pragma unroll
+      for (int a = 0; a < NT; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
+      const int np = (int)(K - base < 32 ? K - base : 32);
+      const int lR = l * R;
+      WarpRing<3> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R)
+      ring.buf = ringbuf;
+      ring.per = 2 * lR + R;
+      ring.src[0] = Qt + base * lR;
+      ring.stride[0] = lR;
+      ring.len[0] = lR;
+      ring.src[1] = Pp + base * lR;
+      ring.stride[1] = lR;
+      ring.len[1] = lR;
+      ring.src[2] = W + base * R;
+      ring.stride[2] = R;
+      ring.len[2] = R;
+#pragma unroll
+      for (int p = 0; p < kRing; ++p) ring.issue(p, np);
+      for (int p = 0; p < np; ++p) {
+        cpa_wait<kRing - 1>();
+        __syncwarp();
+        const double* rec = ring.slot(p);
+        double wv[NT];
+#pragma unroll
+        for (int i = 0; i < NT; ++i) wv[i] = offw[i] >= 0 ? rec[2 * lR + offw[i]] : 0.0;
+        double af[2 * MT][NT], bf[2 * MT][NT];
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            af[ks][i] = offq[ks][i] >= 0 ? rec[offq[ks][i]] : 0.0;               // A[g][t] = Q~^T(r, a)
+            bf[ks][i] = offq[ks][i] >= 0 ? rec[lR + offq[ks][i]] * wv[i] : 0.0;  // B[t][g] = (P'S)(a, s)
+          }
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks)
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma2(fh[i][j][0], fh[i][j][1], af[ks][i], bf[ks][j]);
+        __syncwarp();
+        ring.issue(p + kRing, np);
+      }
+      cpa_wait<0>();
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) fhw[32 * ((i * NT + j) * 2 + c)] += fh[i][j][c];
+    }
+  }
+}
+
+// F_H = sum over warps (fixed order) of the fragment-ordered partials
+static __global__ void k_sum_fh(const double* __restrict__ part, int nw, int R, int NT, double* __restrict__ FH) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= R * R) return;
+  const int r = x / R, s = x - r * R;
+  // fragment position of (r, s): tile (i = r/8, j = s/8), lane g = r%8, t = (s%8)/2, c = s%2
+  const int i = r >> 3, j = s >> 3, g = r & 7, t = (s & 7) >> 1, c = s & 1;
+  const int off = 32 * ((i * NT + j) * 2 + c) + g * 4 + t;
+  const int rp2 = 64 * NT * NT;
+  double v = 0.0;
+  for (int w = 0; w < nw; ++w) v += part[(int64_t)w * rp2 + off];
+  FH[x] = v;
+}
+
+static __global__ void k_sum_rr(const double* part, int nb, int n, double* out) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * n + x];
+  out[x] = s;
+}
+
+constexpr int kDenseThreads = 128;
+
+template <int L, int NT, int RT = 0, int LT = 0>
+static void polar_wide_inst(Handle& h) {
+  constexpr int MT = (L + 7) / 8;
+  auto fn = k_polar_wide<L, MT, NT, RT, LT>;
+  const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
+  const size_t per_warp = (size_t)(32 * MT * 8 * 8 + kRing * (2 * h.l * h.R + h.R));
+  int wpb = kDenseThreads / 32;  // warps per block: fewer when the per-warp slab + ring is large
+  while (wpb > 1 && sizeof(double) * (hoff + wpb * per_warp) > 227 * 1024) wpb /= 2;
+  const int threads = 32 * wpb;
+  size_t smem = sizeof(double) * (hoff + wpb * per_warp);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  int64_t rounds = (h.K + 31) / 32;
+  int64_t blocks = (rounds + wpb - 1) / wpb;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+  if (const char* e = getenv("COPA_POLAR_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
+  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  if (cap > kPartBlocks * 4 / wpb) cap = kPartBlocks * 4 / wpb;  // fh_warp holds kPartBlocks x 4 warps
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, threads, smem, h.stream>>>(h.m, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
+                                                    h.fh_warp);
+  const int RR = h.R * h.R;
+  k_sum_fh<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.fh_warp, (int)blocks * wpb, h.R, NT, h.FH);
+}
+
+template <int L>
+static void polar_wide_n(Handle& h) {
+  // compile-time (R, l) for the BASELINE configs (Medium, Large, Scale); generic otherwise
+  if (L == 7 && h.l == 7 && h.R == 20) { polar_wide_inst<7, 3, 20, 7>(h); return; }
+  if (L == 7 && h.l == 7 && h.R == 15) { polar_wide_inst<7, 2, 15, 7>(h); return; }
+  if (L == 9 && h.l == 9 && h.R == 40) { polar_wide_inst<9, 5, 40, 9>(h); return; }
+  switch ((h.R + 7) / 8) {
+    case 1: polar_wide_inst<L, 1>(h); break;
+    case 2: polar_wide_inst<L, 2>(h); break;
+    case 3: polar_wide_inst<L, 3>(h); break;
+    case 4: polar_wide_inst<L, 4>(h); break;
+    case 5: polar_wide_inst<L, 5>(h); break;
+    case 6: polar_wide_inst<L, 6>(h); break;
+    case 7: polar_wide_inst<L, 7>(h); break;
+    default: polar_wide_inst<L, 8>(h); break;
+  }
+}
+
+// ------------------------------------------------------------------ pass B (wide): F_W, W ADMM, N, M, W^T W
+// Per patient p of a warp round (one MMA tile set per patient, the next patient's fragments loaded
+// while the current one's MMAs run):
+//   T_p = Q~_p H̄ (MMA: M = a, N = r, K = i), F_W(p, r) = sum_a T_p(a, r) P'_p(a, r)   (Alg.1 l.12, W mode)
+// thread per patient: 5 ADMM row steps z = Ginv (f + rho (w̄ + d)), w̄ = prox(z - d), d += w̄ - z with
+//   Ginv = (G_W + rho I)^-1 formed once from the cached Cholesky factor (k_admm_H)          (l.13-19)
+//   N_p = T_p S_p (new w̄_p) -> HBM, M += N_p^T N_p (MMA via the warp's smem scratch), W̄^T W̄ += w̄ w̄^T
+template <int MT, int NT, int RT, int LT>
+__global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, const double* __restrict__ Pp,
+                                                    const double* __restrict__ Qt, const double* __restrict__ Hg,
+                                                    const double* __restrict__ GWi, const double* __restrict__ scal,
+                                                    int n_inner, int kind, double param, double* __restrict__ W,
+                                                    double* __restrict__ DW, double* __restrict__ Nst,
+                                                    double* __restrict__ part /* [blocks][2][R R] */) {
+  constexpr int RP = 8 * NT;
+  constexpr int KS = (NT * 8 + 3) / 4;  // i steps of 4 covering 8 NT >= R
+  const int R = RT ? RT : R_;
+  const int l = LT ? LT : l_;
+  extern __shared__ double sm[];
+  const int hoff = ((R * R + 31) / 32) * 32;
+  double* Hs = sm;                 // R x R
+  double* Gs = sm + hoff;          // R x R  (G_W + rho I)^-1
+  const int wib = threadIdx.x >> 5;
+  double* wv = sm + 2 * hoff + wib * (3 * RP * 32 + MT * 8 * RP);  // per warp: fw, w̄, d as [r][lane] + N scratch
+  double* fwv = wv;
+  double* wbv = wv + RP * 32;
+  double* dv = wv + 2 * RP * 32;
+  double* ns = wv + 3 * RP * 32;   // N_p (MT 8 x RP)
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Gs[x] = GWi[x]; }
+  __syncthreads();
+  const double rho = scal[S_RHO_W];
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nwarps_total = gridDim.x * (blockDim.x >> 5);
+  const int64_t rounds = (K + 31) / 32;
+  const int64_t pstride = (int64_t)l * R;
+  // lane-constant fragment offsets (-1: padding)
+  int offq[KS][MT];   // A[g][t] = Q~(a = 8 mt + g, i = 4 ks + t)
+  int offp[MT][NT][2];  // C-layout (a = 8 mt + g, r = 8 nt + 2 t + c)
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) {
+      const int a = 8 * mt + g, i = 4 * ks + t;
+      offq[ks][mt] = (a < l && i < R) ? a * R + i : -1;
+    }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int a = 8 * mt + g, r = 8 * nt + 2 * t + c;
+        offp[mt][nt][c] = (a < l && r < R) ? a * R + r : -1;
+      }
+  double hb[KS][NT];  // B[t][g] = H̄(i = 4 ks + t, r = 8 nt + g), kept in registers
+#pragma unroll
+  for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int i = 4 * ks + t, r = 8 * nt + g;
+      hb[ks][nt] = (i < R && r < R) ? Hs[i * R + r] : 0.0;
+    }
+  auto load_q = [&](const double* Q, double (&f)[KS][MT]) {
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) f[ks][mt] = offq[ks][mt] >= 0 ? Q[offq[ks][mt]] : 0.0;
+  };
+  auto t_mma = [&](const double (&f)[KS][MT], double (&c)[MT][NT][2]) {
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) c[mt][nt][0] = c[mt][nt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) dmma2(c[mt][nt][0], c[mt][nt][1], f[ks][mt], hb[ks][nt]);
+  };
+  double macc[NT][NT][2], wacc[NT][NT][2];
+#pragma unroll
+  for (int a = 0; a < NT; ++a)
+#pragma unroll
+    for (int b = 0; b < NT; ++b) macc[a][b][0] = macc[a][b][1] = wacc[a][b][0] = wacc[a][b][1] = 0.0;
+  for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
+    const int64_t base = rd * 32;
+    const int np = (int)(K - base < 32 ? K - base : 32);
+    {  // this round's rows into L1, the next round's into L2
+      warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+      warp_prefetch(Qt + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+      warp_prefetch(W + base * R, sizeof(double) * (size_t)(np * R), true);
+      warp_prefetch(DW + base * R, sizeof(double) * (size_t)(np * R), true);
+      const int64_t nb = base + 32 * (int64_t)nwarps_total;
+      if (nb < K) {
+        const int64_t nn = K - nb < 32 ? K - nb : 32;
+        warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
+        warp_prefetch(Qt + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
+      }
+    }
+    // ---- F_W rows: F_W(p, r) = sum_a T_p(a, r) P'_p(a, r)
+    {
+      const double* Q = Qt + base * pstride;
+      const double* P = Pp + base * pstride;
+      double fq[KS][MT];
+      load_q(Q, fq);
+      for (int p = 0; p < np; ++p) {
+        double pv[MT][NT][2];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) pv[mt][nt][c] = offp[mt][nt][c] >= 0 ? P[offp[mt][nt][c]] : 0.0;
+        double c[MT][NT][2];
+        t_mma(fq, c);
+        Q += pstride;
+        P += pstride;
+        if (p + 1 < np) load_q(Q, fq);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            double sv = 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) sv = fma(c[mt][nt][i], pv[mt][nt][i], sv);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 4);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 8);
+            sv += __shfl_xor_sync(0xffffffffu, sv, 16);
+            if (g == 0) fwv[(8 * nt + 2 * t + i) * 32 + p] = sv;
+          }
+      }
+    }
+    __syncwarp();
+    // ---- W-row ADMM (thread = patient)
+    const int64_t kme = base + lane;
+    if (kme < K) {
+      for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
+      for (int it = 0; it < n_inner; ++it) {
+        double rhs[RP];
+#pragma unroll
+        for (int r = 0; r < RP; ++r)
+          rhs[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          if (r < R) {
+            double z = 0.0;
+#pragma unroll
+            for (int q = 0; q < RP; ++q)
+              if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
+            const double d0 = dv[r * 32 + lane];
+            const double nb = prox(kind, param, rho, z - d0);
+            dv[r * 32 + lane] = d0 + nb - z;
+            wbv[r * 32 + lane] = nb;
+          }
+        }
+      }
+      for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
+    } else {
+      for (int r = 0; r < R; ++r) wbv[r * 32 + lane] = 0.0;
+    }
+    __syncwarp();
+    // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T  (MMA with K = patients)
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int p = 4 * ks + t;
+      double af[NT];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int r = 8 * i + g;
+        af[i] = r < R ? wbv[r * 32 + p] : 0.0;  // A[g][t] = w̄_p(r) ; B[t][g] = w̄_p(s) (same values)
+      }
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma2(wacc[i][j][0], wacc[i][j][1], af[i], af[j]);
+    }
+    // ---- N_p = T_p S_p (new w̄_p) -> HBM; M += N_p^T N_p
+    {
+      const double* Q = Qt + base * pstride;
+      double* Nrow = Nst + base * pstride;
+      double fq[KS][MT];
+      load_q(Q, fq);
+      for (int p = 0; p < np; ++p) {
+        double c[MT][NT][2];
+        t_mma(fq, c);
+        Q += pstride;
+        if (p + 1 < np) load_q(Q, fq);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            double v[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int r = 8 * nt + 2 * t + i;
+              v[i] = r < R ? c[mt][nt][i] * wbv[r * 32 + p] : 0.0;
+              if (offp[mt][nt][i] >= 0) Nrow[offp[mt][nt][i]] = v[i];
+            }
+            *reinterpret_cast<double2*>(ns + (8 * mt + g) * RP + 8 * nt + 2 * t) = make_double2(v[0], v[1]);
+          }
+        __syncwarp();
+        // M += N^T N: A[g][t] = N(a = 4 ks + t, r = 8 i + g), B[t][g] = N(a, s = 8 j + g)
+#pragma unroll
+        for (int ks = 0; ks < 2 * MT; ++ks) {
+          const int a = 4 * ks + t;
+          double af[NT];
+#pragma unroll
+          for (int i = 0; i < NT; ++i) af[i] = a < l ? ns[a * RP + 8 * i + g] : 0.0;
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma2(macc[i][j][0], macc[i][j][1], af[i], af[j]);
+        }
+        __syncwarp();
+        Nrow += pstride;
+      }
+    }
+  }
+  __syncthreads();
+  double* red = sm + 2 * hoff;  // reuse: warps x 2 x RP^2
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        red[(wib * 2 + 0) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = macc[i][j][c];
+        red[(wib * 2 + 1) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = wacc[i][j][c];
+      }
+  __syncthreads();
+  for (int x = threadIdx.x; x < 2 * R * R; x += blockDim.x) {
+    const int which = x / (R * R), y = x - which * R * R;
+    const int r = y / R, s2 = y - r * R;
+    double v = 0.0;
+    for (int ww = 0; ww < nw; ++ww) v += red[(ww * 2 + which) * RP * RP + r * RP + s2];
+    part[((int64_t)blockIdx.x * 2 + which) * R * R + y] = v;
+  }
+}
+
+static __global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, double* WtW) {
+  int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 2 * RR) return;
+  int which = x / RR, y = x - which * RR;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[((int64_t)b * 2 + which) * RR + y];
+  (which == 0 ? M : WtW)[y] = s;
+}
+
+template <int MT, int NT, int RT = 0, int LT = 0>
+static void passB_wide_inst(Handle& h) {
+  constexpr int RP = 8 * NT;
+  auto fn = k_passB_wide<MT, NT, RT, LT>;
+  const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
+  size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32 + MT * 8 * RP);
+  size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
+  size_t smem = sizeof(double) * 2 * hoff + (per_warp * (kDenseThreads / 32) > red ? per_warp * (kDenseThreads / 32) : red);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  int64_t rounds = (h.K + 31) / 32;
+  int64_t blocks = (rounds + 3) / 4;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, smem);
+  if (const char* e = getenv("COPA_PASSB_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
+  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  if (cap > kPartBlocks) cap = kPartBlocks;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.K, h.R, h.l, h.Pp, h.Qt, h.H, h.GWi, h.scal,
+                                                         h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
+                                                         h.Nst, h.partial);
+  const int RR = h.R * h.R;
+  k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
+}
+
+template <int MT>
+static void passB_wide_n(Handle& h) {
+  if (MT == 1 && h.l == 7 && h.R == 20) { passB_wide_inst<1, 3, 20, 7>(h); return; }
+  if (MT == 1 && h.l == 7 && h.R == 15) { passB_wide_inst<1, 2, 15, 7>(h); return; }
+  if (MT == 2 && h.l == 9 && h.R == 40) { passB_wide_inst<2, 5, 40, 9>(h); return; }
+  switch ((h.R + 7) / 8) {
+    case 1: passB_wide_inst<MT, 1>(h); break;
+    case 2: passB_wide_inst<MT, 2>(h); break;
+    case 3: passB_wide_inst<MT, 3>(h); break;
+    case 4: passB_wide_inst<MT, 4>(h); break;
+    case 5: passB_wide_inst<MT, 5>(h); break;
+    case 6: passB_wide_inst<MT, 6>(h); break;
+    case 7: passB_wide_inst<MT, 7>(h); break;
+    default: passB_wide_inst<MT, 8>(h); break;
+  }
+}
+
+// F_W + W-ADMM + N + M + W^T W for smooth patients (m_k <= l <= 16). Returns kernels launched.
+}  // namespace copa
