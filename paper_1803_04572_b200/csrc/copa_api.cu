@@ -88,7 +88,10 @@ size_t carve(Handle& h, char* base) {
     h.order = c.take<int32_t>(h.K);
     h.perm = c.take<int32_t>(h.J);
     h.inv = c.take<int32_t>(h.Jl);
-    h.Vl = c.take<double>(h.Jl * R);
+    h.Vl = c.take<double>(h.Jl * R + 64);  // +64: unpredicated pass-A gathers past the last row
+    h.fa_col = c.take<int32_t>(h.F + 64);
+    h.fa_val = c.take<double>((h.F + 64) * h.l);
+    h.pa_wk = c.take<int64_t>(h.pa_nw + 1);
     h.block_k = c.take<int64_t>(h.sc_ranges + 1);
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
@@ -151,7 +154,10 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   h.R = p->R;
   h.S = h.smooth ? h.K * h.l : h.rows;
   h.Jl = h.J;
-  if (h.smooth) plan_scatter(h);
+  if (h.smooth) {
+    plan_scatter(h);
+    plan_passA(h);
+  }
 }
 
 copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
@@ -309,10 +315,25 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
                "cta_st");
       CUDA_TRY(cudaMemcpyAsync(h.block_k, block_k.data(), sizeof(int64_t) * block_k.size(), cudaMemcpyHostToDevice, s),
                "block_k");
+      {  // pass-A warp ranges (fiber-balanced) from the per-patient fiber counts
+        std::vector<int64_t> fp((size_t)h.K + 1, 0), wk;
+        for (int64_t k = 0; k < h.K; ++k) {
+          int64_t c = 0;
+          for (int g = 0; g < G; ++g) c += gcnt[(size_t)g * h.K + k];
+          fp[(size_t)k + 1] = fp[(size_t)k] + c;
+        }
+        plan_passA_ranges(h, fp, wk);
+        CUDA_TRY(cudaMemcpyAsync(h.pa_wk, wk.data(), sizeof(int64_t) * wk.size(), cudaMemcpyHostToDevice, s), "pa_wk");
+        CUDA_TRY(cudaStreamSynchronize(s), "pa_wk sync");
+      }
       CUDA_TRY(cudaStreamSynchronize(s), "layout sync");  // host vectors go out of scope
     }
     launch_basis(h);
     launch_build_fibers(h);
+    cudaMemsetAsync(h.fa_col + h.F, 0, 64 * sizeof(int32_t), s);  // slack read by the pass-A chunk grid
+    cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
+    cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
+    launch_layoutA(h);
     build_fiber_layout(h, h.layout_tmp, h.layout_tmp_bytes);
   } else {
     launch_row_patient(h);

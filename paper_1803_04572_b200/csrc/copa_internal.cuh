@@ -59,7 +59,13 @@ struct Handle {
   int32_t* order;        // [K] patients by fiber count, descending
   int32_t* perm;         // [J] feature -> label
   int32_t* inv;          // [Jl] label -> feature (-1: unused label)
-  double* Vl;            // [Jl x R] V̄ in label order (pass A gathers when V̄ does not fit in smem)
+  double* Vl;            // [Jl x R] V̄ in label order (pass A)
+  int32_t* fa_col;       // pass A layout: patient k's fibers at [fiber_ptr[k], fiber_ptr[k+1]) (+64 slack)
+  double* fa_val;
+  int64_t* pa_wk;        // [pa_nw + 1] patient range of each pass-A warp (fiber-balanced)
+  int64_t pa_nw = 0;
+  int pa_ctas = 0;
+  bool pa_vs = false;    // V̄ in shared memory in pass A
   int64_t* block_k;      // [sc_ranges+1] patient range of each pass-B range
   double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
   unsigned long long* fhist;  // [J] fibers per feature (init)
@@ -217,7 +223,11 @@ int launch_fit(Handle& h);
 int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
 void launch_U(Handle& h, double* U);
 // fiber passes (k_fibers.cu)
-void launch_spmm_fibers(Handle& h);
+void launch_spmm_fibers(Handle& h);   // pass A (k_passA.cu)
+void launch_relabel_V(Handle& h);
+void launch_layoutA(Handle& h);
+void plan_passA(Handle& h);
+void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
 int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);

@@ -85,120 +85,8 @@ __device__ __forceinline__ uint32_t bulk_g2s_span(void* dst, const void* src, si
   return shift;
 }
 
-// ------------------------------------------------------------------ pass A
-template <int MT>
-struct TileA {  // one k-step pair (8 fibers) of pass A: lane's fiber f = fb + 4 s + t
-  double a[2][MT];
-  int32_t col[2];
-};
-
-template <int MT>
-__device__ __forceinline__ void load_tile_a(TileA<MT>& T, int64_t fb, int64_t f1, int l, const int32_t* fiber_col,
-                                            const double* fiber_val) {
-  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int s = 0; s < 2; ++s) {
-    const int64_t f = fb + 4 * s + t;
-    const bool ok = f < f1;
-    T.col[s] = ok ? __ldg(fiber_col + f) : -1;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int a = mt * 8 + g;
-      T.a[s][mt] = (ok && a < l) ? __ldg(fiber_val + f * l + a) : 0.0;
-    }
-  }
-}
-
-template <int MT, int NT, bool VSMEM>
-__global__ void __launch_bounds__(512) k_spmm_mma(const int64_t* __restrict__ gptr, int G,
-                                                  const int32_t* __restrict__ fiber_col,
-                                                  const double* __restrict__ fiber_val, const int32_t* __restrict__ m,
-                                                  const int32_t* __restrict__ order, const int32_t* __restrict__ inv,
-                                                  int64_t K, int l, int R, int64_t Jl, const double* __restrict__ Vg,
-                                                  const double* __restrict__ Vl, double* __restrict__ Pp,
-                                                  int* counter) {
-  extern __shared__ double smem_v[];
-  if (VSMEM) {
-    for (int64_t x = threadIdx.x; x < Jl * R; x += blockDim.x) {
-      const int64_t nj = x / R, r = x - nj * R;
-      const int32_t j = inv[nj];
-      smem_v[x] = j >= 0 ? Vg[(int64_t)j * R + r] : 0.0;
-    }
-    __syncthreads();
-  }
-  const double* Vs = VSMEM ? smem_v : Vl;
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int64_t K1 = K + 1;
-  // lanes < G hold [start, end) of the current / next patient's run in stream `lane`
-  auto grab = [&](int64_t& kk, int64_t& s0, int64_t& s1) {
-    int idx = 0;
-    if (lane == 0) idx = atomicAdd(counter, 1);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    kk = idx < K ? order[idx] : -1;
-    s0 = s1 = 0;
-    if (kk >= 0 && lane < G) {
-      s0 = gptr[lane * K1 + kk];
-      s1 = gptr[lane * K1 + kk + 1];
-      l2_prefetch(fiber_col + s0, sizeof(int32_t) * (size_t)(s1 - s0));
-      l2_prefetch(fiber_val + s0 * l, sizeof(double) * (size_t)((s1 - s0) * l));
-    }
-  };
-  int64_t k, c0, c1;
-  grab(k, c0, c1);
-  while (k >= 0) {
-    int64_t kn, n0, n1;
-    grab(kn, n0, n1);
-    double acc[MT][NT][2];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-    for (int gg = 0; gg < G; ++gg) {
-      const int64_t f0 = __shfl_sync(0xffffffffu, c0, gg), f1 = __shfl_sync(0xffffffffu, c1, gg);
-      if (f0 >= f1) continue;
-      TileA<MT> cur;
-      load_tile_a<MT>(cur, f0, f1, l, fiber_col, fiber_val);
-      for (int64_t fb = f0; fb < f1; fb += 8) {
-        TileA<MT> nxt;
-        if (fb + 8 < f1) load_tile_a<MT>(nxt, fb + 8, f1, l, fiber_col, fiber_val);
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          double bfr[NT];
-          const int64_t j = cur.col[s];
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const int r = nt * 8 + g;
-            bfr[nt] = (j >= 0 && r < R) ? (VSMEM ? Vs[j * R + r] : __ldg(Vs + j * R + r)) : 0.0;
-          }
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], cur.a[s][mt], bfr[nt]);
-        }
-        cur = nxt;
-      }
-    }
-    const int mk = m[k];
-    double* out = Pp + k * l * R;  // smooth state rows: srow[k] = k * l
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) {
-      const int a = mt * 8 + g;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = nt * 8 + 2 * t + i;
-          if (a < mk && r < R) out[a * R + r] = acc[mt][nt][i];
-        }
-    }
-    k = kn;
-    c0 = n0;
-    c1 = n1;
-  }
-}
-
-// V̄ in label order for the global-gather variant of pass A.
+// ------------------------------------------------------------------ V̄ in label order
+// (pass A, k_passA.cu, gathers V̄ rows by fiber label)
 __global__ void k_relabel_V(const double* V, const int32_t* inv, int64_t Jl, int R, double* Vl) {
   int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x >= Jl * R) return;
@@ -207,50 +95,9 @@ __global__ void k_relabel_V(const double* V, const int32_t* inv, int64_t Jl, int
   Vl[x] = j >= 0 ? V[(int64_t)j * R + r] : 0.0;
 }
 
-template <int MT, int NT, bool VS>
-static void spmm_inst(Handle& h, int smem_bytes) {
-  auto fn = k_spmm_mma<MT, NT, VS>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 512, smem_bytes);
-  if (per_sm < 1) per_sm = 1;
-  if (!VS) {
-    const int64_t n = h.Jl * h.R;
-    k_relabel_V<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.V, h.inv, h.Jl, h.R, h.Vl);
-  }
-  cudaMemsetAsync(h.counter, 0, sizeof(int), h.stream);
-  fn<<<148 * per_sm, 512, smem_bytes, h.stream>>>(h.gptr, h.sc_G, h.fiber_col, h.fiber_val, h.m, h.order, h.inv,
-                                                   h.K, h.l, h.R, h.Jl, h.V, h.Vl, h.Pp, h.counter);
-}
-
-template <int MT, int NT>
-static void spmm_dispatch_v(Handle& h) {
-  size_t vbytes = sizeof(double) * (size_t)(h.Jl * h.R);
-  if (vbytes <= 200 * 1024 && !getenv("COPA_SPMM_VGLOBAL")) spmm_inst<MT, NT, true>(h, (int)vbytes);
-  else spmm_inst<MT, NT, false>(h, 0);
-}
-
-template <int MT>
-static void spmm_dispatch_n(Handle& h) {
-  switch ((h.R + 7) / 8) {
-    case 1: spmm_dispatch_v<MT, 1>(h); break;
-    case 2: spmm_dispatch_v<MT, 2>(h); break;
-    case 3: spmm_dispatch_v<MT, 3>(h); break;
-    case 4: spmm_dispatch_v<MT, 4>(h); break;
-    case 5: spmm_dispatch_v<MT, 5>(h); break;
-    case 6: spmm_dispatch_v<MT, 6>(h); break;
-    case 7: spmm_dispatch_v<MT, 7>(h); break;
-    default: spmm_dispatch_v<MT, 8>(h); break;
-  }
-}
-
-void launch_spmm_fibers(Handle& h) {
-  if (h.l <= 8) spmm_dispatch_n<1>(h);
-  else spmm_dispatch_n<2>(h);
+void launch_relabel_V(Handle& h) {
+  const int64_t n = h.Jl * h.R;
+  k_relabel_V<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.V, h.inv, h.Jl, h.R, h.Vl);
 }
 
 // ------------------------------------------------------------------ pass B (TMA-staged scatter)
