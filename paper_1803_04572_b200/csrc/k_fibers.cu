@@ -351,10 +351,9 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-template <int KS, int NT>
-static void scatter_inst(Handle& h) {
-  constexpr int W = kScW;
-  auto fn = k_scatter_tma<KS, NT, W, 2>;
+template <int KS, int NT, int W, int TB>
+static void scatter_inst_w(Handle& h) {
+  auto fn = k_scatter_tma<KS, NT, W, TB>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -367,6 +366,12 @@ static void scatter_inst(Handle& h) {
                                                    getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
+}
+
+template <int KS, int NT>
+static void scatter_inst(Handle& h) {
+  if (h.sc_W == 2) scatter_inst_w<KS, NT, 2, 4>(h);
+  else scatter_inst_w<KS, NT, 4, 2>(h);
 }
 
 template <int KS>
@@ -397,13 +402,16 @@ int launch_scatter_fibers(Handle& h) {
 // ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared memory.
 void plan_scatter(Handle& h) {
   const size_t budget = 225 * 1024;
-  h.sc_W = kScW;  // label sub-ranges per group = consumer warps of k_scatter_tma
+  h.sc_W = kScW;  // label sub-ranges per group = consumer warps of k_scatter_tma (2 or 4)
+  if (getenv("COPA_SC_W")) h.sc_W = atoi(getenv("COPA_SC_W")) == 2 ? 2 : 4;
   h.sc_RS = (h.R + 1) & ~1;
   h.sc_FB = 256;
   h.sc_ok = 0;
   const int pbs[3] = {16, 8, 4};
+  const int gmin = getenv("COPA_SC_GMIN") ? atoi(getenv("COPA_SC_GMIN")) : 1;  // tuning experiments
+  if (getenv("COPA_SC_FB")) h.sc_FB = atoi(getenv("COPA_SC_FB"));
   for (int pass = 0; pass < 2 && !h.sc_ok; ++pass)  // pass 0: >= 3 stages of >= 8 patients
-    for (int G = 1; G <= kMaxGroups && !h.sc_ok; ++G) {
+    for (int G = gmin; G <= kMaxGroups && !h.sc_ok; ++G) {
       const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
       const int64_t Jg = Js * h.sc_W;
       const size_t fs = ((size_t)Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
