@@ -11,6 +11,7 @@
 // Templates of the wide per-patient kernels; instantiated by k_polar_l*.cu and k_passB_m*.cu
 // (split so that the heavily unrolled instantiations compile in parallel).
 #pragma once
+#include <algorithm>
 #include <cstdlib>
 
 #include "copa_internal.cuh"
@@ -136,40 +137,94 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 
 constexpr int kRing = 4;  // patients staged ahead (per warp) by the cp.async rings of the wide kernels
 
-// Per-warp ring of kRing patient records in shared memory, filled with cp.async (8-byte granules,
-// any alignment): record p holds nseg segments (segment j: len[j] doubles from src[j] + p stride[j]).
-// issue(p) copies record p into slot p % kRing as one commit group; wait() makes the oldest
-// outstanding record visible to the whole warp.
-template <int NSEG>
+__device__ __forceinline__ uint32_t su32d(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Per-warp ring of kRing patient records in shared memory: record p holds NSEG segments (segment j:
+// len[j] doubles from src[j] + p stride[j]). BULK: one lane issues 1-D TMA bulk copies completing on
+// the slot's mbarrier (all segments 16-byte aligned: R even); otherwise every lane issues 8-byte
+// cp.async granules (any alignment) as one commit group per record. issue(p) fills slot p % kRing;
+// wait(p) makes record p visible to the whole warp. init() (re)arms the barriers for a new pass.
+template <int NSEG, bool BULK>
 struct WarpRing {
   double* buf;
+  uint64_t* bar;           // kRing mbarriers (BULK), armed once per kernel (ring_bars_init)
+  int q0;                  // records issued by earlier passes of this warp (slot / phase continuity)
   int per;                 // doubles per record
   const double* src[NSEG];
   int64_t stride[NSEG];
   int len[NSEG];
-  __device__ __forceinline__ double* slot(int p) const { return buf + (p % kRing) * per; }
+  __device__ __forceinline__ double* slot(int p) const { return buf + ((q0 + p) % kRing) * per; }
   __device__ __forceinline__ void issue(int p, int np) {
-    if (p < np) {
-      const int lane = threadIdx.x & 31;
-      double* dst = slot(p);
+    if (BULK) {
+      if (p < np && (threadIdx.x & 31) == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior reads of the slot first
+        uint64_t* b = bar + ((q0 + p) % kRing);
+        uint32_t tx = 0;
 #pragma unroll
-      for (int j = 0; j < NSEG; ++j) {
-        const double* sp = src[j] + (int64_t)p * stride[j];
-        for (int x = lane; x < len[j]; x += 32) cpa8(dst + x, sp + x);
-        dst += len[j];
+        for (int j = 0; j < NSEG; ++j) tx += 8u * (uint32_t)len[j];
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32d(b)), "r"(tx) : "memory");
+        double* dst = slot(p);
+#pragma unroll
+        for (int j = 0; j < NSEG; ++j) {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  su32d(dst)),
+              "l"(src[j] + (int64_t)p * stride[j]), "r"(8u * (uint32_t)len[j]), "r"(su32d(b))
+              : "memory");
+          dst += len[j];
+        }
       }
+    } else {
+      if (p < np) {
+        const int lane = threadIdx.x & 31;
+        double* dst = slot(p);
+#pragma unroll
+        for (int j = 0; j < NSEG; ++j) {
+          const double* sp = src[j] + (int64_t)p * stride[j];
+          for (int x = lane; x < len[j]; x += 32) cpa8(dst + x, sp + x);
+          dst += len[j];
+        }
+      }
+      cpa_commit();
     }
-    cpa_commit();
+  }
+  __device__ __forceinline__ void wait(int p) {
+    if (BULK) {
+      const int q = q0 + p;
+      const uint32_t a = su32d(bar + (q % kRing)), parity = (uint32_t)((q / kRing) & 1);
+      asm volatile(
+          "{\n .reg .pred P1;\n"
+          "WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE%=;\n bra WAIT%=;\n"
+          "DONE%=:\n}" ::"r"(a),
+          "r"(parity)
+          : "memory");
+    } else {
+      cpa_wait<kRing - 1>();
+      __syncwarp();
+    }
+  }
+  __device__ __forceinline__ void drain() {
+    if (!BULK) cpa_wait<0>();
   }
 };
+
+__device__ __forceinline__ void ring_bars_init(uint64_t* bar) {
+  if ((threadIdx.x & 31) == 0) {
+    for (int i = 0; i < kRing; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32d(bar + i)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
 
 // Warp-cooperative A slab: slab[p][a][cc] = A_p(a, s = 8 nt + cc) for the round's patients.
 // A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps). Rows a >= m_p of
 // P'_p are zero (never written), so only a < l is checked. P'_p and w̄_p arrive through the warp's
 // cp.async ring, kRing patients ahead of the MMAs.
-template <int MT, int KS>
+template <int MT, int KS, bool BULK>
 __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, int R, const double* Pp,
-                                       const double* W, const double* Hs, double* slab, double* ringbuf) {
+                                       const double* W, const double* Hs, double* slab, double* ringbuf,
+                                       uint64_t* bars, int& q0) {
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int s = 8 * nt + g;
   double hb[KS];
@@ -188,8 +243,10 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
     }
   }
   const int np = (int)(K - base < 32 ? K - base : 32);
-  WarpRing<2> ring;
+  WarpRing<2, BULK> ring;
   ring.buf = ringbuf;
+  ring.bar = bars;
+  ring.q0 = q0;
   ring.per = lR + R;
   ring.src[0] = Pp + base * lR;
   ring.stride[0] = lR;
@@ -200,8 +257,7 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
 #pragma unroll
   for (int p = 0; p < kRing; ++p) ring.issue(p, np);
   for (int p = 0; p < np; ++p) {
-    cpa_wait<kRing - 1>();
-    __syncwarp();
+    ring.wait(p);
     const double* rec = ring.slot(p);
     double c[MT][2];
 #pragma unroll
@@ -221,7 +277,8 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
     __syncwarp();  // slot p fully read before it is refilled
     ring.issue(p + kRing, np);
   }
-  cpa_wait<0>();
+  ring.drain();
+  q0 += np;
   for (int p = np; p < 32; ++p)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
@@ -242,9 +299,15 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
   const int hoff = ((R * R + 31) / 32) * 32;
   double* Hs = sm;                                      // R x R
   const int wib = threadIdx.x >> 5;
-  const int ringd = kRing * (2 * l * R + R);           // per warp: cp.async ring (doubles)
-  double* slab = sm + hoff + wib * (32 * MT * 8 * 8 + ringd);  // per warp: 32 patients x (MT 8) x 8
-  double* ringbuf = slab + 32 * MT * 8 * 8;
+  constexpr bool BULK = RT > 0 && (RT % 2) == 0;     // 16-byte aligned records: TMA bulk copies
+  const int ringd = kRing * (l * R + R) + kRing;      // per warp: a-slab ring (doubles) + mbarriers
+  // per warp: slab of 32 patients x (MT 8) x 8, reused as the F_H ring (kRing x (2 l R + R))
+  const int slabd = 32 * MT * 8 * 8 > kRing * (2 * l * R + R) ? 32 * MT * 8 * 8 : kRing * (2 * l * R + R);
+  double* slab = sm + hoff + wib * (slabd + ringd);
+  double* ringbuf = slab + slabd;
+  uint64_t* bars = (uint64_t*)(ringbuf + kRing * (l * R + R));
+  if (BULK) ring_bars_init(bars);
+  int q0 = 0;  // records this warp has pulled through its ring (mbarrier phase continuity)
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) Hs[x] = Hg[x];
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -274,7 +337,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
 #pragma unroll
       for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf);
+      a_slab<MT, KS, BULK>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
@@ -315,7 +378,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf);
+      a_slab<MT, KS, BULK>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
       if (kme < K && mme > 0) {
         double* Q = Qt + kme * pstride;
@@ -365,8 +428,10 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
         for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
       const int np = (int)(K - base < 32 ? K - base : 32);
       const int lR = l * R;
-      WarpRing<3> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R)
-      ring.buf = ringbuf;
+      WarpRing<3, BULK> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R), staged in the (free) slab
+      ring.buf = slab;
+      ring.bar = bars;
+      ring.q0 = q0;
       ring.per = 2 * lR + R;
       ring.src[0] = Qt + base * lR;
       ring.stride[0] = lR;
@@ -380,8 +445,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
 #pragma unroll
       for (int p = 0; p < kRing; ++p) ring.issue(p, np);
       for (int p = 0; p < np; ++p) {
-        cpa_wait<kRing - 1>();
-        __syncwarp();
+        ring.wait(p);
         const double* rec = ring.slot(p);
         double wv[NT];
 #pragma unroll
@@ -403,7 +467,9 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
         __syncwarp();
         ring.issue(p + kRing, np);
       }
-      cpa_wait<0>();
+      ring.drain();
+      q0 += np;
+      __syncwarp();  // the slab is rewritten by the next round
 #pragma unroll
       for (int i = 0; i < NT; ++i)
 #pragma unroll
@@ -443,7 +509,8 @@ static void polar_wide_inst(Handle& h) {
   constexpr int MT = (L + 7) / 8;
   auto fn = k_polar_wide<L, MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
-  const size_t per_warp = (size_t)(32 * MT * 8 * 8 + kRing * (2 * h.l * h.R + h.R));
+  const size_t slabd = (size_t)std::max(32 * MT * 8 * 8, kRing * (2 * h.l * h.R + h.R));
+  const size_t per_warp = slabd + (size_t)(kRing * (h.l * h.R + h.R) + kRing);
   int wpb = kDenseThreads / 32;  // warps per block: fewer when the per-warp slab + ring is large
   while (wpb > 1 && sizeof(double) * (hoff + wpb * per_warp) > 227 * 1024) wpb /= 2;
   const int threads = 32 * wpb;
