@@ -34,6 +34,7 @@ import synthgen  # noqa: E402
 # one host core.
 ORACLE_SAMPLE = {"tiny": 200, "small": 20000, "medium": 12000, "large": 1500, "scale": 8000}
 FP64_PEAK_TFLOPS = 34.2  # measured DFMA loop on this pool's B200 at 1965 MHz (tools/probe_fp64.cu, profiles/)
+DMMA_PEAK_TFLOPS = 36.9  # measured mma.sync m8n8k4 f64 (SASS DMMA) loop, same box (tools/probe_dmma*.cu)
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -268,6 +269,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             ach = mdl["bytes"] / (ms_launch / 1e3) / 1e9
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": ach / hbm_peak, "traffic": traffic, "peak_source": hbm_src, "ms_per_launch": ms_launch}
+            if mdl["flops"] > 0:  # the fiber passes also sit at the FP64 tensor-core (DMMA) ridge
+                tf = mdl["flops"] / (ms_launch / 1e3) / 1e12
+                roof["fp64_tensor"] = {"achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                       "frac": tf / DMMA_PEAK_TFLOPS, "flops": "2 F l R (useful, no padding)"}
     step_bytes = sum(model[k]["bytes"] for k in model)
     phase_report = {k: {"ms_per_launch": per_launch[k][0], "share": per_launch[k][0] / ms_per_step,
                         "alg_GBps": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9) if k in model else None}
