@@ -69,7 +69,10 @@ size_t carve(Handle& h, char* base) {
   h.Pp = c.take<double>(h.S * R + 4);   // +4: bulk copies round up to 16 bytes
   h.Qt = c.take<double>(h.S * R + 4);
   h.Nst = c.take<double>(h.S * R + 4);
-  h.partial = c.take<double>(2 * (int64_t)kPartBlocks * RR);
+  {  // per-block partials of the R x R reductions; also the chunk sums of the F_H reduction
+    const int64_t NT = (R + 7) / 8, a = 2 * (int64_t)kPartBlocks * RR, b = 32 * 64 * NT * NT;
+    h.partial = c.take<double>(a > b ? a : b);
+  }
   {
     const int64_t RP = 8 * ((R + 7) / 8);
     h.fh_warp = c.take<double>(h.smooth ? (int64_t)kPartBlocks * 4 * RP * RP : 1);

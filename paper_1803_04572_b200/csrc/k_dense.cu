@@ -31,7 +31,7 @@ int launch_polar_wide(Handle& h) {
   else if (h.l <= 8) polar_wide_L8(h);
   else if (h.l <= 9) polar_wide_L9(h);
   else polar_wide_L12(h);
-  return 2;
+  return 3;  // polar kernel + two-stage F_H reduction
 }
 
 int launch_passB_wide(Handle& h) {

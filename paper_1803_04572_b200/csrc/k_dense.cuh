@@ -481,16 +481,28 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
 }
 
 // F_H = sum over warps (fixed order) of the fragment-ordered partials
-static __global__ void k_sum_fh(const double* __restrict__ part, int nw, int R, int NT, double* __restrict__ FH) {
+// F_H = sum over the per-warp fragment-ordered partials, in a fixed order (deterministic):
+// stage 1 sums kFhChunks contiguous warp chunks per fragment position, stage 2 sums the chunks.
+constexpr int kFhChunks = 32;
+static __global__ void k_sum_fh1(const double* __restrict__ part, int nw, int P, double* __restrict__ tmp) {
+  const int pos = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pos >= P) return;
+  const int c = blockIdx.y;
+  const int w0 = (int)((int64_t)nw * c / kFhChunks), w1 = (int)((int64_t)nw * (c + 1) / kFhChunks);
+  double v = 0.0;
+  for (int w = w0; w < w1; ++w) v += part[(int64_t)w * P + pos];
+  tmp[(int64_t)c * P + pos] = v;
+}
+static __global__ void k_sum_fh(const double* __restrict__ tmp, int R, int NT, double* __restrict__ FH) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= R * R) return;
   const int r = x / R, s = x - r * R;
   // fragment position of (r, s): tile (i = r/8, j = s/8), lane g = r%8, t = (s%8)/2, c = s%2
   const int i = r >> 3, j = s >> 3, g = r & 7, t = (s & 7) >> 1, c = s & 1;
   const int off = 32 * ((i * NT + j) * 2 + c) + g * 4 + t;
-  const int rp2 = 64 * NT * NT;
+  const int P = 64 * NT * NT;
   double v = 0.0;
-  for (int w = 0; w < nw; ++w) v += part[(int64_t)w * rp2 + off];
+  for (int ch = 0; ch < kFhChunks; ++ch) v += tmp[(int64_t)ch * P + off];
   FH[x] = v;
 }
 
@@ -532,7 +544,9 @@ static void polar_wide_inst(Handle& h) {
   fn<<<(unsigned)blocks, threads, smem, h.stream>>>(h.m, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
                                                     h.fh_warp);
   const int RR = h.R * h.R;
-  k_sum_fh<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.fh_warp, (int)blocks * wpb, h.R, NT, h.FH);
+  const int P = 64 * NT * NT;
+  k_sum_fh1<<<dim3((P + 127) / 128, kFhChunks), 128, 0, h.stream>>>(h.fh_warp, (int)blocks * wpb, P, h.partial);
+  k_sum_fh<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, h.R, NT, h.FH);
 }
 
 template <int L>

@@ -127,12 +127,15 @@ constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ran
 constexpr int kPfFibers = 4096;   // pass-B L2 prefetch distance (fibers) ahead of the ring
 constexpr int kPfPatients = 64;   // and patients (N rows)
 
-template <int KS, int NT, int W, int TB>
+template <int KS, int NT, int W, int TB, int LT, int RT>
 __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
-    const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l, int R, int RS, int FB, int PB,
+    const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l_, int R_, int RS_, int FB, int PB,
     int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg) {
+  const int R = RT ? RT : R_;           // compile-time for the configured (R, l) shapes
+  const int l = LT ? LT : l_;
+  const int RS = RT ? ((RT + 1) & ~1) : RS_;
   extern __shared__ __align__(128) unsigned char smraw[];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int grp = blockIdx.x % G;
@@ -351,9 +354,9 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-template <int KS, int NT, int W, int TB>
+template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0>
 static void scatter_inst_w(Handle& h) {
-  auto fn = k_scatter_tma<KS, NT, W, TB>;
+  auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -376,6 +379,11 @@ static void scatter_inst(Handle& h) {
 
 template <int KS>
 static void scatter_dispatch_n(Handle& h) {
+  if (h.sc_W == 4) {
+    if (KS == 2 && h.l == 7 && h.R == 20) { scatter_inst_w<2, 3, 4, 2, 7, 20>(h); return; }
+    if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 2, 7, 15>(h); return; }
+    if (KS == 3 && h.l == 9 && h.R == 40) { scatter_inst_w<3, 5, 4, 2, 9, 40>(h); return; }
+  }
   switch ((h.R + 7) / 8) {
     case 1: scatter_inst<KS, 1>(h); break;
     case 2: scatter_inst<KS, 2>(h); break;
