@@ -580,7 +580,8 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
                                                     const double* __restrict__ GWi, const double* __restrict__ scal,
                                                     int n_inner, int kind, double param, double* __restrict__ W,
                                                     double* __restrict__ DW, double* __restrict__ Nst,
-                                                    double* __restrict__ part /* [blocks][2][R R] */) {
+                                                    double* __restrict__ part /* [blocks][2][R R] */,
+                                                    int getenv_l1) {
   constexpr int RP = 8 * NT;
   constexpr int KS = (NT * 8 + 3) / 4;  // i steps of 4 covering 8 NT >= R
   const int R = RT ? RT : R_;
@@ -655,11 +656,14 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
   for (int64_t rd = blockIdx.x * (blockDim.x >> 5) + wib; rd < rounds; rd += nwarps_total) {
     const int64_t base = rd * 32;
     const int np = (int)(K - base < 32 ? K - base : 32);
-    {  // this round's rows into L1, the next round's into L2
-      warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
-      warp_prefetch(Qt + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
-      warp_prefetch(W + base * R, sizeof(double) * (size_t)(np * R), true);
-      warp_prefetch(DW + base * R, sizeof(double) * (size_t)(np * R), true);
+    {  // this round's rows into L1 (measured better than L2-only), the next round's into L2
+      const bool l1 = getenv_l1;
+      if (l1) {
+        warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+        warp_prefetch(Qt + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
+        warp_prefetch(W + base * R, sizeof(double) * (size_t)(np * R), true);
+        warp_prefetch(DW + base * R, sizeof(double) * (size_t)(np * R), true);
+      }
       const int64_t nb = base + 32 * (int64_t)nwarps_total;
       if (nb < K) {
         const int64_t nn = K - nb < 32 ? K - nb : 32;
@@ -841,7 +845,7 @@ static void passB_wide_inst(Handle& h) {
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.K, h.R, h.l, h.Pp, h.Qt, h.H, h.GWi, h.scal,
                                                          h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
-                                                         h.Nst, h.partial);
+                                                         h.Nst, h.partial, getenv("COPA_PASSB_NOL1") ? 0 : 1);
   const int RR = h.R * h.R;
   k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
 }
