@@ -136,6 +136,7 @@ template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int kRing = 4;  // patients staged ahead (per warp) by the cp.async rings of the wide kernels
+constexpr bool kSplitK = false;  // even/odd k-step accumulators in the A slabs (changes rounding order)
 
 __device__ __forceinline__ uint32_t su32d(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -203,6 +204,16 @@ struct WarpRing {
       __syncwarp();
     }
   }
+  // records p and p + 1 (consumed in pairs; the pair loop issues two groups per step)
+  __device__ __forceinline__ void wait_pair(int p, bool two) {
+    if (BULK) {
+      wait(p);
+      if (two) wait(p + 1);
+    } else {
+      cpa_wait<kRing - 2>();
+      __syncwarp();
+    }
+  }
   __device__ __forceinline__ void drain() {
     if (!BULK) cpa_wait<0>();
   }
@@ -256,26 +267,42 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
   ring.len[1] = R;
 #pragma unroll
   for (int p = 0; p < kRing; ++p) ring.issue(p, np);
-  for (int p = 0; p < np; ++p) {
-    ring.wait(p);
-    const double* rec = ring.slot(p);
-    double c[MT][2];
+  // two patients per step, each with even / odd k-step accumulators: four independent DMMA chains
+  // (a single KS-long chain per patient would expose the ~30-cycle DMMA latency KS times)
+  for (int p = 0; p < np; p += 2) {
+    const bool two = p + 1 < np;
+    ring.wait_pair(p, two);
+    const double* rec[2] = {ring.slot(p), two ? ring.slot(p + 1) : ring.slot(p)};
+    double c[2][2][MT][2];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+    for (int q = 0; q < 2; ++q)
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const double wr = offw[ks] >= 0 ? rec[offw[ks]] : 0.0;
+      for (int e = 0; e < 2; ++e)
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const double av = offp[ks][mt] >= 0 ? rec[offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
-        dmma2(c[mt][0], c[mt][1], av, hb[ks]);
+        for (int mt = 0; mt < MT; ++mt) c[q][e][mt][0] = c[q][e][mt][1] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double wr = offw[ks] >= 0 ? rec[q][offw[ks]] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double av = offp[ks][mt] >= 0 ? rec[q][offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+          dmma2(c[q][kSplitK ? (ks & 1) : 0][mt][0], c[q][kSplitK ? (ks & 1) : 0][mt][1], av, hb[ks]);
+        }
       }
-    }
-    double* sp = slab + (p * MT * 8 + g) * 8 + 2 * t;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) *reinterpret_cast<double2*>(sp + mt * 64) = make_double2(c[mt][0], c[mt][1]);
-    __syncwarp();  // slot p fully read before it is refilled
+    for (int q = 0; q < 2; ++q)
+      if (q == 0 || two) {
+        double* sp = slab + ((p + q) * MT * 8 + g) * 8 + 2 * t;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          *reinterpret_cast<double2*>(sp + mt * 64) =
+              make_double2(c[q][0][mt][0] + c[q][1][mt][0], c[q][0][mt][1] + c[q][1][mt][1]);
+      }
+    __syncwarp();  // slots p, p+1 fully read before they are refilled
     ring.issue(p + kRing, np);
+    ring.issue(p + 1 + kRing, np);
   }
   ring.drain();
   q0 += np;
