@@ -49,7 +49,7 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
 }
 
 constexpr int kAWarps = 8;   // warps per CTA
-constexpr int kANS = 4;      // ring slots per warp
+constexpr int kANS = 4;      // ring slots per warp (power of two)
 constexpr int kAChunk = 32;  // fibers per chunk
 
 __host__ __device__ inline int chunk_val_off() { return kAChunk * 4; }  // col block, then val block
@@ -106,11 +106,12 @@ __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restric
   const int64_t C0 = F0 & ~(int64_t)3;  // chunk grid aligned to 4 fibers (16-byte bulk copies)
   const int64_t nch = (F1 - C0 + kAChunk - 1) / kAChunk;
   const uint32_t vbytes_chunk = (uint32_t)(kAChunk * l * 8);
-  auto issue = [&](int64_t c) {
-    if (lane == 0 && c < nch) {
-      unsigned char* dst = ring + (c % kANS) * cb;
-      uint64_t* bar = bars + (c % kANS);
-      const int64_t cs = C0 + c * kAChunk;
+  const int nchi = (int)nch;  // chunks per warp stream (< 2^31)
+  auto issue = [&](int c) {
+    if (lane == 0 && c < nchi) {
+      unsigned char* dst = ring + (c & (kANS - 1)) * cb;
+      uint64_t* bar = bars + (c & (kANS - 1));
+      const int64_t cs = C0 + (int64_t)c * kAChunk;
       mb_arrive_tx(bar, kAChunk * 4 + vbytes_chunk);
       bulk_copy(dst, acol + cs, kAChunk * 4, bar);
       bulk_copy(dst + chunk_val_off(), aval + cs * l, vbytes_chunk, bar);
@@ -156,12 +157,12 @@ __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restric
   // patient segment are masked to zero in the A operand at MMA time; rows a >= l and columns r >= R
   // only feed accumulator entries that are never written (labels are always valid: the slack of
   // fa_col is zeroed and V̄ rows are padded).
-  for (int64_t c = 0; c < nch; ++c) {
-    mb_wait(bars + (c % kANS), (uint32_t)((c / kANS) & 1));
-    const unsigned char* buf = ring + (c % kANS) * cb;
+  for (int c = 0; c < nchi; ++c) {
+    mb_wait(bars + (c & (kANS - 1)), (uint32_t)((c / kANS) & 1));
+    const unsigned char* buf = ring + (c & (kANS - 1)) * cb;
     const int32_t* colS = (const int32_t*)buf;
     const double* valS = (const double*)(buf + chunk_val_off());
-    const int64_t cs = C0 + c * kAChunk;
+    const int64_t cs = C0 + (int64_t)c * kAChunk;
     double x[8][MT], bv[8][NT];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
