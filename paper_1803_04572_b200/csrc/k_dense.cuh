@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
                                                        const double* __restrict__ Pp, const double* __restrict__ W,
                                                        const double* __restrict__ Hg, double tau,
                                                        double* __restrict__ Qt, int32_t* __restrict__ rank,
-                                                       double* __restrict__ FHwarp) {
+                                                       double* __restrict__ FHwarp, int nextpf) {
   constexpr int KS = (NT * 8 + 3) / 4;  // r steps of 4 covering 8 NT >= R
   constexpr int RP = 8 * NT;
   const int R = RT ? RT : R_;           // compile-time for the configured (R, l) pairs
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     const int64_t base = rd * 32;
     {  // prefetch the next round's P' and W rows into L2
       const int64_t nb = base + 32 * (int64_t)nwarps_total;
-      if (nb < K) {
+      if (nextpf && nb < K) {
         const int64_t nl = nb + 32 < K ? nb + 32 : K;
         warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)((nl - nb) * pstride), false);
         warp_prefetch(W + nb * R, sizeof(double) * (size_t)((nl - nb) * R), false);
@@ -569,7 +569,7 @@ static void polar_wide_inst(Handle& h) {
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, threads, smem, h.stream>>>(h.m, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
-                                                    h.fh_warp);
+                                                    h.fh_warp, getenv("COPA_NEXT_PF") ? 1 : 0);
   const int RR = h.R * h.R;
   const int P = 64 * NT * NT;
   k_sum_fh1<<<dim3((P + 127) / 128, kFhChunks), 128, 0, h.stream>>>(h.fh_warp, (int)blocks * wpb, P, h.partial);
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
                                                     int n_inner, int kind, double param, double* __restrict__ W,
                                                     double* __restrict__ DW, double* __restrict__ Nst,
                                                     double* __restrict__ part /* [blocks][2][R R] */,
-                                                    int getenv_l1) {
+                                                    int getenv_l1, int nextpf) {
   constexpr int RP = 8 * NT;
   constexpr int KS = (NT * 8 + 3) / 4;  // i steps of 4 covering 8 NT >= R
   const int R = RT ? RT : R_;
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
         warp_prefetch(DW + base * R, sizeof(double) * (size_t)(np * R), true);
       }
       const int64_t nb = base + 32 * (int64_t)nwarps_total;
-      if (nb < K) {
+      if (nextpf && nb < K) {
         const int64_t nn = K - nb < 32 ? K - nb : 32;
         warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
         warp_prefetch(Qt + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
@@ -872,7 +872,8 @@ static void passB_wide_inst(Handle& h) {
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.K, h.R, h.l, h.Pp, h.Qt, h.H, h.GWi, h.scal,
                                                          h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
-                                                         h.Nst, h.partial, getenv("COPA_PASSB_NOL1") ? 0 : 1);
+                                                         h.Nst, h.partial, getenv("COPA_PASSB_NOL1") ? 0 : 1,
+                                                         getenv("COPA_NEXT_PF") ? 1 : 0);
   const int RR = h.R * h.R;
   k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
 }

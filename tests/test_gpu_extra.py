@@ -165,11 +165,14 @@ def test_single_visit_patients_and_tiny_patients(copa):
     assert rel(g.U().cpu().numpy(), o.U_all()) <= 1e-9
 
 
-@pytest.mark.parametrize("R,l", [(3, 0), (16, 0), (8, 5), (24, 9), (40, 12), (20, 16), (64, 16)])
-def test_shape_sweep(copa, R, l):
-    """Kernel template/limit coverage: tall and wide polar, MMA tile counts, smooth l up to 16."""
+@pytest.mark.parametrize("R,l,J", [(3, 0, 120), (16, 0, 120), (8, 5, 120), (24, 9, 120), (40, 12, 120), (20, 16, 120),
+                                   (64, 16, 120), (20, 7, 4000), (40, 7, 30000)])
+def test_shape_sweep(copa, R, l, J):
+    """Kernel template/limit coverage: tall and wide polar, MMA tile counts, smooth l up to 16, and
+    pass B's label groups: J = 4000 needs G = 4 F_V slices; J = 30000 (R = 40) fits no smem slice
+    and takes the FP64-atomic fallback."""
     base = "medium" if l else "small"
-    cfg = dataclasses.replace(synthgen.CONFIGS[base], R=R, smooth_l=l, K=400, J=120)
+    cfg = dataclasses.replace(synthgen.CONFIGS[base], R=R, smooth_l=l, K=400, J=J)
     p = synthgen.generate(cfg)
     g = copa.Copa(p, copa.Options.from_config(cfg))
     o = oracle.Oracle(p)
