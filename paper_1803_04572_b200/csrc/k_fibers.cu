@@ -244,6 +244,14 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int64_t jbase = grp * Jg;
     const int per = l * R;
     double sink = 0.0;  // timing experiments (dbg 3, 4) only
+    int offn[KS][NT];   // lane's B-fragment offsets inside an N_k block (-1: padding)
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int a = 4 * ks + t, r = 8 * nt + g;
+        offn[ks][nt] = (a < l && r < R) ? a * R + r : -1;
+      }
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
       mbar_wait(full + slot, phase);
@@ -256,21 +264,31 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
       const int32_t* colS = (const int32_t*)(base + sg.col + mi[2]);
       const double* valS = (const double*)(base + sg.val + mi[3]);
       const double* nS = (const double*)(base + sg.nrows + mi[4]);
-      for (int p = 0; p < (dbg == 1 ? 0 : k1 - k0); ++p) {
+      // per-patient setup (sub-run bounds, B fragments B[t][g] = N(a = 4 ks + t, r = 8 nt + g)) is
+      // loaded one patient ahead, off the critical path of the current patient's tiles
+      const int npat = dbg == 1 ? 0 : k1 - k0;
+      auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NT]) {
         const int64_t rs = gp[p];
-        const int lo = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
-        const int hi = (int)(min(rs + wo[p * kWoS + w + 1], f1) - f0);
-        if (lo >= hi) continue;
-        // B fragments of this patient: B[t][g] = N(a = 4 ks + t, r = 8 nt + g)
+        lo_ = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
+        hi_ = (int)(min(rs + wo[p * kWoS + w + 1], f1) - f0);
         const double* Np = nS + (int64_t)p * per;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) b[ks][nt] = offn[ks][nt] >= 0 ? Np[offn[ks][nt]] : 0.0;
+      };
+      int nlo = 0, nhi = 0;
+      double nbfr[KS][NT];
+      if (npat > 0) setup(0, nlo, nhi, nbfr);
+      for (int p = 0; p < npat; ++p) {
+        const int lo = nlo, hi = nhi;
         double bfr[KS][NT];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const int a = 4 * ks + t, r = 8 * nt + g;
-            bfr[ks][nt] = (a < l && r < R) ? Np[a * R + r] : 0.0;
-          }
+          for (int nt = 0; nt < NT; ++nt) bfr[ks][nt] = nbfr[ks][nt];
+        if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
+        if (lo >= hi) continue;
         if (dbg == 3) { sink += bfr[0][0]; continue; }
         // TB tiles at a time while >= TB tiles remain, then single tiles (no MMAs on empty tiles).
         // Tiles of one sub-run belong to one patient => distinct labels => distinct F_V rows, so
