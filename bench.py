@@ -141,7 +141,7 @@ def load_traffic():
     for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*traffic*.json"))):
         try:
             with open(f) as fh:
-                out.update(json.load(fh))
+                out.update({k: v for k, v in json.load(fh).items() if not k.startswith("_")})
         except Exception:  # noqa: BLE001
             pass
     return out

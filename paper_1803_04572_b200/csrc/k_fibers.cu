@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
     const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l_, int R_, int RS_, int FB, int PB,
-    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg) {
+    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg, int pf_scale) {
   const int R = RT ? RT : R_;           // compile-time for the configured (R, l) shapes
   const int l = LT ? LT : l_;
   const int RS = RT ? ((RT + 1) & ~1) : RS_;
@@ -179,14 +179,14 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         const int64_t f0 = nf0, f1 = nf1;
         const int32_t k0 = nk0, k1 = nk1;
         {
-          const int64_t ft = min(f1 + (int64_t)kPfFibers, end_f);
+          const int64_t ft = min(f1 + (int64_t)(pf_scale * kPfFibers), end_f);
           while (pf_f < ft) {
             const int64_t n = min((int64_t)1024, ft - pf_f);
             l2_prefetch(fiber_col + pf_f, 4ull * n);
             l2_prefetch(fiber_val + pf_f * l, 8ull * n * l);
             pf_f += n;
           }
-          const int64_t kt = min((int64_t)k1 + kPfPatients, end_k);
+          const int64_t kt = min((int64_t)k1 + (int64_t)(pf_scale * kPfPatients), end_k);
           while (pf_k < kt) {
             const int64_t n = min((int64_t)16, kt - pf_k);
             l2_prefetch(Nst + pf_k * l * R, 8ull * n * l * R);
@@ -384,7 +384,8 @@ static void scatter_inst_w(Handle& h) {
   fn<<<ctas, 32 * (W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js, h.sc_Jg,
                                                    h.st_f, h.st_k, h.cta_st, h.woff, h.l, h.R, h.sc_RS, h.sc_FB,
                                                    h.sc_PB, h.sc_NS, h.Nst, h.fv_part,
-                                                   getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0);
+                                                   getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0,
+                                                   getenv("COPA_SC_PF") ? atoi(getenv("COPA_SC_PF")) : 0);  // L2 frontier: off (no gain, +15 GB DRAM)
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
