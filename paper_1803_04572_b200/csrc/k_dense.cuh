@@ -136,6 +136,7 @@ template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int kRing = 4;  // patients staged ahead (per warp) by the cp.async rings of the wide kernels
+constexpr int kRingA = 3; // ... by the polar A-slab ring (smaller, for 3 polar CTAs per SM)
 constexpr bool kSplitK = false;  // even/odd k-step accumulators in the A slabs (changes rounding order)
 
 __device__ __forceinline__ uint32_t su32d(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -145,21 +146,21 @@ __device__ __forceinline__ uint32_t su32d(const void* p) { return (uint32_t)__cv
 // the slot's mbarrier (all segments 16-byte aligned: R even); otherwise every lane issues 8-byte
 // cp.async granules (any alignment) as one commit group per record. issue(p) fills slot p % kRing;
 // wait(p) makes record p visible to the whole warp. init() (re)arms the barriers for a new pass.
-template <int NSEG, bool BULK>
+template <int NSEG, bool BULK, int NR = kRing>
 struct WarpRing {
   double* buf;
-  uint64_t* bar;           // kRing mbarriers (BULK), armed once per kernel (ring_bars_init)
+  uint64_t* bar;           // NR mbarriers (BULK), armed once per kernel (ring_bars_init)
   int q0;                  // records issued by earlier passes of this warp (slot / phase continuity)
   int per;                 // doubles per record
   const double* src[NSEG];
   int64_t stride[NSEG];
   int len[NSEG];
-  __device__ __forceinline__ double* slot(int p) const { return buf + ((q0 + p) % kRing) * per; }
+  __device__ __forceinline__ double* slot(int p) const { return buf + ((q0 + p) % NR) * per; }
   __device__ __forceinline__ void issue(int p, int np) {
     if (BULK) {
       if (p < np && (threadIdx.x & 31) == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior reads of the slot first
-        uint64_t* b = bar + ((q0 + p) % kRing);
+        uint64_t* b = bar + ((q0 + p) % NR);
         uint32_t tx = 0;
 #pragma unroll
         for (int j = 0; j < NSEG; ++j) tx += 8u * (uint32_t)len[j];
@@ -192,7 +193,7 @@ struct WarpRing {
   __device__ __forceinline__ void wait(int p) {
     if (BULK) {
       const int q = q0 + p;
-      const uint32_t a = su32d(bar + (q % kRing)), parity = (uint32_t)((q / kRing) & 1);
+      const uint32_t a = su32d(bar + (q % NR)), parity = (uint32_t)((q / NR) & 1);
       asm volatile(
           "{\n .reg .pred P1;\n"
           "WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE%=;\n bra WAIT%=;\n"
@@ -200,7 +201,7 @@ struct WarpRing {
           "r"(parity)
           : "memory");
     } else {
-      cpa_wait<kRing - 1>();
+      cpa_wait<NR - 1>();
       __syncwarp();
     }
   }
@@ -210,7 +211,7 @@ struct WarpRing {
       wait(p);
       if (two) wait(p + 1);
     } else {
-      cpa_wait<kRing - 2>();
+      cpa_wait<NR - 2>();
       __syncwarp();
     }
   }
@@ -219,9 +220,9 @@ struct WarpRing {
   }
 };
 
-__device__ __forceinline__ void ring_bars_init(uint64_t* bar) {
+__device__ __forceinline__ void ring_bars_init(uint64_t* bar, int n = kRing) {
   if ((threadIdx.x & 31) == 0) {
-    for (int i = 0; i < kRing; ++i)
+    for (int i = 0; i < n; ++i)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32d(bar + i)) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -232,7 +233,7 @@ __device__ __forceinline__ void ring_bars_init(uint64_t* bar) {
 // A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps). Rows a >= m_p of
 // P'_p are zero (never written), so only a < l is checked. P'_p and w̄_p arrive through the warp's
 // cp.async ring, kRing patients ahead of the MMAs.
-template <int MT, int KS, bool BULK>
+template <int MT, int KS, bool BULK, int SR>
 __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, int R, const double* Pp,
                                        const double* W, const double* Hs, double* slab, double* ringbuf,
                                        uint64_t* bars, int& q0) {
@@ -254,7 +255,7 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
     }
   }
   const int np = (int)(K - base < 32 ? K - base : 32);
-  WarpRing<2, BULK> ring;
+  WarpRing<2, BULK, kRingA> ring;
   ring.buf = ringbuf;
   ring.bar = bars;
   ring.q0 = q0;
@@ -266,50 +267,36 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
   ring.stride[1] = R;
   ring.len[1] = R;
 #pragma unroll
-  for (int p = 0; p < kRing; ++p) ring.issue(p, np);
-  // two patients per step, each with even / odd k-step accumulators: four independent DMMA chains
-  // (a single KS-long chain per patient would expose the ~30-cycle DMMA latency KS times)
-  for (int p = 0; p < np; p += 2) {
-    const bool two = p + 1 < np;
-    ring.wait_pair(p, two);
-    const double* rec[2] = {ring.slot(p), two ? ring.slot(p + 1) : ring.slot(p)};
-    double c[2][2][MT][2];
+  for (int p = 0; p < kRingA; ++p) ring.issue(p, np);
+  for (int p = 0; p < np; ++p) {
+    ring.wait(p);
+    const double* rec = ring.slot(p);
+    double c[MT][2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
 #pragma unroll
-      for (int e = 0; e < 2; ++e)
+    for (int ks = 0; ks < KS; ++ks) {
+      const double wr = offw[ks] >= 0 ? rec[offw[ks]] : 0.0;
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) c[q][e][mt][0] = c[q][e][mt][1] = 0.0;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const double wr = offw[ks] >= 0 ? rec[q][offw[ks]] : 0.0;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const double av = offp[ks][mt] >= 0 ? rec[q][offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
-          dmma2(c[q][kSplitK ? (ks & 1) : 0][mt][0], c[q][kSplitK ? (ks & 1) : 0][mt][1], av, hb[ks]);
-        }
+      for (int mt = 0; mt < MT; ++mt) {
+        const double av = offp[ks][mt] >= 0 ? rec[offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+        dmma2(c[mt][0], c[mt][1], av, hb[ks]);
       }
+    }
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      if (q == 0 || two) {
-        double* sp = slab + ((p + q) * MT * 8 + g) * 8 + 2 * t;
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          *reinterpret_cast<double2*>(sp + mt * 64) =
-              make_double2(c[q][0][mt][0] + c[q][1][mt][0], c[q][0][mt][1] + c[q][1][mt][1]);
-      }
-    __syncwarp();  // slots p, p+1 fully read before they are refilled
-    ring.issue(p + kRing, np);
-    ring.issue(p + 1 + kRing, np);
+    for (int mt = 0; mt < MT; ++mt)
+      if (8 * mt + g < SR)
+        *reinterpret_cast<double2*>(slab + (p * SR + 8 * mt + g) * 8 + 2 * t) = make_double2(c[mt][0], c[mt][1]);
+    __syncwarp();  // slot p fully read before it is refilled
+    ring.issue(p + kRingA, np);
   }
   ring.drain();
   q0 += np;
   for (int p = np; p < 32; ++p)
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
-      *reinterpret_cast<double2*>(slab + (p * MT * 8 + 8 * mt + g) * 8 + 2 * t) = make_double2(0.0, 0.0);
+      if (8 * mt + g < SR)
+        *reinterpret_cast<double2*>(slab + (p * SR + 8 * mt + g) * 8 + 2 * t) = make_double2(0.0, 0.0);
 }
 
 template <int L, int MT, int NT, int RT, int LT>
@@ -327,14 +314,20 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
   double* Hs = sm;                                      // R x R
   const int wib = threadIdx.x >> 5;
   constexpr bool BULK = RT > 0 && (RT % 2) == 0;     // 16-byte aligned records: TMA bulk copies
-  const int ringd = kRing * (l * R + R) + kRing;      // per warp: a-slab ring (doubles) + mbarriers
-  // per warp: slab of 32 patients x (MT 8) x 8, reused as the F_H ring (kRing x (2 l R + R))
-  const int slabd = 32 * MT * 8 * 8 > kRing * (2 * l * R + R) ? 32 * MT * 8 * 8 : kRing * (2 * l * R + R);
+  constexpr int SR = LT ? LT : MT * 8;                 // A rows kept per patient in the slab
+  // per warp: a-slab ring + 2 barrier sets, kept a multiple of 2 doubles (16-byte bulk-copy alignment)
+  const int ringd = kRingA * (l * R + R) + ((kRingA + kRing + 1) & ~1);
+  // per warp: slab of 32 patients x SR x 8, reused as the F_H ring (kRing x (2 l R + R))
+  const int slabd = 32 * SR * 8 > kRing * (2 * l * R + R) ? 32 * SR * 8 : kRing * (2 * l * R + R);
   double* slab = sm + hoff + wib * (slabd + ringd);
   double* ringbuf = slab + slabd;
-  uint64_t* bars = (uint64_t*)(ringbuf + kRing * (l * R + R));
-  if (BULK) ring_bars_init(bars);
-  int q0 = 0;  // records this warp has pulled through its ring (mbarrier phase continuity)
+  uint64_t* bars = (uint64_t*)(ringbuf + kRingA * (l * R + R));  // kRingA (a-slab ring)
+  uint64_t* barsf = bars + kRingA;                                 // kRing (F_H ring)
+  if (BULK) {
+    ring_bars_init(bars, kRingA);
+    ring_bars_init(barsf, kRing);
+  }
+  int q0 = 0, qf = 0;  // records pulled through each ring (mbarrier phase continuity)
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) Hs[x] = Hg[x];
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -364,14 +357,14 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
 #pragma unroll
       for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS, BULK>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
+      a_slab<MT, KS, BULK, SR>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
         if (8 * nt + cc < R) {
           double col[L];
 #pragma unroll
-          for (int a = 0; a < L; ++a) col[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+          for (int a = 0; a < L; ++a) col[a] = slab[(lane * SR + a) * 8 + cc];
           givens_insert_reg<L>(Rf, col);
         }
       }
@@ -405,7 +398,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS, BULK>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
+      a_slab<MT, KS, BULK, SR>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
       if (kme < K && mme > 0) {
         double* Q = Qt + kme * pstride;
@@ -415,7 +408,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
           if (s < R) {
             double y[L];
 #pragma unroll
-            for (int a = 0; a < L; ++a) y[a] = slab[(lane * MT * 8 + a) * 8 + cc];
+            for (int a = 0; a < L; ++a) y[a] = slab[(lane * SR + a) * 8 + cc];
             double q[L];
 #pragma unroll
             for (int a = 0; a < L; ++a) q[a] = 0.0;
@@ -457,8 +450,8 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
       const int lR = l * R;
       WarpRing<3, BULK> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R), staged in the (free) slab
       ring.buf = slab;
-      ring.bar = bars;
-      ring.q0 = q0;
+      ring.bar = barsf;
+      ring.q0 = qf;
       ring.per = 2 * lR + R;
       ring.src[0] = Qt + base * lR;
       ring.stride[0] = lR;
@@ -495,7 +488,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
         ring.issue(p + kRing, np);
       }
       ring.drain();
-      q0 += np;
+      qf += np;
       __syncwarp();  // the slab is rewritten by the next round
 #pragma unroll
       for (int i = 0; i < NT; ++i)
@@ -548,8 +541,9 @@ static void polar_wide_inst(Handle& h) {
   constexpr int MT = (L + 7) / 8;
   auto fn = k_polar_wide<L, MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
-  const size_t slabd = (size_t)std::max(32 * MT * 8 * 8, kRing * (2 * h.l * h.R + h.R));
-  const size_t per_warp = slabd + (size_t)(kRing * (h.l * h.R + h.R) + kRing);
+  constexpr int SR = LT ? LT : MT * 8;
+  const size_t slabd = (size_t)std::max(32 * SR * 8, kRing * (2 * h.l * h.R + h.R));
+  const size_t per_warp = slabd + (size_t)(kRingA * (h.l * h.R + h.R) + ((kRingA + kRing + 1) & ~1));
   int wpb = kDenseThreads / 32;  // warps per block: fewer when the per-warp slab + ring is large
   while (wpb > 1 && sizeof(double) * (hoff + wpb * per_warp) > 227 * 1024) wpb /= 2;
   const int threads = 32 * wpb;
