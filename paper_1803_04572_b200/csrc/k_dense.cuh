@@ -428,6 +428,10 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
       }
       __syncwarp();
     }
+    // Q~ rows were just written by this warp's threads (generic proxy) and are read back below by
+    // TMA bulk copies (async proxy): every writer fences its stores into the async proxy first.
+    if (BULK) asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncwarp();
     // ---- F_H += Q~_p^T (P'_p S_p): MMA with M = r, N = s, K = a (rows a >= m_p are zero)
     {
       int offq[2 * MT][NT];
