@@ -166,11 +166,12 @@ def test_single_visit_patients_and_tiny_patients(copa):
 
 
 @pytest.mark.parametrize("R,l,J", [(3, 0, 120), (16, 0, 120), (8, 5, 120), (24, 9, 120), (40, 12, 120), (20, 16, 120),
-                                   (64, 16, 120), (20, 7, 4000), (40, 7, 30000)])
+                                   (64, 16, 120), (20, 7, 4000), (40, 7, 30000), (8, 12, 120)])
 def test_shape_sweep(copa, R, l, J):
     """Kernel template/limit coverage: tall and wide polar, MMA tile counts, smooth l up to 16, and
     pass B's label groups: J = 4000 needs G = 4 F_V slices; J = 30000 (R = 40) fits no smem slice
-    and takes the FP64-atomic fallback."""
+    and takes the FP64-atomic fallback; l >= R (SURVEY N2 regime: smooth patients with l'_k >= R take
+    the tall polar)."""
     base = "medium" if l else "small"
     cfg = dataclasses.replace(synthgen.CONFIGS[base], R=R, smooth_l=l, K=400, J=J)
     p = synthgen.generate(cfg)
