@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
   const int grp = blockIdx.x % G;
   const int64_t rng = blockIdx.x / G;
   const SlotGeom sg = slot_geom(FB, PB, l, R);
-  double* Fs = (double*)smraw;  // Jg x RS
-  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + 127) & ~127ull);
+  double* Fs = (double*)smraw;  // Jg x RS, then W x 64 doubles of per-warp scratch (branch-free RMW)
+  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * 512 + 127) & ~127ull);
   uint64_t* full = (uint64_t*)(smraw + fs_bytes);
   uint64_t* empty = full + NSt;
   unsigned char* slots = smraw + fs_bytes + ((2 * NSt * 8 + 127) & ~127);
@@ -243,6 +243,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int g = lane >> 2, t = lane & 3;
     const int64_t jbase = grp * Jg;
     const int per = l * R;
+    double* scratch = Fs + (int64_t)Jg * RS + w * 64;
     double sink = 0.0;  // timing experiments (dbg 3, 4) only
     int offn[KS][NT];   // lane's B-fragment offsets inside an N_k block (-1: padding)
 #pragma unroll
@@ -324,22 +325,26 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
               for (int nt = 0; nt < NT; ++nt) sink += cc[b][nt][0] + cc[b][nt][1] + (double)col[b];
             return;
           }
+          // branch-free row updates: lanes without a valid (fiber, column) pair hit their scratch slot
+          double2* addr[NB][NT];
           double2 v[NB][NT];
 #pragma unroll
           for (int b = 0; b < NB; ++b)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-              if (col[b] >= 0 && 8 * nt + 2 * t < R)
-                v[b][nt] = *reinterpret_cast<const double2*>(Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t);
+            for (int nt = 0; nt < NT; ++nt) {
+              const bool ok = col[b] >= 0 && 8 * nt + 2 * t < R;
+              addr[b][nt] = reinterpret_cast<double2*>(ok ? Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t
+                                                          : scratch + 2 * lane);
+              v[b][nt] = *addr[b][nt];
+            }
 #pragma unroll
           for (int b = 0; b < NB; ++b)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-              if (col[b] >= 0 && 8 * nt + 2 * t < R) {
-                v[b][nt].x += cc[b][nt][0];
-                v[b][nt].y += cc[b][nt][1];
-                *reinterpret_cast<double2*>(Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t) = v[b][nt];
-              }
+            for (int nt = 0; nt < NT; ++nt) {
+              v[b][nt].x += cc[b][nt][0];
+              v[b][nt].y += cc[b][nt][1];
+              *addr[b][nt] = v[b][nt];
+            }
         };
         int tb = lo;
         for (; tb + 8 * (TB - 1) < hi; tb += 8 * TB) run_tiles(tb, std::integral_constant<int, TB>());
@@ -441,7 +446,7 @@ void plan_scatter(Handle& h) {
     for (int G = gmin; G <= kMaxGroups && !h.sc_ok; ++G) {
       const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
       const int64_t Jg = Js * h.sc_W;
-      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
+      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + (size_t)h.sc_W * 512 + 127) & ~(size_t)127;
       for (int NSt = 4; NSt >= (pass ? 2 : 3) && !h.sc_ok; --NSt)
         for (int pi = 0; pi < (pass ? 3 : 2) && !h.sc_ok; ++pi) {
           const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
@@ -461,7 +466,7 @@ void plan_scatter(Handle& h) {
   // Larger stages (FB = 512: fewer per-stage overheads; measured 43 -> 40 ms at Scale, 2.26 -> 2.10 ms
   // at Medium) when they still fit at the same G with >= 3 slots of >= 8 patients.
   if (h.sc_ok && !getenv("COPA_SC_FB")) {
-    const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + 127) & ~(size_t)127;
+    const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + (size_t)h.sc_W * 512 + 127) & ~(size_t)127;
     bool done = false;
     for (int NSt = 4; NSt >= 3 && !done; --NSt)
       for (int pi = 0; pi < 2 && !done; ++pi) {
