@@ -348,6 +348,10 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         };
         int tb = lo;
         for (; tb + 8 * (TB - 1) < hi; tb += 8 * TB) run_tiles(tb, std::integral_constant<int, TB>());
+        if (TB > 2 && tb + 8 < hi) {
+          run_tiles(tb, std::integral_constant<int, 2>());
+          tb += 16;
+        }
         for (; tb < hi; tb += 8) run_tiles(tb, std::integral_constant<int, 1>());
       }
       __syncwarp();
@@ -404,7 +408,12 @@ static void scatter_inst(Handle& h) {
 template <int KS>
 static void scatter_dispatch_n(Handle& h) {
   if (h.sc_W == 4) {
-    if (KS == 2 && h.l == 7 && h.R == 20) { scatter_inst_w<2, 3, 4, 2, 7, 20>(h); return; }
+    if (KS == 2 && h.l == 7 && h.R == 20) {
+      if (getenv("COPA_SC_TB4")) scatter_inst_w<2, 3, 4, 4, 7, 20>(h);        // tile-batch experiments
+      else if (getenv("COPA_SC_TB3")) scatter_inst_w<2, 3, 4, 3, 7, 20>(h);   // (no clear winner)
+      else scatter_inst_w<2, 3, 4, 2, 7, 20>(h);
+      return;
+    }
     if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 2, 7, 15>(h); return; }
     if (KS == 3 && h.l == 9 && h.R == 40) { scatter_inst_w<3, 5, 4, 2, 9, 40>(h); return; }
   }
