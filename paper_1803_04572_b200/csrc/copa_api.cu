@@ -87,8 +87,6 @@ size_t carve(Handle& h, char* base) {
     h.fiber_col = c.take<int32_t>(h.Fcap);
     h.fiber_val = c.take<double>(h.Fcap * h.l);
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
-    h.counter = c.take<int>(64);
-    h.order = c.take<int32_t>(h.K);
     h.perm = c.take<int32_t>(h.J);
     h.inv = c.take<int32_t>(h.Jl);
     h.Vl = c.take<double>(h.Jl * R + 64);  // +64: unpredicated pass-A gathers past the last row
@@ -103,9 +101,7 @@ size_t carve(Handle& h, char* base) {
     h.st_f = c.take<int64_t>(2 * h.nst_cap);
     h.st_k = c.take<int32_t>(2 * h.nst_cap);
     h.cta_st = c.take<int32_t>((int64_t)h.sc_ranges * G + 1);
-    size_t lt = fiber_layout_temp_bytes(h.K) + 12 * (size_t)h.K + 4096;
-    size_t gc = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;
-    h.layout_tmp_bytes = lt > gc ? lt : gc;
+    h.layout_tmp_bytes = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;  // per-group run lengths
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     h.row_patient = c.take<int32_t>(h.rows);
@@ -337,7 +333,6 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
     cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
     launch_layoutA(h);
-    build_fiber_layout(h, h.layout_tmp, h.layout_tmp_bytes);
   } else {
     launch_row_patient(h);
     if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);

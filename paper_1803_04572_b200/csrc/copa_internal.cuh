@@ -55,8 +55,6 @@ struct Handle {
   int64_t* gptr;       // smooth: [G x (K+1)] absolute offset of patient k's run in stream g
   int64_t Fcap = 0;    // fiber slots incl. stream padding
   // fiber-pass layout (smooth): relabeled features, pass A order, pass B CTAs and stage table
-  int* counter;          // pass A work counter
-  int32_t* order;        // [K] patients by fiber count, descending
   int32_t* perm;         // [J] feature -> label
   int32_t* inv;          // [Jl] label -> feature (-1: unused label)
   double* Vl;            // [Jl x R] V̄ in label order (pass A)
@@ -232,8 +230,6 @@ int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
 void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int32_t* perm, int32_t* inv, int64_t* Js);
-size_t fiber_layout_temp_bytes(int64_t K);
-void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes);  // pass A order (device)
 int64_t stage_cap(const Handle& h);                                // pass-B stage table bound
 // host: gptr (G x (K+1), absolute) from per-group counts; stage table; pass-B patient ranges
 void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::vector<int64_t>& st_f,

@@ -571,21 +571,7 @@ void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int
   cta_st[(size_t)nr * G] = (int32_t)(st_k.size() / 2);
 }
 
-// ------------------------------------------------------------------ init-time layout for pass A
-__global__ void k_fiber_counts(const int64_t* fiber_ptr, int64_t K, int32_t* cnt, int32_t* idx) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  cnt[k] = (int32_t)(fiber_ptr[k + 1] - fiber_ptr[k]);
-  idx[k] = (int32_t)k;
-}
-
-size_t fiber_layout_temp_bytes(int64_t K) {
-  size_t a = 0;
-  cub::DeviceRadixSort::SortPairsDescending(nullptr, a, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
-                                            (int32_t*)nullptr, (int)K);
-  return a + 256;
-}
-
+// ------------------------------------------------------------------ init-time relabeling
 // Feature relabeling from the per-feature fiber counts: features sorted by count (descending,
 // ties by id) are dealt serpentine over the G*W label sub-ranges of Js labels each; perm[j] = new
 // label, inv[new] = j. Host-side (J <= 65535).
@@ -606,23 +592,6 @@ void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int3
     inv[label] = idx[(size_t)i];
   }
   *Js = js;
-}
-
-// Pass A patient order (by fiber count, descending). tmp: >= fiber_layout_temp_bytes(K) + 12 K bytes.
-void build_fiber_layout(Handle& h, void* tmp, size_t tmp_bytes) {
-  (void)tmp_bytes;
-  cudaStream_t s = h.stream;
-  char* p = (char*)tmp;
-  auto take = [&](size_t n) { char* r = p; p += (n + 255) & ~(size_t)255; return (void*)r; };
-  int32_t* cnt = (int32_t*)take(sizeof(int32_t) * (size_t)h.K);
-  int32_t* cnt_sorted = (int32_t*)take(sizeof(int32_t) * (size_t)h.K);
-  int32_t* idx = (int32_t*)take(sizeof(int32_t) * (size_t)h.K);
-  size_t sort_bytes = fiber_layout_temp_bytes(h.K);
-  void* sort_tmp = take(sort_bytes);
-  if (h.K > 0) {
-    k_fiber_counts<<<(unsigned)((h.K + 255) / 256), 256, 0, s>>>(h.fiber_ptr, h.K, cnt, idx);
-    cub::DeviceRadixSort::SortPairsDescending(sort_tmp, sort_bytes, cnt, cnt_sorted, idx, h.order, (int)h.K, 0, 32, s);
-  }
 }
 
 }  // namespace copa
