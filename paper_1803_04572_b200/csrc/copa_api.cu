@@ -93,6 +93,8 @@ size_t carve(Handle& h, char* base) {
     h.fa_col = c.take<int32_t>(h.F + 64);
     h.fa_val = c.take<double>((h.F + 64) * h.l);
     h.pa_wk = c.take<int64_t>(h.pa_nw + 1);
+    h.hot_slot = c.take<int32_t>(h.Jl);
+    h.hot_lab = c.take<int32_t>(h.pa_nhot > 0 ? h.pa_nhot : 1);
     h.block_k = c.take<int64_t>(h.sc_ranges + 1);
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
@@ -285,6 +287,13 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       compute_relabel(h.J, h.sc_G * h.sc_W, hist.data(), perm.data(), inv.data(), &Js);
       CUDA_TRY(cudaMemcpyAsync(h.perm, perm.data(), sizeof(int32_t) * (size_t)h.J, cudaMemcpyHostToDevice, s), "perm");
       CUDA_TRY(cudaMemcpyAsync(h.inv, inv.data(), sizeof(int32_t) * (size_t)h.Jl, cudaMemcpyHostToDevice, s), "inv");
+      std::vector<int32_t> hslot, hlab;
+      plan_passA_hot(h, hist.data(), inv.data(), hslot, hlab);
+      CUDA_TRY(cudaMemcpyAsync(h.hot_slot, hslot.data(), sizeof(int32_t) * hslot.size(), cudaMemcpyHostToDevice, s),
+               "hot_slot");
+      if (!hlab.empty())
+        CUDA_TRY(cudaMemcpyAsync(h.hot_lab, hlab.data(), sizeof(int32_t) * hlab.size(), cudaMemcpyHostToDevice, s),
+                 "hot_lab");
       CUDA_TRY(cudaStreamSynchronize(s), "perm sync");
     }
     {  // g-stream layout: per-group run lengths (device) -> offsets and pass-B stage table (host)

@@ -64,6 +64,9 @@ struct Handle {
   int64_t pa_nw = 0;
   int pa_ctas = 0;
   bool pa_vs = false;    // V̄ in shared memory in pass A
+  int pa_nhot = 0;       // else: rows of the pa_nhot heaviest labels staged in shared memory
+  int32_t* hot_slot;     // [Jl] label -> hot slot or -1
+  int32_t* hot_lab;      // [pa_nhot] hot slot -> label
   int64_t* block_k;      // [sc_ranges+1] patient range of each pass-B range
   double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
   unsigned long long* fhist;  // [J] fibers per feature (init)
@@ -226,6 +229,8 @@ void launch_relabel_V(Handle& h);
 void launch_layoutA(Handle& h);
 void plan_passA(Handle& h);
 void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
+void plan_passA_hot(const Handle& h, const unsigned long long* hist, const int32_t* inv, std::vector<int32_t>& slot,
+                    std::vector<int32_t>& lab);
 int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
