@@ -61,6 +61,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Producer-side wait: the producer shares an SM sub-partition with a consumer warp, so it backs off
+// with nanosleep instead of spinning on try_wait (a tight spin takes issue slots from that consumer).
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, unsigned ns) {
+  while (!mbar_try(b, parity)) __nanosleep(ns);
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
     const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l_, int R_, int RS_, int FB, int PB,
-    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg, int pf_scale) {
+    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg, int pf_scale, unsigned psleep) {
   const int R = RT ? RT : R_;           // compile-time for the configured (R, l) shapes
   const int l = LT ? LT : l_;
   const int RS = RT ? ((RT + 1) & ~1) : RS_;
@@ -199,7 +213,8 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
           nf0 = st_f[2 * st]; nf1 = st_f[2 * st + 1];
           nk0 = st_k[2 * st]; nk1 = st_k[2 * st + 1];
         }
-        mbar_wait(empty + slot, phase);
+        if (psleep) mbar_wait_sleep(empty + slot, phase, psleep);
+        else mbar_wait(empty + slot, phase);
         unsigned char* base = slots + (size_t)slot * sg.bytes;
         int64_t* meta = (int64_t*)base;
         int32_t* mi = (int32_t*)(base + 16);
@@ -394,7 +409,8 @@ static void scatter_inst_w(Handle& h) {
                                                    h.st_f, h.st_k, h.cta_st, h.woff, h.l, h.R, h.sc_RS, h.sc_FB,
                                                    h.sc_PB, h.sc_NS, h.Nst, h.fv_part,
                                                    getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0,
-                                                   getenv("COPA_SC_PF") ? atoi(getenv("COPA_SC_PF")) : 0);  // L2 frontier: off (no gain, +15 GB DRAM)
+                                                   getenv("COPA_SC_PF") ? atoi(getenv("COPA_SC_PF")) : 0,  // L2 frontier: off (no gain, +15 GB DRAM)
+                                                   getenv("COPA_SC_SLEEP") ? (unsigned)atoi(getenv("COPA_SC_SLEEP")) : 256u);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
