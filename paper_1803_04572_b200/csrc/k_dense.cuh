@@ -233,7 +233,11 @@ __device__ __forceinline__ void ring_bars_init(uint64_t* bar, int n = kRing) {
 // A_p = P'_p S_p H^T. MMA: M = a (MT tiles), N = s (this slab), K = r (KS steps). Rows a >= m_p of
 // P'_p are zero (never written), so only a < l is checked. P'_p and w̄_p arrive through the warp's
 // cp.async ring, kRing patients ahead of the MMAs.
-template <int MT, int KS, bool BULK, int SR>
+//
+// FAST (MT == 1, l >= 7, R % 4 == 0): fragment loads without masks from a per-lane base. Every K
+// index r = 4 ks + t is < R; the only out-of-range operand row is a = g >= l (g = 7 when l = 7),
+// which reads in-record values (the w̄ part) and only feeds row 7 of D, never stored.
+template <int MT, int KS, bool BULK, int SR, bool FAST = false>
 __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, int R, const double* Pp,
                                        const double* W, const double* Hs, double* slab, double* ringbuf,
                                        uint64_t* bars, int& q0) {
@@ -274,13 +278,20 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
     double c[MT][2];
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt) c[mt][0] = c[mt][1] = 0.0;
+    if (FAST) {
+      const double* ra = rec + g * R + t;
+      const double* rw = rec + lR + t;
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const double wr = offw[ks] >= 0 ? rec[offw[ks]] : 0.0;
+      for (int ks = 0; ks < KS; ++ks) dmma2(c[0][0], c[0][1], ra[4 * ks] * rw[4 * ks], hb[ks]);
+    } else {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        const double av = offp[ks][mt] >= 0 ? rec[offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
-        dmma2(c[mt][0], c[mt][1], av, hb[ks]);
+      for (int ks = 0; ks < KS; ++ks) {
+        const double wr = offw[ks] >= 0 ? rec[offw[ks]] : 0.0;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+          const double av = offp[ks][mt] >= 0 ? rec[offp[ks][mt]] * wr : 0.0;  // A[g][t] = (P'S)(a, r)
+          dmma2(c[mt][0], c[mt][1], av, hb[ks]);
+        }
       }
     }
 #pragma unroll
@@ -305,7 +316,10 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
                                                        const double* __restrict__ Hg, double tau,
                                                        double* __restrict__ Qt, int32_t* __restrict__ rank,
                                                        double* __restrict__ FHwarp, int nextpf) {
-  constexpr int KS = (NT * 8 + 3) / 4;  // r steps of 4 covering 8 NT >= R
+  constexpr int KS = RT ? (RT + 3) / 4 : (NT * 8 + 3) / 4;  // r steps of 4 covering R (an all-zero step
+                                                             // costs a DMMA like any other)
+  // fixed-shape slab path: unmasked fragment loads (needs l >= 7, one M tile, R % 4 == 0; see a_slab)
+  constexpr bool FAST = MT == 1 && LT >= 7 && RT > 0 && RT % 4 == 0;
   constexpr int RP = 8 * NT;
   const int R = RT ? RT : R_;           // compile-time for the configured (R, l) pairs
   const int l = LT ? LT : l_;
@@ -357,7 +371,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
 #pragma unroll
       for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS, BULK, SR>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
+      a_slab<MT, KS, BULK, SR, FAST>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
@@ -398,7 +412,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
     for (int nt = 0; nt < NT; ++nt) {
-      a_slab<MT, KS, BULK, SR>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
+      a_slab<MT, KS, BULK, SR, FAST>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
       if (kme < K && mme > 0) {
         double* Q = Qt + kme * pstride;
@@ -608,7 +622,7 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
                                                     double* __restrict__ part /* [blocks][2][R R] */,
                                                     int getenv_l1, int nextpf) {
   constexpr int RP = 8 * NT;
-  constexpr int KS = (NT * 8 + 3) / 4;  // i steps of 4 covering 8 NT >= R
+  constexpr int KS = RT ? (RT + 3) / 4 : (NT * 8 + 3) / 4;  // i steps of 4 covering R
   const int R = RT ? RT : R_;
   const int l = LT ? LT : l_;
   extern __shared__ double sm[];
