@@ -2,7 +2,9 @@
 // outer iteration on one stream, and the allreduce hand-off points C1/C2.
 #include <cub/cub.cuh>
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -247,6 +249,23 @@ copa_status copa_workspace_size(const copa_problem* p, const copa_options* o, si
   return COPA_OK;
 }
 
+// Init stage timing (COPA_INIT_TIMES=1): synchronises the stream at each mark and prints the
+// elapsed host time per stage to stderr. Off by default (the marks are no-ops).
+namespace {
+struct InitTimer {
+  bool on = getenv("COPA_INIT_TIMES") != nullptr;
+  cudaStream_t s = nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* name) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[copa init] %-16s %9.2f ms\n", name, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+}  // namespace
+
 copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out) {
   copa_status st = check_args(p, o);
   if (st != COPA_OK) return st;
@@ -256,8 +275,12 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   if (!H) return fail(COPA_E_ARG, "out of host memory");
   Handle& h = H->h;
   fill_sizes(h, p, o);
+  InitTimer tm;
+  tm.s = h.stream;
+  tm.mark("start");
   st = count_fibers(h, &h.F, &h.cub_temp_bytes);
   if (st != COPA_OK) { delete H; return st; }
+  tm.mark("count_fibers F");
   size_t need = carve(h, nullptr);
   if (bytes < need) { delete H; return fail(COPA_E_WORKSPACE, "workspace too small: need " + std::to_string(need)); }
   carve(h, (char*)ws);
@@ -272,11 +295,13 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   launch_validate(h);
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
+  tm.mark("memset+validate");
   if (h.smooth) {
     if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
     launch_count_fibers(h, h.fiber_ptr, h.fhist);
     size_t tb = h.cub_temp_bytes;
     if (h.K > 0) cub::DeviceScan::InclusiveSum(h.cub_temp, tb, h.fiber_ptr, h.fiber_ptr, (int)(h.K + 1), s);
+    tm.mark("fiber_ptr");
     {  // feature relabeling by fiber mass (host, J <= 65535)
       std::vector<unsigned long long> hist((size_t)h.J);
       std::vector<int32_t> perm((size_t)h.J), inv((size_t)h.Jl);
@@ -296,6 +321,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
                  "hot_lab");
       CUDA_TRY(cudaStreamSynchronize(s), "perm sync");
     }
+    tm.mark("relabel");
     {  // g-stream layout: per-group run lengths (device) -> offsets and pass-B stage table (host)
       const int G = h.sc_G;
       int32_t* gcnt_dev = (int32_t*)h.layout_tmp;
@@ -306,6 +332,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
         CUDA_TRY(cudaMemcpyAsync(gcnt.data(), gcnt_dev, sizeof(int32_t) * gcnt.size(), cudaMemcpyDeviceToHost, s),
                  "gcnt copy");
       CUDA_TRY(cudaStreamSynchronize(s), "gcnt sync");
+      tm.mark("count_groups");
       std::vector<int64_t> st_f, block_k;
       std::vector<int32_t> st_k, cta_st;
       plan_streams(h, gcnt.data(), gptr.data(), st_f, st_k, cta_st, block_k);
@@ -323,6 +350,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
                "cta_st");
       CUDA_TRY(cudaMemcpyAsync(h.block_k, block_k.data(), sizeof(int64_t) * block_k.size(), cudaMemcpyHostToDevice, s),
                "block_k");
+      tm.mark("plan_streams+h2d");
       {  // pass-A warp ranges (fiber-balanced) from the per-patient fiber counts
         std::vector<int64_t> fp((size_t)h.K + 1, 0), wk;
         for (int64_t k = 0; k < h.K; ++k) {
@@ -336,12 +364,16 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       }
       CUDA_TRY(cudaStreamSynchronize(s), "layout sync");  // host vectors go out of scope
     }
+    tm.mark("passA ranges");
     launch_basis(h);
+    tm.mark("basis");
     launch_build_fibers(h);
+    tm.mark("build_fibers");
     cudaMemsetAsync(h.fa_col + h.F, 0, 64 * sizeof(int32_t), s);  // slack read by the pass-A chunk grid
     cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
     cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
     launch_layoutA(h);
+    tm.mark("layoutA");
   } else {
     launch_row_patient(h);
     if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);
@@ -364,6 +396,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   }
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
+  tm.mark("factors+grams");
   *out = H;
   return COPA_OK;
 }

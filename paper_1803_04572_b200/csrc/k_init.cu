@@ -7,6 +7,7 @@
 #include <cub/cub.cuh>
 
 #include "copa_internal.cuh"
+#include "k_dense.cuh"  // register Givens / Jacobi helpers (givens_insert_reg, jacobi_rows_reg)
 
 namespace copa {
 
@@ -164,10 +165,85 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
   m[k] = c;
 }
 
+// Same computation with the l x l factor in registers (fixed l): Givens insert of each spline row
+// (zero entries are skipped), round-robin one-sided Jacobi, kept columns placed by their rank in
+// descending sigma (stable) — the order the selection loop above produces.
+template <int L>
+__global__ void __launch_bounds__(64) k_basis_reg(const int64_t* prp, const double* times, int64_t K, int d,
+                                                  double tau, double* Bk, int32_t* m) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = k < K;
+  int64_t r0 = 0, r1 = 0;
+  double t1 = 0.0, tn = 0.0;
+  if (live) {
+    r0 = prp[k];
+    r1 = prp[k + 1];
+    t1 = times[r0];
+    tn = times[r1 - 1];
+  }
+  const bool active = live && tn > t1;  // single visit: M_k = 0
+  double Rm[L][L];
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j) Rm[i][j] = 0.0;
+  for (int64_t i = r0; active && i < r1; ++i) {
+    double N[kMaxDeg + 1];
+    const int mu = spline_eval(times[i], t1, tn, L, d, N);
+    double a[L];
+#pragma unroll
+    for (int b = 0; b < L; ++b) {
+      const int r = b - (mu - d);
+      a[b] = (r >= 0 && r <= d) ? N[r] : 0.0;
+    }
+    givens_insert_reg<L>(Rm, a);
+  }
+  jacobi_rows_reg<L>(Rm);  // warp-collective convergence vote: every lane takes part
+  if (!live) return;
+  double* B = Bk + k * (int64_t)L * L;
+  double sig[L], smax = 0.0;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) s = fma(Rm[j][i], Rm[j][i], s);
+    sig[j] = sqrt(s);
+    smax = fmax(smax, sig[j]);
+  }
+  int c = 0;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const bool keep = active && smax > 0.0 && sig[j] > tau * smax;
+    c += keep ? 1 : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    if (!(active && smax > 0.0 && sig[j] > tau * smax)) continue;
+    int pos = 0;
+#pragma unroll
+    for (int q = 0; q < L; ++q) pos += (sig[q] > sig[j] || (q < j && sig[q] == sig[j])) ? 1 : 0;
+    const double inv2 = 1.0 / (sig[j] * sig[j]);
+#pragma unroll
+    for (int i = 0; i < L; ++i) B[i * L + pos] = Rm[j][i] * inv2;
+  }
+  for (int cc = c; cc < L; ++cc)
+#pragma unroll
+    for (int i = 0; i < L; ++i) B[i * L + cc] = 0.0;
+  m[k] = c;
+}
+
 void launch_basis(Handle& h) {
   if (h.K == 0) return;
-  k_basis<<<(unsigned)((h.K + 63) / 64), 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.l, h.d,
-                                                          h.o.basis_tol, h.Bk, h.m);
+  const unsigned blocks = (unsigned)((h.K + 63) / 64);
+  if (h.l == 7) {
+    k_basis_reg<7><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m);
+    return;
+  }
+  if (h.l == 9) {
+    k_basis_reg<9><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m);
+    return;
+  }
+  k_basis<<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.l, h.d, h.o.basis_tol, h.Bk, h.m);
 }
 
 // ------------------------------------------------------------------ fibers: per-group counts
@@ -254,85 +330,145 @@ void launch_count_groups(Handle& h, int32_t* gcnt) {
 // ------------------------------------------------------------------ fibers: build X'_k = C_k^T X_k
 // Warp per patient. The fibers of a patient are its distinct labels; the fiber with label j goes to
 // stream g = j / Jg at gptr[g][k] + (rank(j) - rank(g Jg)), so every stream is sorted by label within
-// each patient. Rows are processed in order; within a row the lanes own distinct nonzeros (distinct
-// columns => distinct fibers), so the accumulation is race-free and its order (ascending row)
-// deterministic.
-__global__ void k_build_fibers(const int64_t* prp, const int64_t* rp, const int32_t* col, const double* val,
-                               const double* times, int64_t K, int words, int l, int d, const double* Bk,
-                               const int32_t* m, const int64_t* gptr, int G, int64_t Jg, const int32_t* perm,
-                               int32_t* fiber_col, double* fiber_val) {
-  extern __shared__ unsigned smem_b[];
+// each patient. The fibers are accumulated in shared memory, kBfWF ranks per window (patients with
+// more distinct labels take several windows), then written out coalesced.
+// Per window: rows in chunks (<= 32 rows, <= kBfNZ nonzeros): lane r evaluates the spline row
+// C_k(i0 + r, :) = M_k(i, :) B_k into smem and the chunk's (rank, value) pairs are staged in smem;
+// then rows one after the other, lanes over the row's (nonzero, a) pairs: a row's nonzeros have
+// distinct labels, so the updates Fs(f, a) = fma(x, C(i, a), Fs(f, a)) of one row never collide, and
+// every fiber entry is accumulated in ascending row order (deterministic).
+constexpr int kBfWF = 256;   // fiber ranks per shared-memory window
+constexpr int kBfWarps = 4;  // warps (patients in flight) per block
+constexpr int kBfNZ = 256;   // staged nonzeros per row chunk
+
+__host__ __device__ inline size_t bf_warp_doubles(int l, int words) {
+  // Fs [WF l] | Cs [32 l] | xz [NZ] | rps [33] i64 | gd [kMaxGroups] i64 | fz [NZ] i32 | lab, dst [WF] i32 |
+  // bits, pref [words]
+  return (size_t)kBfWF * l + 32 * (size_t)l + kBfNZ + 33 + kMaxGroups + kBfNZ / 2 + kBfWF + (size_t)words;
+}
+
+__global__ void __launch_bounds__(32 * kBfWarps) k_build_fibers(
+    const int64_t* prp, const int64_t* rp, const int32_t* col, const double* val, const double* times, int64_t K,
+    int words, int l, int d, const double* Bk, const int32_t* m, const int64_t* gptr, int G, int Jg,
+    const int32_t* perm, int32_t* fiber_col, double* fiber_val) {
+  extern __shared__ double smem_bf[];
+  const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  unsigned* bits = smem_b + wib * words;
-  int* pref = (int*)(smem_b + nw * words) + wib * words;
-  const int64_t nwarps = (int64_t)gridDim.x * nw;
+  double* Fs = smem_bf + (size_t)wib * bf_warp_doubles(l, words);
+  double* Cs = Fs + (size_t)kBfWF * l;
+  double* xz = Cs + 32 * l;
+  int64_t* rps = (int64_t*)(xz + kBfNZ);
+  int64_t* gd = rps + 33;
+  int32_t* fz = (int32_t*)(gd + kMaxGroups);
+  int32_t* lab = fz + kBfNZ;
+  int32_t* grp = lab + kBfWF;
+  unsigned* bits = (unsigned*)(grp + kBfWF);
+  int* pref = (int*)(bits + words);
+  const int64_t nwarps = (int64_t)gridDim.x * kBfWarps;
   const int64_t K1 = K + 1;
-  for (int64_t k = blockIdx.x * (int64_t)nw + wib; k < K; k += nwarps) {
+  for (int64_t k = blockIdx.x * (int64_t)kBfWarps + wib; k < K; k += nwarps) {
     patient_label_bitmap(prp, rp, col, perm, k, words, bits, pref);
-    // per-group destination offset: dst(j) = gptr[g][k] - rank(g Jg) + rank(j)
-    int64_t gdst[kMaxGroups];
-#pragma unroll
-    for (int g = 0; g < kMaxGroups; ++g)
-      gdst[g] = g < G ? gptr[g * K1 + k] - label_rank(bits, pref, words, g * Jg) : 0;
-    for (int w = lane; w < words; w += 32) {
-      unsigned b = bits[w];
-      int rk = pref[w];
-      while (b) {
-        const int bit = __ffs(b) - 1;
-        b &= b - 1;
-        const int64_t j = (int64_t)w * 32 + bit;
-        const int g = (int)(j / Jg);
-        const int64_t dst = gdst[g] + rk;
-        fiber_col[dst] = (int32_t)j;
-        for (int a = 0; a < l; ++a) fiber_val[dst * l + a] = 0.0;
-        ++rk;
-      }
-    }
-    __syncwarp();
+    const int nf = pref[words - 1] + __popc(bits[words - 1]);
+    if (lane < G) gd[lane] = gptr[lane * K1 + k] - label_rank(bits, pref, words, (int64_t)lane * Jg);
     const int mk = m[k];
+    // p / mk = umulhi(p, ceil(2^32 / mk)), exact for p < 2^24 (p < J mk here)
+    const unsigned mmagic = mk > 0 ? (unsigned)((0x100000000ull + mk - 1) / mk) : 0u;
     const double* B = Bk + k * (int64_t)l * l;
     const int64_t r0 = prp[k], r1 = prp[k + 1];
     const double t1 = times[r0], tn = times[r1 - 1];
-    if (mk > 0) {
-      for (int64_t i = r0; i < r1; ++i) {
-        double N[kMaxDeg + 1];
-        const int mu = spline_eval(times[i], t1, tn, l, d, N);
-        double c[kMaxL];  // C_k(i, :) = M_k(i, :) B_k
-        for (int a = 0; a < mk; ++a) {
-          double s = 0.0;
-          for (int r = 0; r <= d; ++r) s = fma(N[r], B[(mu - d + r) * l + a], s);
-          c[a] = s;
-        }
-        for (int64_t e = rp[i] + lane; e < rp[i + 1]; e += 32) {
-          const int32_t j = perm[col[e]];
-          const double x = val[e];
-          const int g = (int)(j / Jg);
-          double* dst = fiber_val + (gdst[g] + label_rank(bits, pref, words, j)) * l;
-          for (int a = 0; a < mk; ++a) dst[a] = fma(x, c[a], dst[a]);
-        }
+    for (int w0 = 0; w0 < nf; w0 += kBfWF) {
+      const int nw = min(kBfWF, nf - w0);
+      for (int x = lane; x < nw * l; x += 32) Fs[x] = 0.0;
+      __syncwarp();
+      int nr = 0;
+      for (int64_t i0 = r0; mk > 0 && i0 < r1; i0 += nr) {
+        const int n32 = (int)min((int64_t)32, r1 - i0);
+        if (lane < n32) rps[lane] = rp[i0 + lane];
+        if (lane == 0) rps[n32] = rp[i0 + n32];
         __syncwarp();
+        // rows of this chunk: as many as fit kBfNZ staged nonzeros (at least one)
+        const unsigned fit = __ballot_sync(FULL, lane < n32 && rps[lane + 1] - rps[0] <= kBfNZ);
+        nr = fit ? 32 - __clz(fit) : 1;  // fit is a prefix of lanes (row_ptr is monotone)
+        const int64_t e0 = rps[0];
+        const int nz = (int)(rps[nr] - e0);
+        const bool staged = nz <= kBfNZ;
+        if (lane < nr) {
+          double N[kMaxDeg + 1];
+          const int mu = spline_eval(times[i0 + lane], t1, tn, l, d, N);
+          for (int a = 0; a < mk; ++a) {
+            double s = 0.0;
+            for (int r = 0; r <= d; ++r) s = fma(N[r], B[(mu - d + r) * l + a], s);
+            Cs[lane * l + a] = s;
+          }
+        }
+        if (staged)
+          for (int e = lane; e < nz; e += 32) {
+            fz[e] = label_rank(bits, pref, words, perm[col[e0 + e]]) - w0;
+            xz[e] = val[e0 + e];
+          }
+        __syncwarp();
+        for (int r = 0; r < nr; ++r) {
+          const int eb = (int)(rps[r] - e0), ne = (int)(rps[r + 1] - rps[r]);
+          const double* C = Cs + r * l;
+          for (int p = lane; p < ne * mk; p += 32) {  // lanes over the row's (nonzero, a) pairs
+            const int e = (int)__umulhi((unsigned)p, mmagic);
+            const int a = p - e * mk;
+            int f;
+            double x;
+            if (staged) {
+              f = fz[eb + e];
+              x = xz[eb + e];
+            } else {  // a single row longer than kBfNZ: straight from global memory
+              f = label_rank(bits, pref, words, perm[col[e0 + eb + e]]) - w0;
+              x = val[e0 + eb + e];
+            }
+            if (f >= 0 && f < nw) Fs[f * l + a] = fma(x, C[a], Fs[f * l + a]);
+          }
+          __syncwarp();
+        }
       }
+      // labels (and streams) of this window's ranks, then the window's fibers
+      for (int wd = lane; wd < words; wd += 32) {
+        unsigned b = bits[wd];
+        int rk = pref[wd];
+        if (rk >= w0 + nw || rk + __popc(b) <= w0) continue;
+        while (b) {
+          const int bit = __ffs(b) - 1;
+          b &= b - 1;
+          if (rk >= w0 && rk < w0 + nw) {
+            const int j = wd * 32 + bit;
+            lab[rk - w0] = j;
+            grp[rk - w0] = j / Jg;
+          }
+          ++rk;
+        }
+      }
+      __syncwarp();
+      for (int f = lane; f < nw; f += 32) {
+        const int64_t dst = gd[grp[f]] + w0 + f;
+        fiber_col[dst] = lab[f];
+        double* o = fiber_val + dst * l;
+        for (int a = 0; a < l; ++a) o[a] = Fs[f * l + a];
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
 void launch_build_fibers(Handle& h) {
   if (h.K == 0) return;
   const int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
-  const int warps = 8;
-  const size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
+  const size_t smem = (size_t)kBfWarps * bf_warp_doubles(h.l, words) * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_build_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_build_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr = true;
   }
-  int64_t blocks = (h.K + warps - 1) / warps;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_build_fibers<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(
+  int64_t blocks = (h.K + kBfWarps - 1) / kBfWarps;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  k_build_fibers<<<(unsigned)blocks, kBfWarps * 32, smem, h.stream>>>(
       h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m, h.gptr,
-      h.sc_G, h.sc_Jg, h.perm, h.fiber_col, h.fiber_val);
+      h.sc_G, (int)h.sc_Jg, h.perm, h.fiber_col, h.fiber_val);
 }
 
 // ------------------------------------------------------------------ non-smooth helpers
