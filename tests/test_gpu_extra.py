@@ -165,6 +165,33 @@ def test_single_visit_patients_and_tiny_patients(copa):
     assert rel(g.U().cpu().numpy(), o.U_all()) <= 1e-9
 
 
+def test_fiber_build_dense_rows_and_wide_patients(copa):
+    """Init fiber build edge cases: rows with more nonzeros than a staged row chunk holds (256;
+    read straight from global memory), row chunks cut short by the nonzero cap, and patients with
+    more distinct features than one shared-memory window (256 ranks -> several windows)."""
+    rng = np.random.default_rng(11)
+    J, R = 700, 10
+    mats, times = [], []
+    for k in range(40):
+        I = int(rng.integers(2, 30))
+        dens = 0.02 if k % 3 else 0.45  # every third patient: dense rows (~315 nonzeros each)
+        X = (rng.uniform(size=(I, J)) < dens) * rng.integers(1, 4, size=(I, J)).astype(float)
+        if k % 5 == 0:
+            X[0, :] = rng.integers(1, 4, size=J)  # one row with all 700 features
+        X[:, k % J] += 1.0
+        mats.append(X)
+        times.append(np.sort(rng.uniform(0, 36.5 * I, size=I)))
+    p = make_problem(mats, R, base="medium", times=np.concatenate(times), con_V=(2, 0.1))
+    g = copa.Copa(p, copa.Options.from_config(p.cfg))
+    o = oracle.Oracle(p)
+    fg = g.iterate(1)
+    fo = o.iterate(1)
+    H, V, W = [x.cpu().numpy() for x in g.factors()]
+    assert abs(fg[0] - fo[0]) <= 1e-9
+    for a, b, what in ((H, o.H, "H"), (V, o.V, "V"), (W, o.W, "W")):
+        assert rel(a, b) <= 1e-9, (what, rel(a, b))
+
+
 @pytest.mark.parametrize("R,l,J", [(3, 0, 120), (16, 0, 120), (8, 5, 120), (24, 9, 120), (40, 12, 120), (20, 16, 120),
                                    (64, 16, 120), (20, 7, 4000), (40, 7, 30000), (8, 12, 120)])
 def test_shape_sweep(copa, R, l, J):
