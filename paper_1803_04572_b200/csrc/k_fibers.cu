@@ -258,8 +258,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int g = lane >> 2, t = lane & 3;
     const int64_t jbase = grp * Jg;
     const int per = l * R;
-    double* scratch = Fs + (int64_t)Jg * RS + w * 64;
-    double sink = 0.0;  // timing experiments (dbg 3, 4) only
+    const int scr = (int)Jg * RS + w * 64 + 2 * lane;  // this lane's scratch slot (index into Fs)
     int offn[KS][NT];   // lane's B-fragment offsets inside an N_k block (-1: padding)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
@@ -305,7 +304,6 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
           for (int nt = 0; nt < NT; ++nt) bfr[ks][nt] = nbfr[ks][nt];
         if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
         if (lo >= hi) continue;
-        if (dbg == 3) { sink += bfr[0][0]; continue; }
         // TB tiles at a time while >= TB tiles remain, then single tiles (no MMAs on empty tiles).
         // Tiles of one sub-run belong to one patient => distinct labels => distinct F_V rows, so
         // all row loads of a batch may precede its stores.
@@ -333,24 +331,17 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             for (int b = 0; b < NB; ++b)
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) dmma(cc[b][nt][0], cc[b][nt][1], av[b][ks], bfr[ks][nt]);
-          if (dbg == 4) {
-#pragma unroll
-            for (int b = 0; b < NB; ++b)
-#pragma unroll
-              for (int nt = 0; nt < NT; ++nt) sink += cc[b][nt][0] + cc[b][nt][1] + (double)col[b];
-            return;
-          }
-          // branch-free row updates: lanes without a valid (fiber, column) pair hit their scratch slot
-          double2* addr[NB][NT];
+          // branch-free row updates: lanes without a valid (fiber, column) pair hit their scratch
+          // slot. Shared-memory indices (not pointers) so the accesses stay plain LDS/STS.
+          int idx[NB][NT];
           double2 v[NB][NT];
 #pragma unroll
           for (int b = 0; b < NB; ++b)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const bool ok = col[b] >= 0 && 8 * nt + 2 * t < R;
-              addr[b][nt] = reinterpret_cast<double2*>(ok ? Fs + (col[b] - jbase) * RS + 8 * nt + 2 * t
-                                                          : scratch + 2 * lane);
-              v[b][nt] = *addr[b][nt];
+              idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
+              v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
             }
 #pragma unroll
           for (int b = 0; b < NB; ++b)
@@ -358,7 +349,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             for (int nt = 0; nt < NT; ++nt) {
               v[b][nt].x += cc[b][nt][0];
               v[b][nt].y += cc[b][nt][1];
-              *addr[b][nt] = v[b][nt];
+              *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
             }
         };
         int tb = lo;
@@ -373,7 +364,6 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
       if (lane == 0) mbar_arrive(empty + slot);
       if (++slot == NSt) { slot = 0; phase ^= 1; }
     }
-    if (dbg >= 3 && sink == 12345.678) Fs[0] += sink;
   }
   __syncthreads();
   double* out = FVpart + rng * (G * Jg) * (int64_t)R + (int64_t)grp * Jg * R;
