@@ -416,8 +416,8 @@ static void scatter_dispatch_n(Handle& h) {
   if (h.sc_W == 4) {
     if (KS == 2 && h.l == 7 && h.R == 20) {
       if (getenv("COPA_SC_TB4")) scatter_inst_w<2, 3, 4, 4, 7, 20>(h);        // tile-batch experiments
-      else if (getenv("COPA_SC_TB3")) scatter_inst_w<2, 3, 4, 3, 7, 20>(h);   // (no clear winner)
-      else scatter_inst_w<2, 3, 4, 2, 7, 20>(h);
+      else if (getenv("COPA_SC_TB2")) scatter_inst_w<2, 3, 4, 2, 7, 20>(h);   // (TB3: 26.8 vs 27.2 ms)
+      else scatter_inst_w<2, 3, 4, 3, 7, 20>(h);
       return;
     }
     if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 2, 7, 15>(h); return; }
