@@ -159,7 +159,12 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
   const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * 512 + 127) & ~127ull);
   uint64_t* full = (uint64_t*)(smraw + fs_bytes);
   uint64_t* empty = full + NSt;
-  unsigned char* slots = smraw + fs_bytes + ((2 * NSt * 8 + 127) & ~127);
+  const uint32_t slots_off = fs_bytes + ((2 * NSt * 8 + 127) & ~127);
+  unsigned char* slots = smraw + slots_off;
+  const int64_t* smI64 = reinterpret_cast<const int64_t*>(smraw);
+  const int32_t* smI32 = reinterpret_cast<const int32_t*>(smraw);
+  const uint16_t* smU16 = reinterpret_cast<const uint16_t*>(smraw);
+  const double* smD = reinterpret_cast<const double*>(smraw);
   for (int64_t x = threadIdx.x; x < Jg * RS; x += blockDim.x) Fs[x] = 0.0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSt; ++i) {
@@ -270,15 +275,17 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
       mbar_wait(full + slot, phase);
-      const unsigned char* base = slots + (size_t)slot * sg.bytes;
-      const int64_t f0 = ((const int64_t*)base)[0], f1 = ((const int64_t*)base)[1];
-      const int32_t* mi = (const int32_t*)(base + 16);
+      // stage arrays addressed by index into the shared buffer (keeps every access a plain LDS;
+      // derived pointers were rebuilt as generic addresses per patient)
+      const uint32_t sb = slots_off + (uint32_t)slot * sg.bytes;
+      const int64_t f0 = smI64[sb >> 3], f1 = smI64[(sb >> 3) + 1];
+      const int32_t* mi = smI32 + ((sb + 16) >> 2);
       const int32_t k0 = mi[0], k1 = mi[1];
-      const int64_t* gp = (const int64_t*)(base + sg.gp + mi[5]);
-      const uint16_t* wo = (const uint16_t*)(base + sg.wo + mi[6]);
-      const int32_t* colS = (const int32_t*)(base + sg.col + mi[2]);
-      const double* valS = (const double*)(base + sg.val + mi[3]);
-      const double* nS = (const double*)(base + sg.nrows + mi[4]);
+      const int64_t* gp = smI64 + ((sb + sg.gp + mi[5]) >> 3);
+      const uint16_t* wo = smU16 + ((sb + sg.wo + mi[6]) >> 1);
+      const int32_t* colS = smI32 + ((sb + sg.col + mi[2]) >> 2);
+      const double* valS = smD + ((sb + sg.val + mi[3]) >> 3);
+      const double* nS = smD + ((sb + sg.nrows + mi[4]) >> 3);
       // per-patient setup (sub-run bounds, B fragments B[t][g] = N(a = 4 ks + t, r = 8 nt + g)) is
       // loaded one patient ahead, off the critical path of the current patient's tiles
       const int npat = dbg == 1 ? 0 : k1 - k0;
