@@ -512,7 +512,8 @@ void plan_scatter(Handle& h) {
   h.Jl = (int64_t)h.sc_G * h.sc_Jg;
   int bps = h.sc_ok ? (int)((228 * 1024) / (h.sc_smem + 1024)) : 1;
   if (bps < 1) bps = 1;
-  int64_t ranges = (148 * (int64_t)bps + h.sc_G - 1) / h.sc_G;
+  const int waves = getenv("COPA_SC_WAVES") ? std::max(1, atoi(getenv("COPA_SC_WAVES"))) : 1;
+  int64_t ranges = (148 * (int64_t)bps * waves + h.sc_G - 1) / h.sc_G;
   if (ranges > h.K) ranges = h.K > 0 ? h.K : 1;
   h.sc_ranges = (int)ranges;
 }
