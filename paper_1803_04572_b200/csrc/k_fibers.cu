@@ -148,10 +148,13 @@ __host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
 }
 
 constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
+
 constexpr int kPfFibers = 4096;   // pass-B L2 prefetch distance (fibers) ahead of the ring
 constexpr int kPfPatients = 64;   // and patients (N rows)
 
-template <int KS, int NT, int W, int TB, int LT, int RT>
+// PRED: predicated F_V row updates (invalid lanes issue no shared-memory access; measured slower,
+// opt-in COPA_SC_PRED); default: invalid lanes are redirected to a per-lane scratch slot.
+template <int KS, int NT, int W, int TB, int LT, int RT, bool PRED = false>
 __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
@@ -358,8 +361,13 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const bool ok = col[b] >= 0 && 8 * nt + 2 * t < R;
-              idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
-              v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
+              if (PRED) {  // predicated: invalid lanes issue no shared-memory wavefront
+                idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : -1;
+                v[b][nt] = ok ? *reinterpret_cast<const double2*>(Fs + idx[b][nt]) : make_double2(0.0, 0.0);
+              } else {
+                idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
+                v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
+              }
             }
 #pragma unroll
           for (int b = 0; b < NB; ++b)
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             for (int nt = 0; nt < NT; ++nt) {
               v[b][nt].x += cc[b][nt][0];
               v[b][nt].y += cc[b][nt][1];
-              *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
+              if (!PRED || idx[b][nt] >= 0) *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
             }
         };
         int tb = lo;
@@ -404,9 +412,9 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0>
+template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0, bool PRED = false>
 static void scatter_inst_w(Handle& h) {
-  auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT>;
+  auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT, PRED>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -435,6 +443,7 @@ static void scatter_dispatch_n(Handle& h) {
     if (KS == 2 && h.l == 7 && h.R == 20) {
       if (getenv("COPA_SC_TB4")) scatter_inst_w<2, 3, 4, 4, 7, 20>(h);        // tile-batch experiments
       else if (getenv("COPA_SC_TB2")) scatter_inst_w<2, 3, 4, 2, 7, 20>(h);   // (TB3: 26.8 vs 27.2 ms)
+      else if (getenv("COPA_SC_PRED")) scatter_inst_w<2, 3, 4, 3, 7, 20, true>(h);  // 26.6-27.1 vs 24.4 ms
       else scatter_inst_w<2, 3, 4, 3, 7, 20>(h);
       return;
     }
