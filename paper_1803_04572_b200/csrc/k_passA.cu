@@ -169,6 +169,10 @@ __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restric
   // patient segment are masked to zero in the A operand at MMA time; rows a >= l and columns r >= R
   // only feed accumulator entries that are never written (labels are always valid: the slack of
   // fa_col is zeroed and V̄ rows are padded).
+  // the lane's k index t kept in a register (opaque to the compiler): otherwise it is rebuilt from
+  // SR_TID.X right before the masked MMAs of every patient boundary (S2R latency on the MMA path)
+  int tk;
+  asm volatile("mov.b32 %0, %1;" : "=r"(tk) : "r"(t));
   for (int c = 0; c < nchi; ++c) {
     mb_wait(bars + (c & (kANS - 1)), (uint32_t)((c / kANS) & 1));
     const unsigned char* buf = ring + (c & (kANS - 1)) * cb;
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restric
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         if (j >= j0 && j < j1) {
-          const int fl = 4 * j + t;
+          const int fl = 4 * j + tk;
           const bool in = fl >= lo && fl < hi;
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt)
