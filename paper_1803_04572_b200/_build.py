@@ -1,7 +1,8 @@
 """Build libcopa.so in-tree with nvcc for sm_100a (no JIT cache: the .so travels with the repo).
 
-Each .cu is compiled to an object in parallel (``--split-compile`` also parallelises the optimiser
-inside the heavily templated k_dense.cu), then linked into one shared library.
+Each .cu is compiled to an object in parallel, then linked into one shared library. No
+``--split-compile``: its output depends on the thread count (the split points move), and some
+splits produced measurably worse code (pass A 13.2 vs 11.0 ms at Scale with 8 threads).
 """
 from __future__ import annotations
 
@@ -34,7 +35,7 @@ def needs_build() -> bool:
 
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    cmd = [NVCC] + FLAGS + ["--split-compile=0", "-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
+    cmd = [NVCC] + FLAGS + ["-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)

@@ -19,8 +19,17 @@ void polar_wide_L7(Handle& h);
 void polar_wide_L8(Handle& h);
 void polar_wide_L9(Handle& h);
 void polar_wide_L12(Handle& h);
-void passB_wide_M1(Handle& h);
-void passB_wide_M2(Handle& h);
+bool passB_wide_special(Handle& h);
+void passB_wide_g1(Handle& h, int nt);
+void passB_wide_g2a(Handle& h);
+void passB_wide_g2b(Handle& h);
+void passB_wide_g2c(Handle& h);
+void passB_wide_g2d(Handle& h);
+void passB_wide_g3(Handle& h, int nt);
+void passB_wide_g4a(Handle& h);
+void passB_wide_g4b(Handle& h);
+void passB_wide_g4c(Handle& h);
+void passB_wide_g4d(Handle& h);
 
 bool polar_wide_ok(const Handle& h) { return h.smooth && h.l < h.R && h.l <= 12; }
 
@@ -35,8 +44,13 @@ int launch_polar_wide(Handle& h) {
 }
 
 int launch_passB_wide(Handle& h) {
-  if (h.l <= 8) passB_wide_M1(h);
-  else passB_wide_M2(h);
+  if (!passB_wide_special(h)) {
+    const int nt = (h.R + 7) / 8 < 8 ? (h.R + 7) / 8 : 8;
+    static void (*const big[2][4])(Handle&) = {{passB_wide_g2a, passB_wide_g2b, passB_wide_g2c, passB_wide_g2d},
+                                               {passB_wide_g4a, passB_wide_g4b, passB_wide_g4c, passB_wide_g4d}};
+    if (nt <= 4) (h.l <= 8 ? passB_wide_g1 : passB_wide_g3)(h, nt);
+    else big[h.l <= 8 ? 0 : 1][nt - 5](h);
+  }
   return 2;
 }
 

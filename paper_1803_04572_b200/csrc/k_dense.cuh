@@ -890,20 +890,13 @@ static void passB_wide_inst(Handle& h) {
   k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
 }
 
-template <int MT>
-static void passB_wide_n(Handle& h) {
-  if (MT == 1 && h.l == 7 && h.R == 20) { passB_wide_inst<1, 3, 20, 7>(h); return; }
-  if (MT == 1 && h.l == 7 && h.R == 15) { passB_wide_inst<1, 2, 15, 7>(h); return; }
-  if (MT == 2 && h.l == 9 && h.R == 40) { passB_wide_inst<2, 5, 40, 9>(h); return; }
-  switch ((h.R + 7) / 8) {
-    case 1: passB_wide_inst<MT, 1>(h); break;
-    case 2: passB_wide_inst<MT, 2>(h); break;
-    case 3: passB_wide_inst<MT, 3>(h); break;
-    case 4: passB_wide_inst<MT, 4>(h); break;
-    case 5: passB_wide_inst<MT, 5>(h); break;
-    case 6: passB_wide_inst<MT, 6>(h); break;
-    case 7: passB_wide_inst<MT, 7>(h); break;
-    default: passB_wide_inst<MT, 8>(h); break;
+// Generic NT instantiations of the W pass, grouped so the object files compile in parallel
+// (k_passB_g*.cu); the configured (R, l) shapes are in k_passB_s.cu.
+template <int MT, int NT0, int NT1>
+static void passB_wide_group(Handle& h, int nt) {
+  if constexpr (NT0 <= NT1) {
+    if (nt == NT0) { passB_wide_inst<MT, NT0>(h); return; }
+    passB_wide_group<MT, NT0 + 1, NT1>(h, nt);
   }
 }
 

@@ -8,11 +8,11 @@ pids=()
 for src in csrc/*.cu; do
   f=$(basename $src .cu); o=build/$f.cu.o
   dense=0
-  case $f in k_polar_l*|k_passB_m*|k_init) [ csrc/k_dense.cuh -nt $o ] && dense=1 ;; esac
+  case $f in k_polar_l*|k_passB_*|k_init) [ csrc/k_dense.cuh -nt $o ] && dense=1 ;; esac
   if [ ! -f $o ] || [ $src -nt $o ] || [ csrc/copa_internal.cuh -nt $o ] || [ ../include/copa.h -nt $o ] || [ $dense = 1 ]; then
     echo "compiling $f"
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC \
-      -I ../include --split-compile=0 -c $src -o $o &
+      -I ../include -c $src -o $o &
     pids+=($!)
   fi
 done
