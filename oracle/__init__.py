@@ -39,7 +39,8 @@ class _Options(ctypes.Structure):
     _fields_ = [("kind_H", ctypes.c_int32), ("kind_W", ctypes.c_int32), ("kind_V", ctypes.c_int32),
                 ("param_H", ctypes.c_double), ("param_W", ctypes.c_double), ("param_V", ctypes.c_double),
                 ("smooth_l", ctypes.c_int32), ("smooth_d", ctypes.c_int32), ("rho", ctypes.c_double),
-                ("n_inner", ctypes.c_int32), ("tau_polar", ctypes.c_double), ("tau_basis", ctypes.c_double)]
+                ("n_inner", ctypes.c_int32), ("tau_polar", ctypes.c_double), ("tau_basis", ctypes.c_double),
+                ("admm_tol", ctypes.c_double)]
 
 
 _lib = None
@@ -60,6 +61,9 @@ def lib():
         L.oracle_chol_solve.argtypes = [i32, _vp, _vp]
         L.oracle_admm_mode.argtypes = [i64, i32, _vp, _vp, d, i32, i32, d, _vp, _vp, _vp]
         L.oracle_admm_mode.restype = ctypes.c_int
+        L.oracle_admm_mode_tol.argtypes = [i64, i32, _vp, _vp, d, i32, i32, d, d, _vp, _vp, _vp, _vp]
+        L.oracle_admm_mode_tol.restype = ctypes.c_int
+        L.oracle_sparsity.argtypes = [i64, _vp]; L.oracle_sparsity.restype = d
         L.oracle_patient_basis.argtypes = [_vp, i64, i32, i32, d, _vp]; L.oracle_patient_basis.restype = ctypes.c_int
         P, O = ctypes.POINTER(_Problem), ctypes.POINTER(_Options)
         L.oracle_init.argtypes = [P, O, _vp, _vp, _vp, _vp]; L.oracle_init.restype = ctypes.c_int
@@ -71,8 +75,6 @@ def lib():
         L.oracle_mttkrp.restype = ctypes.c_int
         L.oracle_residual.argtypes = [P, O, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.oracle_residual.restype = d
-        L.oracle_patient_procrustes.argtypes = [P, O, i64, _vp, i32, _vp, _vp, _vp, _vp, _vp]
-        L.oracle_patient_procrustes.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -141,24 +143,33 @@ def chol_solve(L, b):
     return x
 
 
-def admm_mode(F, G, Zbar, D, kind, param, rho=0.0, n_inner=5):
-    """One mode's cached-Cholesky ADMM (Alg.1 l.13-l.19). Returns (Zbar, D, rho)."""
+def admm_mode(F, G, Zbar, D, kind, param, rho=0.0, n_inner=5, tol=0.0, steps=None):
+    """One mode's cached-Cholesky ADMM (Alg.1 l.13-l.19). Returns (Zbar, D, rho).
+    tol > 0: per-row inner stop (reading R-inner-tol); steps (int32 array of n rows) receives each
+    row's step count."""
     F = _f64(F); G = _f64(G)
     Zb = _f64(Zbar).copy(); Dd = _f64(D).copy()
     rho_out = ctypes.c_double(0)
-    rc = lib().oracle_admm_mode(F.shape[0], F.shape[1], _p(F), _p(G), rho, n_inner, kind, param, _p(Zb), _p(Dd),
-                                ctypes.byref(rho_out))
+    rc = lib().oracle_admm_mode_tol(F.shape[0], F.shape[1], _p(F), _p(G), rho, n_inner, kind, param, tol, _p(Zb),
+                                    _p(Dd), ctypes.byref(rho_out), None if steps is None else _p(steps))
     if rc:
         raise RuntimeError(f"oracle_admm_mode failed: {rc}")
     return Zb, Dd, rho_out.value
 
 
 # ------------------------------------------------------------------ full iteration
-def options_from_config(cfg, tau_polar=TAU_POLAR, tau_basis=TAU_BASIS, n_inner=None, rho=None):
+def options_from_config(cfg, tau_polar=TAU_POLAR, tau_basis=TAU_BASIS, n_inner=None, rho=None, admm_tol=0.0):
     return _Options(kind_H=cfg.con_H[0], kind_W=cfg.con_W[0], kind_V=cfg.con_V[0],
                     param_H=cfg.con_H[1], param_W=cfg.con_W[1], param_V=cfg.con_V[1],
                     smooth_l=cfg.smooth_l, smooth_d=SPLINE_DEGREE, rho=cfg.rho if rho is None else rho,
-                    n_inner=cfg.n_inner if n_inner is None else n_inner, tau_polar=tau_polar, tau_basis=tau_basis)
+                    n_inner=cfg.n_inner if n_inner is None else n_inner, tau_polar=tau_polar, tau_basis=tau_basis,
+                    admm_tol=admm_tol)
+
+
+def sparsity(V) -> float:
+    """SPARSITY(V) = number of zero elements / size."""
+    V = _f64(V)
+    return lib().oracle_sparsity(V.size, _p(V))
 
 
 class Oracle:
@@ -194,7 +205,8 @@ class Oracle:
         self.Q = np.zeros((int(self.m_off[-1]), R))
         self.rank = np.zeros(K, np.int32)
         self.fits = []
-        self.diag = np.zeros(5)
+        self.inner_steps = []
+        self.diag = np.zeros(8)
 
     def iterate(self, n=1):
         for _ in range(n):
@@ -205,7 +217,23 @@ class Oracle:
             if rc:
                 raise RuntimeError(f"oracle_iterate failed: {rc}")
             self.fits.append(fit.value)
+            self.inner_steps.append(tuple(int(x) for x in self.diag[5:8]))
         return self.fits
+
+    def iterate_until(self, max_outer, outer_tol):
+        """Outer loop with a stop ("while convergence criterion is not met", reading
+        R-outer-tol): after iteration t >= 2, stop when |FIT_t - FIT_{t-1}| < outer_tol * max(|FIT_{t-1}|, 1),
+        or after max_outer iterations. Returns the FIT values of this call."""
+        out = []
+        for _ in range(max_outer):
+            f = self.iterate(1)[-1]
+            out.append(f)
+            if len(out) >= 2 and abs(out[-1] - out[-2]) < outer_tol * max(abs(out[-2]), 1.0):
+                break
+        return out
+
+    def sparsity_V(self):
+        return sparsity(self.V)
 
     def procrustes(self, H=None, V=None, W=None):
         """l.3-l.8 only, on the given (default: current) factors; fills self.Q, self.rank."""

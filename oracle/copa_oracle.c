@@ -48,6 +48,7 @@ typedef struct {
   int32_t n_inner;
   double tau_polar;  /* rank cut of A_k: sigma > tau_polar * sigma_1 */
   double tau_basis;  /* rank cut of M_k */
+  double admm_tol;   /* > 0: per-row inner stop (reading R-inner-tol); 0: exactly n_inner steps */
 } or_options;
 
 /* ---------------------------------------------------------------- prox */
@@ -231,11 +232,18 @@ void oracle_chol_solve(int32_t R, const double* L, double* x) {
 
 /* ------------------------------------------------------------- ADMM (l.10-l.19) */
 /* One mode: given F (n x R), G (R x R), the auxiliary Zbar and dual D (n x R, updated in
- * place), run rho, chol, and n_inner steps of
+ * place), run rho, chol, and up to n_inner steps of
  *   Z = (F + rho (Zbar + D)) (G + rho I)^-1 ; Zbar = prox(Z - D) ; D = D + Zbar - Z.
+ * The least-squares step acts on each row separately and the prox is element-wise, so the rows
+ * are independent ADMM problems sharing G. Inner stop ("while convergence
+ * criterion is not met", reading R-inner-tol): tol = 0 runs exactly n_inner steps; tol > 0 stops
+ * a row after the step where max(||Zbar - Z||, ||Zbar - Zbar_prev||) <= tol ||Zbar|| (primal
+ * residual and change of the auxiliary row, Euclidean norms, compared squared), at most n_inner.
+ * steps (may be NULL) receives the number of steps of each row.
  * Returns OR_OK / error; rho_out receives the step size used. */
-int oracle_admm_mode(int64_t n, int32_t R, const double* F, const double* G, double rho_fixed, int32_t n_inner,
-                     int32_t kind, double param, double* Zbar, double* D, double* rho_out) {
+int oracle_admm_mode_tol(int64_t n, int32_t R, const double* F, const double* G, double rho_fixed, int32_t n_inner,
+                         int32_t kind, double param, double tol, double* Zbar, double* D, double* rho_out,
+                         int32_t* steps) {
   double rho = rho_fixed;
   if (!(rho > 0)) {
     double tr = 0;
@@ -249,19 +257,40 @@ int oracle_admm_mode(int64_t n, int32_t R, const double* F, const double* G, dou
   for (int i = 0; i < R; ++i) L[i * R + i] += rho;
   if (oracle_cholesky(R, L)) { free(L); return OR_E_CHOL; }
   double* z = (double*)malloc(sizeof(double) * (size_t)R);
-  for (int it = 0; it < n_inner; ++it) {
-    for (int64_t row = 0; row < n; ++row) {
+  for (int64_t row = 0; row < n; ++row) {
+    int it = 0;
+    while (it < n_inner) {
       for (int r = 0; r < R; ++r) z[r] = F[row * R + r] + rho * (Zbar[row * R + r] + D[row * R + r]);
       oracle_chol_solve(R, L, z);
+      double pr = 0, du = 0, nz = 0;
       for (int r = 0; r < R; ++r) {
         double zb = oracle_prox(kind, param, rho, z[r] - D[row * R + r]);
+        double dz = zb - Zbar[row * R + r];
         Zbar[row * R + r] = zb;
         D[row * R + r] += zb - z[r];
+        pr += (zb - z[r]) * (zb - z[r]);
+        du += dz * dz;
+        nz += zb * zb;
       }
+      ++it;
+      if (tol > 0 && (pr > du ? pr : du) <= tol * tol * nz) break;
     }
+    if (steps) steps[row] = it;
   }
   free(z); free(L);
   return OR_OK;
+}
+
+int oracle_admm_mode(int64_t n, int32_t R, const double* F, const double* G, double rho_fixed, int32_t n_inner,
+                     int32_t kind, double param, double* Zbar, double* D, double* rho_out) {
+  return oracle_admm_mode_tol(n, R, F, G, rho_fixed, n_inner, kind, param, 0.0, Zbar, D, rho_out, NULL);
+}
+
+/* SPARSITY(V) = nz(V) / size(V), nz = number of zero elements. */
+double oracle_sparsity(int64_t n, const double* V) {
+  int64_t z = 0;
+  for (int64_t i = 0; i < n; ++i) z += V[i] == 0.0;
+  return n > 0 ? (double)z / (double)n : 0.0;
 }
 
 /* ----------------------------------------------------------- per-patient pieces */
@@ -480,7 +509,8 @@ double oracle_residual(const or_problem* P, const or_options* o, const double* C
 
 /* One outer iteration of Alg.1 (l.3-l.20) + FIT. Factors are the auxiliary (working)
  * variables H, V, W (reading R-aux); D* are the scaled duals; mode order H, W, V with
- * fresh factors (reading R-order). diag (may be NULL) receives rho_H, rho_W, rho_V, E, normX. */
+ * fresh factors (reading R-order). diag (may be NULL, else 8 doubles) receives rho_H, rho_W, rho_V, E,
+ * normX and the inner ADMM steps of the H, W, V modes summed over rows. */
 int oracle_iterate(const or_problem* P, const or_options* o, const double* C, const int32_t* m, const int64_t* m_off,
                    double normX, double* H, double* V, double* W, double* DH, double* DV, double* DW, double* Qt,
                    int32_t* rank, double* fit_out, double* diag) {
@@ -492,62 +522,48 @@ int oracle_iterate(const or_problem* P, const or_options* o, const double* C, co
   double* G2 = (double*)malloc(sizeof(double) * (size_t)R * R);
   double rho_used[3] = {0, 0, 0};
   double E = 0;
+  int32_t* steps_H = (int32_t*)calloc((size_t)R, sizeof(int32_t));
+  int32_t* steps_W = (int32_t*)calloc((size_t)(K > 0 ? K : 1), sizeof(int32_t));
+  int32_t* steps_V = (int32_t*)calloc((size_t)J, sizeof(int32_t));
   int status = oracle_procrustes_all(P, o, C, m, m_off, H, V, W, Qt, rank);
   /* n = 1 (H): G = (V^T V) * (W^T W) (l.11), F_H (l.12), ADMM (l.13-19) */
   if (status == OR_OK) {
     oracle_mttkrp(P, o, C, m, m_off, Qt, H, V, W, 1, F);
     gram(J, R, V, G1); gram(K, R, W, G2);
     for (int i = 0; i < R * R; ++i) G[i] = G1[i] * G2[i];
-    status = oracle_admm_mode(R, R, F, G, o->rho, o->n_inner, o->kind_H, o->param_H, H, DH, &rho_used[0]);
+    status = oracle_admm_mode_tol(R, R, F, G, o->rho, o->n_inner, o->kind_H, o->param_H, o->admm_tol, H, DH,
+                                  &rho_used[0], steps_H);
   }
   /* n = 2 (W): with the updated H; G = (H^T H) * (V^T V) */
   if (status == OR_OK) {
     oracle_mttkrp(P, o, C, m, m_off, Qt, H, V, W, 3, F);
     gram(R, R, H, G1); gram(J, R, V, G2);
     for (int i = 0; i < R * R; ++i) G[i] = G1[i] * G2[i];
-    status = oracle_admm_mode(K, R, F, G, o->rho, o->n_inner, o->kind_W, o->param_W, W, DW, &rho_used[1]);
+    status = oracle_admm_mode_tol(K, R, F, G, o->rho, o->n_inner, o->kind_W, o->param_W, o->admm_tol, W, DW,
+                                  &rho_used[1], steps_W);
   }
   /* n = 3 (V): with the updated H and W; G = (H^T H) * (W^T W) */
   if (status == OR_OK) {
     oracle_mttkrp(P, o, C, m, m_off, Qt, H, V, W, 2, F);
     gram(R, R, H, G1); gram(K, R, W, G2);
     for (int i = 0; i < R * R; ++i) G[i] = G1[i] * G2[i];
-    status = oracle_admm_mode(J, R, F, G, o->rho, o->n_inner, o->kind_V, o->param_V, V, DV, &rho_used[2]);
+    status = oracle_admm_mode_tol(J, R, F, G, o->rho, o->n_inner, o->kind_V, o->param_V, o->admm_tol, V, DV,
+                                  &rho_used[2], steps_V);
   }
   if (status == OR_OK) {
     E = oracle_residual(P, o, C, m, m_off, Qt, H, V, W);
     *fit_out = 1.0 - E / normX;
     if (!isfinite(*fit_out)) status = OR_E_NONFINITE;
   }
-  if (diag) { diag[0] = rho_used[0]; diag[1] = rho_used[1]; diag[2] = rho_used[2]; diag[3] = E; diag[4] = normX; }
+  if (diag) {
+    int64_t tH = 0, tW = 0, tV = 0;
+    for (int i = 0; i < R; ++i) tH += steps_H[i];
+    for (int64_t i = 0; i < K; ++i) tW += steps_W[i];
+    for (int64_t i = 0; i < J; ++i) tV += steps_V[i];
+    diag[0] = rho_used[0]; diag[1] = rho_used[1]; diag[2] = rho_used[2]; diag[3] = E; diag[4] = normX;
+    diag[5] = (double)tH; diag[6] = (double)tW; diag[7] = (double)tV; /* inner steps summed over rows */
+  }
+  free(steps_H); free(steps_W); free(steps_V);
   free(F); free(G); free(G1); free(G2);
   return status;
-}
-
-/* Debug/parity helper: the three MTTKRPs and intermediates of the first half of an
- * iteration without updating anything (used by the sampled-output GPU tests). */
-int oracle_patient_procrustes(const or_problem* P, const or_options* o, int64_t k, const double* Ck, int32_t mk,
-                              const double* H, const double* V, const double* wk, double* Pp, double* Qk) {
-  const int32_t R = P->R;
-  int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * (size_t)P->J);
-  int32_t* cols = (int32_t*)malloc(sizeof(int32_t) * (size_t)P->J);
-  for (int64_t j = 0; j < P->J; ++j) mark[j] = -1;
-  double* Xp;
-  int64_t nc = patient_dense(P, k, Ck, o->smooth_l, mk, mark, cols, &Xp);
-  double* A = (double*)malloc(sizeof(double) * (size_t)(mk * R + 1));
-  for (int a = 0; a < mk; ++a)
-    for (int r = 0; r < R; ++r) {
-      double acc = 0;
-      for (int64_t jl = 0; jl < nc; ++jl) acc += Xp[a * nc + jl] * V[(int64_t)cols[jl] * R + r];
-      Pp[a * R + r] = acc;
-    }
-  for (int a = 0; a < mk; ++a)
-    for (int s = 0; s < R; ++s) {
-      double acc = 0;
-      for (int r = 0; r < R; ++r) acc += Pp[a * R + r] * wk[r] * H[s * R + r];
-      A[a * R + s] = acc;
-    }
-  int rk = oracle_polar(mk, R, A, o->tau_polar, Qk);
-  free(A); free(Xp); free(mark); free(cols);
-  return rk;
 }

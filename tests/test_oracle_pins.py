@@ -380,3 +380,164 @@ def test_p18_deterministic():
     a = oracle.Oracle(p); b = oracle.Oracle(p)
     fa = a.iterate(2); fb = b.iterate(2)
     assert fa == fb and np.array_equal(a.V, b.V) and np.array_equal(a.Q, b.Q)
+
+
+# ------------------------------------------------------------------- P19 mode order and freshness (Alg.1 l.9-l.20)
+def _y_tensor(o, p):
+    """Y(:, :, k) = Q_k^T X'_k (Alg.1 l.6) from dense slices and the oracle's stored Q."""
+    Xs = dense_slices(p)
+    Y = np.zeros((o.R, p.J, p.K))
+    for k in range(p.K):
+        Xp = Xs[k] if o.C is None else o.C[p.patient_row_ptr[k]:p.patient_row_ptr[k + 1], :o.m[k]].T @ Xs[k]
+        Y[:, :, k] = o.Qk(k).T @ Xp
+    return Y
+
+
+@pytest.mark.parametrize("name", ["tiny", "medium"])
+def test_p19_mode_order_and_freshness(name):
+    """Alg.1 l.9-l.20 (reading R-order): modes are updated H -> W -> V, the W
+    update uses the NEW H, the V update the new H and W (Gauss-Seidel, not Jacobi block order).
+
+    With no constraint and many inner steps the ADMM of each mode converges to the normal-equation
+    solution F G^-1 (pin P11), so after one outer iteration, from numpy (dense Y, naive Khatri-Rao):
+      H1 = Y_(1)(W0 ⊙ V0) [(V0^T V0) * (W0^T W0)]^-1
+      W1 = Y_(3)(V0 ⊙ H1) [(H1^T H1) * (V0^T V0)]^-1
+      V1 = Y_(2)(W1 ⊙ H1) [(H1^T H1) * (W1^T W1)]^-1
+    A stale factor in any mode (e.g. V from the old W) changes the result at O(1)."""
+    cfg = dataclasses.replace(synthgen.CONFIGS[name], con_H=(NONE, 0.0), con_W=(NONE, 0.0), con_V=(NONE, 0.0))
+    p = synthgen.generate(cfg, K=30)
+    o = oracle.Oracle(p, opts=oracle.options_from_config(cfg, n_inner=3000))
+    H0, V0, W0 = o.H.copy(), o.V.copy(), o.W.copy()
+    o.iterate(1)
+    Y = _y_tensor(o, p)  # Q from the Procrustes step on (H0, V0, W0)
+    R, J, K = o.R, p.J, p.K
+    Y1 = Y.reshape(R, J * K, order="F")
+    Y2 = np.moveaxis(Y, 1, 0).reshape(J, R * K, order="F")
+    Y3 = np.moveaxis(Y, 2, 0).reshape(K, R * J, order="F")
+    H1 = np.linalg.solve(((V0.T @ V0) * (W0.T @ W0)).T, (Y1 @ _naive_kr(W0, V0)).T).T
+    W1 = np.linalg.solve(((H1.T @ H1) * (V0.T @ V0)).T, (Y3 @ _naive_kr(V0, H1)).T).T
+    V1 = np.linalg.solve(((H1.T @ H1) * (W1.T @ W1)).T, (Y2 @ _naive_kr(W1, H1)).T).T
+    for got, ref, what in ((o.H, H1, "H"), (o.W, W1, "W"), (o.V, V1, "V")):
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err <= 1e-8, (what, err)
+    # the stale (Jacobi-order) alternatives are far away: the pin can tell them apart
+    W_stale = np.linalg.solve(((H0.T @ H0) * (V0.T @ V0)).T, (Y3 @ _naive_kr(V0, H0)).T).T
+    V_stale = np.linalg.solve(((H1.T @ H1) * (W0.T @ W0)).T, (Y2 @ _naive_kr(W0, H1)).T).T
+    assert np.linalg.norm(W_stale - W1) > 1e-3 * np.linalg.norm(W1)
+    assert np.linalg.norm(V_stale - V1) > 1e-3 * np.linalg.norm(V1)
+
+
+# ------------------------------------------------------------------- golden fixtures (tests/golden/, each cited)
+def _golden(name):
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", name)
+    rows = []
+    for line in open(path):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        rows.append([part.split() for part in line.split("|")])
+    return rows
+
+
+def test_golden_prox_examples():
+    kinds = {"none": NONE, "nonneg": NONNEG, "l1": L1, "nonneg_l1": NONNEG_L1, "l0": L0}
+    for (kind, param, rho), xs, ys in _golden("prox_examples.txt"):
+        got = oracle.prox(kinds[kind], float(param), float(rho), [float(x) for x in xs])
+        assert np.allclose(got, [float(y) for y in ys], rtol=0, atol=1e-15), (kind, got, ys)
+
+
+def test_golden_bspline_examples():
+    for (l, d), ts, ms in _golden("bspline_examples.txt"):
+        l, d = int(l), int(d)
+        M = oracle.bspline_matrix([float(t) for t in ts], l, d=d)
+        assert np.allclose(M.ravel(), [float(x) for x in ms], rtol=0, atol=1e-15), (l, d, M)
+
+
+def test_golden_sparsity_examples():
+    for (r, c), vals, (want,) in _golden("sparsity_examples.txt"):
+        V = np.array([float(v) for v in vals]).reshape(int(r), int(c))
+        assert oracle.sparsity(V) == float(want)
+
+
+# ------------------------------------------------------------------- P20 inner / outer stops (N3; P:280, P:294)
+def test_p20_inner_stop_identity_prox_closed_form():
+    """Reading R-inner-tol: with the identity prox D stays 0 and each row follows the closed form of
+    P10, Zbar_n = F G^-1 + (Zbar_0 - F G^-1) T^n with T = rho (G + rho I)^-1. The per-row stop after
+    step n is ||Zbar_n - Zbar_{n-1}|| <= tol ||Zbar_n||, so the step count of every row and its final
+    value follow from the closed form alone."""
+    rng = np.random.default_rng(21)
+    R, n, tol, cap = 6, 40, 1e-3, 60
+    M = rng.standard_normal((20, R)); G = M.T @ M
+    F = rng.standard_normal((n, R)) * rng.uniform(0.1, 10, size=(n, 1))
+    Z0 = rng.standard_normal((n, R))
+    rho = np.trace(G) / R
+    X = F @ np.linalg.inv(G)
+    T = rho * np.linalg.inv(G + rho * np.eye(R))
+    steps = np.zeros(n, np.int32)
+    Zb, D, _ = oracle.admm_mode(F, G, Z0, np.zeros((n, R)), NONE, 0.0, rho=0.0, n_inner=cap, tol=tol, steps=steps)
+    checked = 0
+    for i in range(n):
+        prev = Z0[i]
+        want = cap
+        margin_ok = True
+        for s in range(1, cap + 1):
+            cur = X[i] + (Z0[i] - X[i]) @ np.linalg.matrix_power(T, s)
+            ratio = np.linalg.norm(cur - prev) / np.linalg.norm(cur)
+            if abs(ratio - tol) < 1e-6 * tol:
+                margin_ok = False  # too close to the threshold for a rounding-independent decision
+            if ratio <= tol:
+                want = s
+                break
+            prev = cur
+        if not margin_ok:
+            continue
+        checked += 1
+        assert steps[i] == want, (i, steps[i], want)
+        ref = X[i] + (Z0[i] - X[i]) @ np.linalg.matrix_power(T, want)
+        assert np.allclose(Zb[i], ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
+    assert checked >= n - 2 and len(set(steps.tolist())) > 3  # rows stop at different steps
+    assert not D.any()
+
+
+def test_p20_inner_stop_is_truncation():
+    """A row that stops after s steps holds exactly what the fixed-count ADMM (tol = 0, pinned by
+    P10/P11) gives after s steps — for every prox kind."""
+    rng = np.random.default_rng(22)
+    R, n = 5, 25
+    M = rng.standard_normal((15, R)); G = M.T @ M
+    F = rng.standard_normal((n, R)) * 3
+    Z0 = rng.uniform(size=(n, R))
+    for kind, param in ((NONNEG, 0.0), (L1, 0.5), (NONNEG_L1, 0.2), (L0, 0.05)):
+        steps = np.zeros(n, np.int32)
+        Zt, Dt, _ = oracle.admm_mode(F, G, Z0, np.zeros((n, R)), kind, param, rho=0.0, n_inner=50, tol=1e-4,
+                                     steps=steps)
+        assert steps.min() >= 1 and steps.max() <= 50
+        for i in range(n):
+            Zf, Df, _ = oracle.admm_mode(F[i:i + 1], G, Z0[i:i + 1], np.zeros((1, R)), kind, param, rho=0.0,
+                                         n_inner=int(steps[i]))
+            assert np.array_equal(Zf[0], Zt[i]) and np.array_equal(Df[0], Dt[i]), (kind, i)
+
+
+def test_p20_outer_stop_matches_fixed_trajectory():
+    """Reading R-outer-tol: iterate_until stops at the first t >= 2 with
+    |FIT_t - FIT_{t-1}| < tol max(|FIT_{t-1}|, 1); the FIT values are those of the fixed-count run."""
+    p = synthgen.generate("tiny", K=60)
+    a = oracle.Oracle(p); b = oracle.Oracle(p)
+    fa = a.iterate(40)
+    tol = 1e-3
+    fb = b.iterate_until(40, tol)
+    stop = next((t for t in range(1, 40) if abs(fa[t] - fa[t - 1]) < tol * max(abs(fa[t - 1]), 1.0)), 39)
+    assert len(fb) == stop + 1 and fb == fa[:stop + 1]
+    assert len(fb) < 40
+
+
+def test_p20_sparsity_l0_total_threshold():
+    """SPARSITY: l0 with huge mu zeroes V entirely -> 1.0."""
+    rng = np.random.default_rng(23)
+    R, n = 4, 9
+    M = rng.standard_normal((12, R)); G = M.T @ M
+    Z, _, _ = oracle.admm_mode(rng.standard_normal((n, R)), G, np.ones((n, R)), np.zeros((n, R)), L0, 1e12,
+                               rho=0.0, n_inner=2)
+    assert oracle.sparsity(Z) == 1.0
+    assert oracle.sparsity(np.ones((3, 2))) == 0.0
