@@ -30,9 +30,11 @@ sys.path.insert(0, ROOT)
 
 import synthgen  # noqa: E402
 
-# Bounded oracle samples (first n patients of the same workload): ~2-3 s per oracle iteration on
-# one host core.
-ORACLE_SAMPLE = {"tiny": 200, "small": 20000, "medium": 12000, "large": 1500, "scale": 8000}
+METRIC = "COPA outer iteration throughput (nonzeros per second; sec/iteration = ms_per_step/1000)"
+# Patients per host core of the bounded oracle sample: ~2-3 s of one oracle outer iteration per
+# core; the sample is this many patients times the cores used, times SAMPLE_SCALE.
+ORACLE_PER_CORE = {"tiny": 200, "small": 20000, "medium": 12000, "large": 1500, "scale": 8000}
+SAMPLE_SCALE = 4
 FP64_PEAK_TFLOPS = 34.2  # measured DFMA loop on this pool's B200 at 1965 MHz (tools/probe_fp64.cu, profiles/)
 DMMA_PEAK_TFLOPS = 36.9  # measured mma.sync m8n8k4 f64 (SASS DMMA) loop, same box (tools/probe_dmma*.cu)
 FALLBACK_HBM_GBS = 6650.0
@@ -106,32 +108,47 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ roofline
-def phase_model(st: dict, cfg, R: int, K: int, J: int, rows: int, nnz: int, m: np.ndarray):
-    """Algorithmic bytes / flops per launch of each phase (DESIGN.md §5 defines each term)."""
+def phase_model(st: dict, cfg, R: int, K: int, J: int, rows: int, nnz: int, m: np.ndarray, Ik: np.ndarray):
+    """Algorithmic bytes / flops per launch of each phase, from SURVEY.md §8(d):
+
+      B_X   = 12 nnz + 4 sum I_k + 8 (K+1)        CSR bytes (int32 col + f64 val, int32 row ptr, int64 patient ptr)
+      C     = 8 sum_k I_k l'_k                    the basis C_k (smooth), read once per pass
+      U     = 8 R sum_k min(m_k, R)               one pass over the per-patient state (P', Q~ or N)
+      B_iter = 2 B_X + 4 U + 2 C + 5 (8 K R)      the fused two-pass minimum of §8(d)
+
+    assigned per kernel of this build: pass A (spmm) B_X + C + U (P' write) + V; polar 2U + W;
+    W pass 3U + 4 (8KR) (Q~, P' read, N write, W/D_W read+write); pass B (scatter) B_X + C + U (N
+    read) + F_V partial; solves O(JR). The layout's own bytes (projected fibers, padded state rows)
+    are reported beside them as layout_bytes. Flops: §8(d)'s 2 nnz R + 2 R sum I_k l'_k per
+    sparse pass; polar = the QR + Jacobi count of DESIGN.md §4."""
     S, F = st["state_rows"], st["fibers"]
     l = cfg.smooth_l
-    SR8, KR8, JR8 = 8 * S * R, 8 * K * R, 8 * J * R
-    if l > 0:
-        stream = F * (4 + 8 * l) + 8 * (K + 1) + 4 * K + 8 * (K + 1)
-    else:
-        stream = 12 * nnz + 8 * (rows + 1)
     q = np.minimum(m, R).astype(np.float64)
     mm = m.astype(np.float64)
-    # polar flops (lower-bound count): A = P'SH^T, Givens QR of the tall side, one Jacobi sweep
-    # set (5 sweeps assumed), K, and Q~ = AK / KA.
+    BX = 12.0 * nnz + 4.0 * rows + 8.0 * (K + 1)
+    C = 8.0 * float(np.sum(Ik.astype(np.float64) * mm)) if l > 0 else 0.0
+    U = 8.0 * R * float(np.sum(q))
+    KR8, JR8 = 8.0 * K * R, 8.0 * J * R
+    pass_flops = 2.0 * nnz * R + (2.0 * R * float(np.sum(Ik.astype(np.float64) * mm)) if l > 0 else 0.0)
+    SR8 = 8.0 * S * R
+    stream = F * (4 + 8 * l) + 16.0 * (K + 1) + 4.0 * K if l > 0 else 12.0 * nnz + 8.0 * (rows + 1)
     polar_flops = float(np.sum(2 * mm * R * R + 6 * np.maximum(mm, R) * q * q + 5 * 7 * q ** 3 + 2 * q ** 3
                                + 2 * mm * R * q))
-    return {
-        "spmm": {"bytes": stream + SR8 + JR8, "flops": 2.0 * (F * l * R if l else nnz * R), "bound": "hbm"},
-        "polar": {"bytes": 2 * SR8 + KR8 + 16 * K, "flops": polar_flops, "bound": "alu"},
-        "fh": {"bytes": 2 * SR8 + KR8, "flops": 2.0 * S * R * R, "bound": "hbm"},
-        "passB1": {"bytes": 3 * SR8 + 4 * KR8, "flops": float(np.sum(4 * mm * R * R)), "bound": "hbm"},
-        "grams_B": {"bytes": SR8 + KR8, "flops": 2.0 * (S + K) * R * R, "bound": "hbm"},
-        "scatter": {"bytes": stream + SR8 + JR8, "flops": 2.0 * (F * l * R if l else nnz * R), "bound": "hbm"},
-        "admm_V": {"bytes": 4 * JR8, "flops": 0.0, "bound": "hbm"},
-        "fit": {"bytes": 3 * JR8, "flops": 0.0, "bound": "hbm"},
-        "admm_H": {"bytes": 0, "flops": 0.0, "bound": "hbm"},
+    model = {
+        "spmm": {"bytes": BX + C + U + JR8, "layout_bytes": stream + SR8 + JR8, "flops": pass_flops, "bound": "hbm"},
+        "polar": {"bytes": 2 * U + KR8, "layout_bytes": 2 * SR8 + KR8, "flops": polar_flops, "bound": "alu"},
+        "fh": {"bytes": 2 * U + KR8, "layout_bytes": 2 * SR8 + KR8, "flops": 2.0 * S * R * R, "bound": "hbm"},
+        "passB1": {"bytes": 3 * U + 4 * KR8, "layout_bytes": 3 * SR8 + 4 * KR8, "flops": float(np.sum(4 * mm * R * R)),
+                   "bound": "hbm"},
+        "grams_B": {"bytes": U + KR8, "layout_bytes": SR8 + KR8, "flops": 2.0 * (S + K) * R * R, "bound": "hbm"},
+        "scatter": {"bytes": BX + C + U + JR8, "layout_bytes": stream + SR8 + JR8, "flops": pass_flops,
+                    "bound": "hbm"},
+        "admm_V": {"bytes": 4 * JR8, "layout_bytes": 4 * JR8, "flops": 0.0, "bound": "hbm"},
+        "fit": {"bytes": 3 * JR8, "layout_bytes": 3 * JR8, "flops": 0.0, "bound": "hbm"},
+        "admm_H": {"bytes": 0.0, "layout_bytes": 0.0, "flops": 0.0, "bound": "hbm"},
     }
+    b_iter = 2 * BX + 4 * U + 2 * C + 5 * KR8
+    return model, b_iter
 
 
 def load_traffic():
@@ -148,39 +165,73 @@ def load_traffic():
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def oracle_sample(cfg, n_patients: int, iters: int = 1, warm: int = 0):
-    import oracle
-    p = synthgen.generate(cfg, K=min(n_patients, cfg.K))
-    o = oracle.Oracle(p)
-    for _ in range(warm):
-        o.iterate(1)
-    t0 = time.perf_counter()
-    o.iterate(iters)
-    dt = (time.perf_counter() - t0) / iters
-    return p, dt
+def host_cpu():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:  # noqa: BLE001
+        pass
+    return os.cpu_count() or 1, model
+
+
+def oracle_sample(cfg, iters: int = 1, warm: int = 0):
+    """The oracle as it stands, on all host cores (oracle/sharded.py: one serial C oracle per process
+    over nnz-balanced patient shards), on the first n patients of the same workload. Returns
+    (nnz/s, seconds per iteration, description)."""
+    from oracle.sharded import ShardedOracle
+    cores, model = host_cpu()
+    n = min(cfg.K, ORACLE_PER_CORE[cfg.name] * cores * SAMPLE_SCALE)
+    so = ShardedOracle(cfg, procs=cores, K=n)
+    try:
+        if warm:
+            so.iterate(warm)
+        t0 = time.perf_counter()
+        so.iterate(iters)
+        sec = (time.perf_counter() - t0) / iters
+    finally:
+        so.close()
+    desc = (f"first {n} of {cfg.K} patients ({so.nnz} nnz) of the same workload; {iters} outer iteration(s) of the "
+            f"serial C oracle in {len(so.bounds)} processes (one per host core, nnz-balanced patient shards, "
+            f"fixed-order sums); host: {cores} cores, {model}")
+    return so.nnz / sec, sec, desc, cores
+
+
+def config_line(cfg, world: int, total_nnz: int):
+    return {"workload": cfg.baseline, "name": cfg.name, "K": cfg.K, "nnz": total_nnz, "R": cfg.R,
+            "parallelism": f"patients sharded nnz-balanced over {world} GPU(s)",
+            "l2": "inputs far larger than L2 (no flush)"}
 
 
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
     cfg = synthgen.CONFIGS[args.config]
-    n = ORACLE_SAMPLE[args.config]
-    import oracle  # noqa: F401
-    p = synthgen.generate(cfg, K=min(n, cfg.K))
-    o = oracle.Oracle(p)
-    for _ in range(args.warmup):
-        o.iterate(1)
-    t0 = time.perf_counter()
-    o.iterate(args.steps)
-    sec = (time.perf_counter() - t0) / args.steps
-    value = p.nnz / sec
-    sample = f"first {p.K} of {cfg.K} patients ({p.nnz} nnz) of the same workload, serial C oracle, 1 thread"
-    line = {"impl": "reference", "metric": "COPA outer iteration throughput (nonzeros per second)",
-            "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (seeded synthgen, BASELINE.json recipe)",
-            "config": {"workload": cfg.baseline, "sample_patients": p.K},
-            "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": 1, "kind": "oracle", "sample": sample},
+    from oracle.sharded import ShardedOracle
+    cores, model = host_cpu()
+    n = min(cfg.K, ORACLE_PER_CORE[cfg.name] * cores * SAMPLE_SCALE)
+    so = ShardedOracle(cfg, procs=cores, K=n)
+    try:
+        so.iterate(args.warmup)
+        t0 = time.perf_counter()
+        so.iterate(args.steps)
+        sec = (time.perf_counter() - t0) / args.steps
+    finally:
+        so.close()
+    value = so.nnz / sec
+    sample = (f"each step = one outer iteration over the first {n} of {cfg.K} patients ({so.nnz} nnz) of the same "
+              f"workload; serial C oracle in {len(so.bounds)} processes (one per host core); host: {cores} cores, "
+              f"{model}")
+    total_nnz = int(synthgen.patient_nnz(cfg).sum()) if cfg.K <= 4_000_000 else so.nnz
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded synthgen, BASELINE.json recipe)",
+            "config": config_line(cfg, world, total_nnz),
+            "cpu_baseline": {"value": value, "unit": "nnz/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -248,7 +299,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     fit_last = st["fit"]
     clk = clocks.summary(tw0, tw1)
     m = g.debug_state()["m"].cpu().numpy() if g.K > 0 else np.zeros(0, np.int32)
-    model = phase_model(st, cfg, g.R, g.K, g.J, g.rows, g.nnz, m)
+    Ik = np.diff(prob.patient_row_ptr)
+    model, b_iter = phase_model(st, cfg, g.R, g.K, g.J, g.rows, g.nnz, m, Ik)
     value = total_nnz * args.steps / (ms / 1e3)
     hbm_peak, hbm_src = peaks()
 
@@ -268,14 +320,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         else:
             ach = mdl["bytes"] / (ms_launch / 1e3) / 1e9
             roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": ach / hbm_peak, "traffic": traffic, "peak_source": hbm_src, "ms_per_launch": ms_launch}
+                    "frac": ach / hbm_peak, "traffic": traffic, "peak_source": hbm_src, "ms_per_launch": ms_launch,
+                    "alg_bytes": mdl["bytes"], "bytes_source": "SURVEY.md 8(d): B_X + C + U + 8JR per sparse pass",
+                    "layout_bytes": mdl["layout_bytes"],
+                    "layout_frac": mdl["layout_bytes"] / (ms_launch / 1e3) / 1e9 / hbm_peak}
             if mdl["flops"] > 0:  # the fiber passes also sit at the FP64 tensor-core (DMMA) ridge
                 tf = mdl["flops"] / (ms_launch / 1e3) / 1e12
                 roof["fp64_tensor"] = {"achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                       "frac": tf / DMMA_PEAK_TFLOPS, "flops": "2 F l R (useful, no padding)"}
-    step_bytes = sum(model[k]["bytes"] for k in model)
+                                       "frac": tf / DMMA_PEAK_TFLOPS,
+                                       "flops": "SURVEY 8(d): 2 nnz R + 2 R sum I_k l'_k per pass"}
     phase_report = {k: {"ms_per_launch": per_launch[k][0], "share": per_launch[k][0] / ms_per_step,
-                        "alg_GBps": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9) if k in model else None}
+                        "alg_GBps": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9) if k in model else None,
+                        "alg_frac": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9 / hbm_peak) if k in model
+                        else None}
                     for k in per_launch}
 
     # ---------------------------------------------------------------- end to end (host buffers)
@@ -309,34 +366,49 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # ---------------------------------------------------------------- CPU oracle baseline
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        p_s, sec = oracle_sample(cfg, ORACLE_SAMPLE[args.config])
-        cpu = {"value": p_s.nnz / sec, "unit": "nnz/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {p_s.K} of {cfg.K} patients ({p_s.nnz} nnz), 1 outer iteration, serial C oracle"}
     clocks.stop()
+    if rank == 0 and not args.no_cpu_baseline:  # after the timed region; other ranks wait at the barrier
+        v, sec, desc, cores = oracle_sample(cfg)
+        cpu = {"value": v, "unit": "nnz/s", "cores": cores, "kind": "oracle", "sample": desc,
+               "sec_per_iter": sec}
+    barrier()
 
     if rank == 0:
         line = {
-            "metric": "COPA outer iteration throughput (nonzeros per second; sec/iteration = ms_per_step/1000)",
+            "metric": METRIC,
             "value": value, "unit": "nnz/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded synthgen, BASELINE.json recipe)",
-            "config": {"workload": cfg.baseline, "name": args.config, "K": cfg.K, "nnz": total_nnz, "R": cfg.R,
-                       "parallelism": f"patients sharded nnz-balanced over {world} GPU(s)",
-                       "l2": "inputs far larger than L2 (no flush)"},
+            "config": config_line(cfg, world, total_nnz),
             "sec_per_iter": ms_per_step / 1e3,
-            "iteration_alg_GBps": step_bytes * world / (ms_per_step / 1e3) / 1e9,
+            "iteration_alg_GBps": b_iter * world / (ms_per_step / 1e3) / 1e9,
+            "iteration_alg_frac": b_iter * world / (ms_per_step / 1e3) / 1e9 / hbm_peak / world,
             "roofline": roof, "phases": phase_report, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches, "clocks": clk, "fit_last": fit_last, "init_s": init_s,
         }
         print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # not launched by torchrun: start one rank per GPU ourselves (same contract as the driver's launch)
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

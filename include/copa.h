@@ -94,6 +94,10 @@ typedef struct {
   int32_t admm_inner;                /* inner ADMM steps per mode (reading R-inner); >= 1 */
   double rank_tol;                   /* polar rank cut tau: sigma > tau*sigma_1 (reading R-polar-3), e.g. 1e-10 */
   double basis_tol;                  /* basis rank cut (reading R-spline-4), e.g. 1e-6 */
+  double admm_tol;                   /* inner stop ("while convergence criterion is not met", reading
+                                        R-inner-tol): 0 = exactly admm_inner steps; > 0 = each factor row stops
+                                        after the step where max(|row(Zbar) - row(Z)|, |row(Zbar) - previous
+                                        row(Zbar)|) <= admm_tol |row(Zbar)| (Euclidean), at most admm_inner */
   const double* H0;                  /* DEVICE, R x R initial H (copied at init) */
   const double* V0;                  /* DEVICE, J x R initial V (identical on all ranks) */
   const double* W0_local;            /* DEVICE, K_local x R initial W rows of this shard */
@@ -112,9 +116,21 @@ typedef struct {
   int64_t fibers;       /* (patient, feature) pairs of the shard (smooth path) */
   int64_t state_rows;   /* rows of the per-patient state (P', Q~) */
   int64_t rank_deficient; /* patients with r_k < min(m_k, R) in the last iteration (shard) */
+  double sparsity_V;    /* SPARSITY(V) = zero entries / size */
+  int64_t inner_steps[3]; /* ADMM inner steps of the H, W, V modes in the last iteration, summed over the
+                             factor rows (W: this shard's rows); admm_inner x rows when admm_tol = 0 */
+  /* Parity diagnostics of the two rank cuts (SURVEY 8(c) parity protocol; readings R-polar-3 and
+   * R-spline-4), ratios sigma_j / sigma_1. Polar: accumulated over all iterations since init, per
+   * (patient, iteration); basis: at init. near = count with some ratio within a factor 100 of the
+   * cut (tau/100 <= ratio <= 100 tau); min_kept = smallest kept ratio (1 if none); max_dropped =
+   * largest dropped ratio (0 if none). */
+  int64_t polar_near;
+  double polar_min_kept, polar_max_dropped;
+  int64_t basis_near;
+  double basis_min_kept, basis_max_dropped;
 } copa_stats;
 
-/* Kernel limits of this build (thread-per-patient polar: q = min(m_k, R) <= max_q). */
+/* Kernel limits of this build: R <= max_R, q = min(m_k, R) <= max_q (warp polar), smooth_l <= max_smooth_l. */
 typedef struct { int32_t max_R; int32_t max_q; int32_t max_smooth_l; int64_t max_J; } copa_limits;
 void copa_get_limits(copa_limits* out);
 
@@ -133,6 +149,14 @@ copa_status copa_init(const copa_problem* problem, const copa_options* options, 
  * stream once at the end (error check). */
 copa_status copa_iterate(copa_handle* h, int32_t n_outer, double* fit_host);
 
+/* Outer loop with a stop ("while convergence criterion is not met", reading R-outer-tol): runs
+ * up to max_outer iterations and stops after iteration t >= 2 of this call when
+ * |FIT_t - FIT_{t-1}| < outer_tol * max(|FIT_{t-1}|, 1). fit_host: HOST array of max_outer doubles
+ * (or NULL); n_done (HOST, may be NULL) receives the number of iterations run. Synchronises the
+ * stream after every iteration (the stop is a host decision on the device-computed FIT). */
+copa_status copa_iterate_until(copa_handle* h, int32_t max_outer, double outer_tol, double* fit_host,
+                               int32_t* n_done);
+
 /* Factors of record (the auxiliary variables, Alg.1 l.21). Each pointer may be a DEVICE or
  * HOST pointer (detected with cudaPointerGetAttributes) or NULL to skip.
  * H: R x R, V: J x R, W_local: K_local x R. */
@@ -140,6 +164,25 @@ copa_status copa_get_factors(copa_handle* h, double* H, double* V, double* W_loc
 
 /* Duals (scaled form) with the same layout/pointer rules as copa_get_factors. */
 copa_status copa_get_duals(copa_handle* h, double* DH, double* DV, double* DW_local);
+
+/* Checkpoint / resume. The state that carries an outer iteration into the next (Alg.1 l.3-l.20;
+ * Q_k is recomputed from it by the Procrustes step, l.4): the working factors, the scaled duals,
+ * and the two Grams the next H-mode reads (l.11: V^T V, and W^T W summed over ranks). Every
+ * pointer is a DEVICE or HOST pointer (as in copa_get_factors); W_local/DW_local may be NULL when
+ * K_local = 0. Shapes: H, DH, WtW, VtV R x R; V, DV J x R; W_local, DW_local K_local x R. */
+typedef struct {
+  double *H, *V, *W_local, *DH, *DV, *DW_local, *WtW, *VtV;
+  int64_t iterations; /* outer iterations completed */
+} copa_state;
+
+/* Copy the state out (synchronises the stream). */
+copa_status copa_get_state(copa_handle* h, const copa_state* out);
+
+/* Load a state into an initialised handle (same problem, options and rank layout). WtW and VtV may
+ * be NULL: they are then recomputed from W and V (W^T W through the allreduce callback, so every
+ * rank must call it), equal to the saved ones up to summation order. With all eight arrays the
+ * resumed run continues bit-identically. */
+copa_status copa_set_state(copa_handle* h, const copa_state* in);
 
 /* U_k = C_k Q_k H (smooth) or Q_k H (Alg.1 l.24), stacked over the shard's rows:
  * U_rows is a DEVICE or HOST pointer to rows x R doubles. */

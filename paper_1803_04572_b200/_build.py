@@ -33,22 +33,45 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.basename(src) + ".o")
+
+
+def _stale(src: str) -> bool:
+    """Object older than its source or any header nvcc listed for it (-MD dependency file)."""
+    obj = _obj(src)
+    dep = obj + ".d"
+    if not (os.path.exists(obj) and os.path.exists(dep)):
+        return True
+    t = os.path.getmtime(obj)
+    text = open(dep).read().replace("\\\n", " ")
+    files = [w for w in text.split(":", 1)[-1].split() if w != "\\"]
+    return any((not os.path.exists(d)) or os.path.getmtime(d) > t for d in files + [src])
+
+
 def _compile(src: str, verbose: bool) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    cmd = [NVCC] + FLAGS + ["-I", os.path.join(HERE, "..", "include"), "-c", src, "-o", obj]
+    obj = _obj(src)
+    cmd = [NVCC] + FLAGS + ["-I", os.path.join(HERE, "..", "include"), "-MD", "-MF", obj + ".d", "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
     return obj
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, incremental: bool = False) -> str:
+    """force: recompile every object (the driver's build check). incremental: recompile only the
+    objects whose source or headers changed (developer loop), then relink."""
+    if not force and not incremental and not needs_build():
         return SO
     os.makedirs(OBJ, exist_ok=True)
     srcs = sources()
-    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    todo = srcs if force else [s for s in srcs if _stale(s)]
+    if todo:
+        with ThreadPoolExecutor(max_workers=len(todo)) as ex:
+            list(ex.map(lambda s: _compile(s, verbose), todo))
+    elif os.path.exists(SO) and not force:
+        return SO
+    objs = [_obj(s) for s in srcs]
     cmd = [NVCC] + ARCH + ["-shared", "-o", SO] + objs
     if verbose:
         print(" ".join(cmd), flush=True)
@@ -57,4 +80,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    build(force="--incremental" not in sys.argv, incremental="--incremental" in sys.argv, verbose=True)

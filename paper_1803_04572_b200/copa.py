@@ -44,14 +44,24 @@ class _Options(ctypes.Structure):
     _fields_ = [("on_H", _Constraint), ("on_W", _Constraint), ("on_V", _Constraint),
                 ("smooth_l", ctypes.c_int32), ("smooth_degree", ctypes.c_int32), ("rho", ctypes.c_double),
                 ("admm_inner", ctypes.c_int32), ("rank_tol", ctypes.c_double), ("basis_tol", ctypes.c_double),
-                ("H0", ctypes.c_void_p), ("V0", ctypes.c_void_p), ("W0_local", ctypes.c_void_p),
+                ("admm_tol", ctypes.c_double), ("H0", ctypes.c_void_p), ("V0", ctypes.c_void_p), ("W0_local", ctypes.c_void_p),
                 ("allreduce", ALLREDUCE_FN), ("allreduce_ctx", ctypes.c_void_p), ("stream", ctypes.c_void_p)]
 
 
 class _Stats(ctypes.Structure):
     _fields_ = [("fit", ctypes.c_double), ("rho", ctypes.c_double * 3), ("normX", ctypes.c_double),
                 ("iterations", ctypes.c_int64), ("fibers", ctypes.c_int64), ("state_rows", ctypes.c_int64),
-                ("rank_deficient", ctypes.c_int64)]
+                ("rank_deficient", ctypes.c_int64), ("sparsity_V", ctypes.c_double),
+                ("inner_steps", ctypes.c_int64 * 3), ("polar_near", ctypes.c_int64),
+                ("polar_min_kept", ctypes.c_double), ("polar_max_dropped", ctypes.c_double),
+                ("basis_near", ctypes.c_int64), ("basis_min_kept", ctypes.c_double),
+                ("basis_max_dropped", ctypes.c_double)]
+
+
+class _State(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_void_p), ("V", ctypes.c_void_p), ("W_local", ctypes.c_void_p), ("DH", ctypes.c_void_p),
+                ("DV", ctypes.c_void_p), ("DW_local", ctypes.c_void_p), ("WtW", ctypes.c_void_p),
+                ("VtV", ctypes.c_void_p), ("iterations", ctypes.c_int64)]
 
 
 class _Limits(ctypes.Structure):
@@ -74,6 +84,9 @@ def lib() -> ctypes.CDLL:
         L.copa_workspace_size.argtypes = [P, O, sz]
         L.copa_init.argtypes = [P, O, vp, ctypes.c_size_t, ctypes.POINTER(vp)]
         L.copa_iterate.argtypes = [vp, i32, vp]
+        L.copa_iterate_until.argtypes = [vp, i32, ctypes.c_double, vp, ctypes.POINTER(i32)]
+        L.copa_set_state.argtypes = [vp, ctypes.POINTER(_State)]
+        L.copa_get_state.argtypes = [vp, ctypes.POINTER(_State)]
         L.copa_get_factors.argtypes = [vp, vp, vp, vp]
         L.copa_get_duals.argtypes = [vp, vp, vp, vp]
         L.copa_get_U.argtypes = [vp, vp]
@@ -90,7 +103,9 @@ def lib() -> ctypes.CDLL:
         L.copa_phase_name.restype = ctypes.c_char_p
         L.copa_get_limits.argtypes = [ctypes.POINTER(_Limits)]
         L.copa_get_limits.restype = None
-        for f in ("copa_workspace_size", "copa_init", "copa_iterate", "copa_get_factors", "copa_get_duals",
+        for f in ("copa_workspace_size", "copa_init", "copa_iterate", "copa_iterate_until", "copa_set_state",
+                  "copa_get_state",
+                  "copa_get_factors", "copa_get_duals",
                   "copa_get_U", "copa_get_stats", "copa_fit_workspace_size", "copa_fit", "copa_debug_state",
                   "copa_set_profiling", "copa_get_phase_times"):
             getattr(L, f).restype = ctypes.c_int
@@ -121,11 +136,21 @@ class Options:
     admm_inner: int = 5
     rank_tol: float = 1e-10
     basis_tol: float = 1e-6
+    admm_tol: float = 0.0
 
     @staticmethod
-    def from_config(cfg) -> "Options":
-        return Options(con_H=tuple(cfg.con_H), con_W=tuple(cfg.con_W), con_V=tuple(cfg.con_V), smooth_l=cfg.smooth_l,
-                       rho=cfg.rho, admm_inner=cfg.n_inner)
+    def from_config(cfg, **over) -> "Options":
+        kw = dict(con_H=tuple(cfg.con_H), con_W=tuple(cfg.con_W), con_V=tuple(cfg.con_V), smooth_l=cfg.smooth_l,
+                  rho=cfg.rho, admm_inner=cfg.n_inner)
+        kw.update(over)
+        return Options(**kw)
+
+    def c_struct(self, H0, V0, W0, allreduce_cb, stream) -> "_Options":
+        return _Options(on_H=_Constraint(*self.con_H), on_W=_Constraint(*self.con_W), on_V=_Constraint(*self.con_V),
+                        smooth_l=self.smooth_l, smooth_degree=self.smooth_degree, rho=self.rho,
+                        admm_inner=self.admm_inner, rank_tol=self.rank_tol, basis_tol=self.basis_tol,
+                        admm_tol=self.admm_tol, H0=H0, V0=V0, W0_local=W0, allreduce=allreduce_cb,
+                        allreduce_ctx=None, stream=stream)
 
 
 def _torch():
@@ -144,9 +169,11 @@ class _CAI:
 def torch_allreduce(group=None, device: str = "cuda") -> Callable:
     """Allreduce(sum) callback over torch.distributed for copa_options.allreduce.
 
-    device="cuda": the library passes a device pointer and its stream, which is torch's current
-    stream, so NCCL's all_reduce is ordered after the producing kernels without a host sync.
-    device="cpu": host buffers (gloo), used by the multi-rank host-logic tests.
+    device="cuda": the library passes a device pointer and the stream it enqueues on; the
+    all_reduce is issued with that stream as torch's current stream, so NCCL is ordered after the
+    producing kernels and before the consuming ones without a host sync, whatever stream the
+    handle was created with. device="cpu": host buffers (gloo), used by the multi-rank host-logic
+    tests.
     """
     torch = _torch()
     import torch.distributed as dist
@@ -156,9 +183,11 @@ def torch_allreduce(group=None, device: str = "cuda") -> Callable:
             if device == "cpu":
                 arr = np.ctypeslib.as_array((ctypes.c_double * int(n)).from_address(int(ptr)))
                 t = torch.from_numpy(arr)
+                dist.all_reduce(t, group=group)
             else:
                 t = torch.as_tensor(_CAI(ptr, n), device="cuda")
-            dist.all_reduce(t, group=group)
+                with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0))):
+                    dist.all_reduce(t, group=group)
             return 0
         except Exception:  # noqa: BLE001 - reported to the library as a status
             return 1
@@ -201,12 +230,8 @@ class Copa:
                           visit_time=self.t_times.data_ptr() if self.t_times is not None else None)
         self._cb = ALLREDUCE_FN(allreduce) if allreduce is not None else ALLREDUCE_FN()
         self.options = options
-        self.o = _Options(on_H=_Constraint(*options.con_H), on_W=_Constraint(*options.con_W),
-                          on_V=_Constraint(*options.con_V), smooth_l=options.smooth_l,
-                          smooth_degree=options.smooth_degree, rho=options.rho, admm_inner=options.admm_inner,
-                          rank_tol=options.rank_tol, basis_tol=options.basis_tol, H0=self.t_H0.data_ptr(),
-                          V0=self.t_V0.data_ptr(), W0_local=self.t_W0.data_ptr() if self.K else None,
-                          allreduce=self._cb, allreduce_ctx=None, stream=self.stream.cuda_stream)
+        self.o = options.c_struct(self.t_H0.data_ptr(), self.t_V0.data_ptr(), self.t_W0.data_ptr() if self.K else None,
+                                  self._cb, self.stream.cuda_stream)
         nbytes = ctypes.c_size_t(0)
         _check(L.copa_workspace_size(ctypes.byref(self.p), ctypes.byref(self.o), ctypes.byref(nbytes)))
         self.ws = torch.empty(int(nbytes.value), dtype=torch.uint8, device="cuda")
@@ -222,6 +247,40 @@ class Copa:
         _check(lib().copa_iterate(self.h, n, fits.ctypes.data_as(ctypes.c_void_p)))
         self.fits.extend(fits[:n].tolist())
         return fits[:n].tolist()
+
+    def iterate_until(self, max_outer: int, outer_tol: float) -> list:
+        """copa_iterate_until: outer loop with the FIT-change stop (reading R-outer-tol)."""
+        fits = np.zeros(max(max_outer, 1))
+        done = ctypes.c_int32(0)
+        _check(lib().copa_iterate_until(self.h, max_outer, outer_tol, fits.ctypes.data_as(ctypes.c_void_p),
+                                        ctypes.byref(done)))
+        out = fits[:done.value].tolist()
+        self.fits.extend(out)
+        return out
+
+    _STATE_KEYS = ("H", "V", "W", "DH", "DV", "DW", "WtW", "VtV")
+
+    def get_state(self) -> dict:
+        """copa_get_state (checkpoint): factors, scaled duals and the two Grams, as device tensors."""
+        t = self.torch
+        R, J, K = self.R, self.J, self.K
+        shapes = {"H": (R, R), "V": (J, R), "W": (max(K, 1), R), "DH": (R, R), "DV": (J, R), "DW": (max(K, 1), R),
+                  "WtW": (R, R), "VtV": (R, R)}
+        out = {k: t.empty(shapes[k], dtype=t.float64, device="cuda") for k in self._STATE_KEYS}
+        st = _State(*[out[k].data_ptr() for k in self._STATE_KEYS], 0)
+        _check(lib().copa_get_state(self.h, ctypes.byref(st)))
+        out["W"] = out["W"][:K]
+        out["DW"] = out["DW"][:K]
+        out["iterations"] = self.stats()["iterations"]
+        return out
+
+    def set_state(self, state: dict):
+        """copa_set_state (resume). WtW / VtV may be missing (recomputed from W and V)."""
+        t = self.torch
+        keep = {k: _dev(t, state[k], t.float64).contiguous() for k in self._STATE_KEYS if state.get(k) is not None}
+        ptr = [keep[k].data_ptr() if k in keep and keep[k].numel() else None for k in self._STATE_KEYS]
+        st = _State(*ptr, int(state.get("iterations", 0)))
+        _check(lib().copa_set_state(self.h, ctypes.byref(st)))
 
     def iterate_async(self, n: int = 1):
         """Enqueue n outer iterations without a FIT host copy (the library still syncs once at the end)."""
@@ -250,11 +309,20 @@ class Copa:
         _check(lib().copa_get_U(self.h, U.data_ptr()))
         return U[:self.rows]
 
+    def U_host(self) -> np.ndarray:
+        """copa_get_U into a HOST buffer (the library stages patient chunks through device state)."""
+        U = np.zeros((max(self.rows, 1), self.R))
+        _check(lib().copa_get_U(self.h, U.ctypes.data_as(ctypes.c_void_p)))
+        return U[:self.rows]
+
     def stats(self) -> dict:
         s = _Stats()
         _check(lib().copa_get_stats(self.h, ctypes.byref(s)))
         return {"fit": s.fit, "rho": list(s.rho), "normX": s.normX, "iterations": s.iterations, "fibers": s.fibers,
-                "state_rows": s.state_rows, "rank_deficient": s.rank_deficient}
+                "state_rows": s.state_rows, "rank_deficient": s.rank_deficient, "sparsity_V": s.sparsity_V,
+                "inner_steps": list(s.inner_steps), "polar_near": s.polar_near, "polar_min_kept": s.polar_min_kept,
+                "polar_max_dropped": s.polar_max_dropped, "basis_near": s.basis_near,
+                "basis_min_kept": s.basis_min_kept, "basis_max_dropped": s.basis_max_dropped}
 
     def set_profiling(self, on: bool = True):
         """Record CUDA events around each phase of the iteration (on the library's stream)."""
@@ -321,12 +389,8 @@ def fit_host(prob, options: Options, n_outer: int, R: Optional[int] = None, stre
                  visit_time=hp(prob.times, np.float64) if options.smooth_l > 0 else None)
     stream = stream if stream is not None else torch.cuda.current_stream()
     cb = ALLREDUCE_FN(allreduce) if allreduce is not None else ALLREDUCE_FN()
-    o = _Options(on_H=_Constraint(*options.con_H), on_W=_Constraint(*options.con_W), on_V=_Constraint(*options.con_V),
-                 smooth_l=options.smooth_l, smooth_degree=options.smooth_degree, rho=options.rho,
-                 admm_inner=options.admm_inner, rank_tol=options.rank_tol, basis_tol=options.basis_tol,
-                 H0=hp(np.asarray(prob.H0)[:R, :R], np.float64), V0=hp(prob.V0, np.float64),
-                 W0_local=hp(prob.W0, np.float64), allreduce=cb, allreduce_ctx=None,
-                 stream=stream.cuda_stream)
+    o = options.c_struct(hp(np.asarray(prob.H0)[:R, :R], np.float64), hp(prob.V0, np.float64),
+                         hp(prob.W0, np.float64), cb, stream.cuda_stream)
     if workspace is None:
         nbytes = ctypes.c_size_t(0)
         _check(L.copa_fit_workspace_size(ctypes.byref(p), ctypes.byref(o), ctypes.byref(nbytes)))
@@ -347,10 +411,7 @@ def fit_workspace_bytes(prob, options: Options, R: Optional[int] = None) -> int:
     p = _Problem(K_local=len(prp) - 1, K_global=len(prp) - 1, J=int(prob.J), R=R, rows=len(rp) - 1,
                  nnz=len(prob.col), patient_row_ptr=prp.ctypes.data, row_ptr=rp.ctypes.data, col=1, val=1,
                  visit_time=1 if options.smooth_l > 0 else None)
-    o = _Options(on_H=_Constraint(*options.con_H), on_W=_Constraint(*options.con_W), on_V=_Constraint(*options.con_V),
-                 smooth_l=options.smooth_l, smooth_degree=options.smooth_degree, rho=options.rho,
-                 admm_inner=options.admm_inner, rank_tol=options.rank_tol, basis_tol=options.basis_tol, H0=1, V0=1,
-                 W0_local=1, allreduce=ALLREDUCE_FN(), allreduce_ctx=None, stream=None)
+    o = options.c_struct(1, 1, 1, ALLREDUCE_FN(), None)
     nbytes = ctypes.c_size_t(0)
     _check(L.copa_fit_workspace_size(ctypes.byref(p), ctypes.byref(o), ctypes.byref(nbytes)))
     return int(nbytes.value)

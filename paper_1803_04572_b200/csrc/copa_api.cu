@@ -3,6 +3,7 @@
 #include <cub/cub.cuh>
 
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -80,6 +81,8 @@ size_t carve(Handle& h, char* base) {
     h.fh_warp = c.take<double>(h.smooth ? (int64_t)kPartBlocks * 4 * RP * RP : 1);
   }
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
+  h.diag = c.take<unsigned long long>(kDiagSlots);
+  h.steps = c.take<unsigned long long>(4);
   if (h.smooth) {
     const int G = h.sc_G;
     h.Fcap = h.F + 8;
@@ -95,8 +98,6 @@ size_t carve(Handle& h, char* base) {
     h.fa_col = c.take<int32_t>(h.F + 64);
     h.fa_val = c.take<double>((h.F + 64) * h.l);
     h.pa_wk = c.take<int64_t>(h.pa_nw + 1);
-    h.hot_slot = c.take<int32_t>(h.Jl);
-    h.hot_lab = c.take<int32_t>(h.pa_nhot > 0 ? h.pa_nhot : 1);
     h.block_k = c.take<int64_t>(h.sc_ranges + 1);
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
@@ -109,6 +110,15 @@ size_t carve(Handle& h, char* base) {
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     h.row_patient = c.take<int32_t>(h.rows);
+    h.csc_ptr = c.take<int64_t>(h.J + 1);
+    h.csc_row = c.take<int32_t>(h.nnz);
+    h.csc_val = c.take<double>(h.nnz);
+    h.csc_chunk_cap = h.nnz / kCscChunk + h.J + 1;
+    h.csc_chunk = c.take<int64_t>(2 * h.csc_chunk_cap);
+    h.csc_chunk_first = c.take<int64_t>(h.J + 1);
+    h.csc_part = c.take<double>(h.csc_chunk_cap * R);
+    h.csc_tmp_bytes = csc_temp_bytes(h);
+    h.csc_tmp = c.take<char>((int64_t)h.csc_tmp_bytes);
   }
   return c.off;
 }
@@ -128,16 +138,14 @@ copa_status check_args(const copa_problem* p, const copa_options* o) {
     if ((c->kind == COPA_L1 || c->kind == COPA_NONNEG_L1) && !(c->param >= 0)) return fail(COPA_E_ARG, "lambda < 0");
     if (c->kind == COPA_L0 && !(c->param > 0)) return fail(COPA_E_ARG, "mu <= 0");
   }
-  if (!(o->rank_tol >= 0) || !(o->basis_tol >= 0)) return fail(COPA_E_ARG, "tolerances must be >= 0");
+  if (!(o->rank_tol >= 0) || !(o->basis_tol >= 0) || !(o->admm_tol >= 0))
+    return fail(COPA_E_ARG, "tolerances must be >= 0");
   if (o->smooth_l < 0) return fail(COPA_E_ARG, "smooth_l < 0");
   if (o->smooth_l > 0) {
     if (o->smooth_l > kMaxL) return fail(COPA_E_UNSUPPORTED, "smooth_l > 16 not supported");
     if (o->smooth_degree < 0 || o->smooth_degree > kMaxDeg || o->smooth_degree >= o->smooth_l)
       return fail(COPA_E_ARG, "smooth_degree must be in [0, min(7, l-1)]");
     if (p->K_local > 0 && !p->visit_time) return fail(COPA_E_ARG, "smoothness requires visit times");
-  } else if (p->R > kMaxQ) {
-    // plain path: tall patients have q = R; this build's thread-per-patient polar needs q <= 16
-    return fail(COPA_E_UNSUPPORTED, "R > 16 without smoothness not supported by this build");
   }
   if (!o->H0 || !o->V0 || (p->K_local > 0 && !o->W0_local)) return fail(COPA_E_ARG, "null initial factors");
   return COPA_OK;
@@ -147,6 +155,10 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   h.p = *p;
   h.o = *o;
   h.stream = (cudaStream_t)o->stream;
+  if (cudaGetDevice(&h.dev) != cudaSuccess) { cudaGetLastError(); h.dev = 0; }
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.dev) == cudaSuccess && sms > 0) h.sms = sms;
+  else cudaGetLastError();
   h.smooth = o->smooth_l > 0;
   h.l = o->smooth_l;
   h.d = o->smooth_degree;
@@ -230,7 +242,7 @@ extern "C" {
 void copa_get_limits(copa_limits* out) {
   if (!out) return;
   out->max_R = kMaxR;
-  out->max_q = kMaxQ;
+  out->max_q = kMaxR;
   out->max_smooth_l = kMaxL;
   out->max_J = kMaxJ;
 }
@@ -292,6 +304,11 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   cudaMemsetAsync(h.Qt, 0, sizeof(double) * (size_t)(h.S * h.R), s);
   cudaMemsetAsync(h.Nst, 0, sizeof(double) * (size_t)(h.S * h.R), s);
   cudaMemsetAsync(h.rank, 0, sizeof(int32_t) * (size_t)(h.K > 0 ? h.K : 1), s);
+  cudaMemsetAsync(h.steps, 0, 4 * sizeof(unsigned long long), s);
+  {  // rank-cut diagnostics: counts 0, min-kept ratios +inf, max-dropped ratios 0
+    static const unsigned long long d0[kDiagSlots] = {0, 0x7ff0000000000000ull, 0, 0, 0x7ff0000000000000ull, 0, 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(h.diag, d0, sizeof(d0), cudaMemcpyHostToDevice, s), "diag init");
+  }
   launch_validate(h);
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
@@ -312,13 +329,6 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       compute_relabel(h.J, h.sc_G * h.sc_W, hist.data(), perm.data(), inv.data(), &Js);
       CUDA_TRY(cudaMemcpyAsync(h.perm, perm.data(), sizeof(int32_t) * (size_t)h.J, cudaMemcpyHostToDevice, s), "perm");
       CUDA_TRY(cudaMemcpyAsync(h.inv, inv.data(), sizeof(int32_t) * (size_t)h.Jl, cudaMemcpyHostToDevice, s), "inv");
-      std::vector<int32_t> hslot, hlab;
-      plan_passA_hot(h, hist.data(), inv.data(), hslot, hlab);
-      CUDA_TRY(cudaMemcpyAsync(h.hot_slot, hslot.data(), sizeof(int32_t) * hslot.size(), cudaMemcpyHostToDevice, s),
-               "hot_slot");
-      if (!hlab.empty())
-        CUDA_TRY(cudaMemcpyAsync(h.hot_lab, hlab.data(), sizeof(int32_t) * hlab.size(), cudaMemcpyHostToDevice, s),
-                 "hot_lab");
       CUDA_TRY(cudaStreamSynchronize(s), "perm sync");
     }
     tm.mark("relabel");
@@ -377,6 +387,12 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   } else {
     launch_row_patient(h);
     if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);
+    const int rc = build_csc(h);
+    if (rc != 0) {
+      delete H;
+      return rc == -2 ? fail(COPA_E_WORKSPACE, "internal: CSC chunk table exceeds its bound")
+                      : cuda_fail(cudaGetLastError(), "CSC build");
+    }
   }
   cudaMemcpyAsync(h.H, o->H0, sizeof(double) * RR, cudaMemcpyDefault, s);
   cudaMemcpyAsync(h.V, o->V0, sizeof(double) * (size_t)(h.J * h.R), cudaMemcpyDefault, s);
@@ -435,11 +451,13 @@ static void phase_collect(Handle& h) {
   h.ev_phase.clear();
 }
 
-#define PHASE(ph, expr)  \
-  do {                   \
-    phase_begin(h, ph);  \
-    h.launches += (expr); \
-    phase_end(h);        \
+#define PHASE(ph, expr)                                                    \
+  do {                                                                     \
+    phase_begin(h, ph);                                                    \
+    h.launches += (expr);                                                  \
+    phase_end(h);                                                          \
+    const cudaError_t pe_ = cudaGetLastError();                            \
+    if (pe_ != cudaSuccess) return cuda_fail(pe_, kPhaseNames[ph]);         \
   } while (0)
 
 static copa_status iterate_once(Handle& h) {
@@ -447,7 +465,7 @@ static copa_status iterate_once(Handle& h) {
   const int64_t RR = (int64_t)h.R * h.R;
   const bool wide = polar_wide_ok(h);
   PHASE(0, launch_spmm(h));
-  PHASE(1, wide ? launch_polar_wide(h) : launch_polar(h));  // wide: F_H fused into the polar kernel
+  PHASE(1, wide ? launch_polar_wide(h) : launch_polar_warp(h));  // wide: F_H fused into the polar kernel
   if (!wide) PHASE(2, launch_fh(h));
   PHASE(3, (st = allreduce(h, h.FH, RR), 0));  // C1
   if (st != COPA_OK) return st;
@@ -455,7 +473,7 @@ static copa_status iterate_once(Handle& h) {
   if (wide) {
     PHASE(5, launch_passB_wide(h));  // F_W, W rows, N, M and W^T W in one pass
   } else {
-    PHASE(5, launch_passB1(h));
+    PHASE(5, launch_passB_warp(h));
     PHASE(6, launch_gram(h, h.W, h.W, h.K, 0, h.WtW) + launch_gram(h, h.Nst, h.Nst, h.S, 0, h.M));
   }
   PHASE(7, launch_scatter(h));
@@ -492,6 +510,79 @@ copa_status copa_iterate(copa_handle* H, int32_t n_outer, double* fit_host) {
   return COPA_OK;
 }
 
+copa_status copa_iterate_until(copa_handle* H, int32_t max_outer, double outer_tol, double* fit_host,
+                               int32_t* n_done) {
+  if (!H) return fail(COPA_E_ARG, "null handle");
+  if (max_outer < 0 || !(outer_tol >= 0)) return fail(COPA_E_ARG, "max_outer < 0 or outer_tol < 0");
+  Handle& h = H->h;
+  if (n_done) *n_done = 0;
+  double prev = 0.0;
+  for (int32_t t = 0; t < max_outer; ++t) {
+    copa_status st = iterate_once(h);
+    if (st != COPA_OK) return st;
+    ++h.iterations;
+    double fit = 0.0;
+    CUDA_TRY(cudaMemcpyAsync(&fit, h.scal + S_FIT, sizeof(double), cudaMemcpyDeviceToHost, h.stream), "fit copy");
+    st = check_err(h);  // synchronises
+    if (st != COPA_OK) return st;
+    phase_collect(h);
+    if (fit_host) fit_host[t] = fit;
+    if (n_done) *n_done = t + 1;
+    if (t >= 1 && std::fabs(fit - prev) < outer_tol * std::fmax(std::fabs(prev), 1.0)) break;
+    prev = fit;
+  }
+  return COPA_OK;
+}
+
+copa_status copa_get_state(copa_handle* H, const copa_state* out) {
+  if (!H || !out) return fail(COPA_E_ARG, "null handle/state");
+  Handle& h = H->h;
+  const size_t RR = sizeof(double) * (size_t)h.R * h.R, JR = sizeof(double) * (size_t)(h.J * h.R),
+               KR = sizeof(double) * (size_t)(h.K * h.R);
+  cudaStream_t s = h.stream;
+  const double* src[8] = {h.H, h.V, h.W, h.DH, h.DV, h.DW, h.WtW, h.VtV};
+  double* dst[8] = {out->H, out->V, out->W_local, out->DH, out->DV, out->DW_local, out->WtW, out->VtV};
+  const size_t sz[8] = {RR, JR, KR, RR, JR, KR, RR, RR};
+  for (int i = 0; i < 8; ++i) {
+    if (sz[i] == 0) continue;
+    if (!dst[i]) return fail(COPA_E_ARG, "null state pointer");
+    CUDA_TRY(cudaMemcpyAsync(dst[i], src[i], sz[i], cudaMemcpyDefault, s), "get state");
+  }
+  CUDA_TRY(cudaStreamSynchronize(s), "get state sync");
+  // the caller's struct is const; iterations is reported through copa_get_stats
+  return COPA_OK;
+}
+
+copa_status copa_set_state(copa_handle* H, const copa_state* in) {
+  if (!H || !in) return fail(COPA_E_ARG, "null handle/state");
+  Handle& h = H->h;
+  if (!in->H || !in->V || !in->DH || !in->DV || (h.K > 0 && (!in->W_local || !in->DW_local)))
+    return fail(COPA_E_ARG, "null state pointer");
+  const size_t RR = sizeof(double) * (size_t)h.R * h.R, JR = sizeof(double) * (size_t)(h.J * h.R),
+               KR = sizeof(double) * (size_t)(h.K * h.R);
+  cudaStream_t s = h.stream;
+  CUDA_TRY(cudaMemcpyAsync(h.H, in->H, RR, cudaMemcpyDefault, s), "set H");
+  CUDA_TRY(cudaMemcpyAsync(h.DH, in->DH, RR, cudaMemcpyDefault, s), "set DH");
+  CUDA_TRY(cudaMemcpyAsync(h.V, in->V, JR, cudaMemcpyDefault, s), "set V");
+  CUDA_TRY(cudaMemcpyAsync(h.DV, in->DV, JR, cudaMemcpyDefault, s), "set DV");
+  if (h.K > 0) {
+    CUDA_TRY(cudaMemcpyAsync(h.W, in->W_local, KR, cudaMemcpyDefault, s), "set W");
+    CUDA_TRY(cudaMemcpyAsync(h.DW, in->DW_local, KR, cudaMemcpyDefault, s), "set DW");
+  }
+  // the Grams the next iteration's H-mode reads (Alg.1 l.11)
+  if (in->VtV) CUDA_TRY(cudaMemcpyAsync(h.VtV, in->VtV, RR, cudaMemcpyDefault, s), "set VtV");
+  else launch_gram(h, h.V, h.V, h.J, 0, h.VtV);
+  if (in->WtW) {
+    CUDA_TRY(cudaMemcpyAsync(h.WtW, in->WtW, RR, cudaMemcpyDefault, s), "set WtW");
+  } else {
+    launch_gram(h, h.W, h.W, h.K, 0, h.WtW);
+    copa_status st = allreduce(h, h.WtW, (int64_t)h.R * h.R);
+    if (st != COPA_OK) return st;
+  }
+  h.iterations = in->iterations;
+  return check_err(h);
+}
+
 copa_status copa_get_factors(copa_handle* H, double* Hout, double* Vout, double* Wout) {
   if (!H) return fail(COPA_E_ARG, "null handle");
   Handle& h = H->h;
@@ -521,12 +612,27 @@ copa_status copa_get_U(copa_handle* H, double* U) {
   cudaError_t e = cudaPointerGetAttributes(&attr, U);
   if (e != cudaSuccess) cudaGetLastError();
   if (e == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged)) {
-    launch_U(h, U);
-  } else {
-    // host destination: stage through the state buffer N (overwritten; rebuilt by the next iteration)
-    if (h.rows > h.S) return fail(COPA_E_UNSUPPORTED, "host U needs a device buffer when rows > state rows");
-    launch_U(h, h.Nst);
-    CUDA_TRY(cudaMemcpyAsync(U, h.Nst, sizeof(double) * h.rows * h.R, cudaMemcpyDefault, h.stream), "get U");
+    launch_U(h, U, 0, h.K);
+  } else if (h.K > 0) {
+    // host destination: patient chunks staged through the state buffer N (S x R doubles; overwritten,
+    // rebuilt by the next iteration's pass B)
+    std::vector<int64_t> prp((size_t)h.K + 1);
+    CUDA_TRY(cudaMemcpyAsync(prp.data(), h.p.patient_row_ptr, sizeof(int64_t) * prp.size(), cudaMemcpyDeviceToHost,
+                             h.stream), "get U prp");
+    CUDA_TRY(cudaStreamSynchronize(h.stream), "get U sync");
+    const int64_t cap = h.S > 0 ? h.S : 0;
+    int64_t k0 = 0;
+    while (k0 < h.K) {
+      int64_t k1 = k0;
+      while (k1 < h.K && prp[(size_t)k1 + 1] - prp[(size_t)k0] <= cap) ++k1;
+      if (k1 == k0) return fail(COPA_E_UNSUPPORTED, "host U: a patient has more rows than the state buffer");
+      launch_U(h, h.Nst, k0, k1);
+      CUDA_TRY(cudaMemcpyAsync(U + prp[(size_t)k0] * h.R, h.Nst,
+                               sizeof(double) * (size_t)(prp[(size_t)k1] - prp[(size_t)k0]) * h.R,
+                               cudaMemcpyDeviceToHost, h.stream), "get U");
+      CUDA_TRY(cudaStreamSynchronize(h.stream), "get U sync");  // N is reused by the next chunk
+      k0 = k1;
+    }
   }
   return check_err(h);
 }
@@ -552,6 +658,24 @@ copa_status copa_get_stats(copa_handle* H, copa_stats* out) {
   out->fibers = h.F;
   out->state_rows = h.S;
   out->rank_deficient = (int64_t)rd;
+  unsigned long long dg[kDiagSlots], stp[4];
+  launch_count_zeros(h);
+  CUDA_TRY(cudaMemcpyAsync(dg, h.diag, sizeof(dg), cudaMemcpyDeviceToHost, h.stream), "stats diag");
+  CUDA_TRY(cudaMemcpyAsync(stp, h.steps, sizeof(stp), cudaMemcpyDeviceToHost, h.stream), "stats steps");
+  CUDA_TRY(cudaStreamSynchronize(h.stream), "stats sync");
+  auto ratio = [](unsigned long long b, double none) {
+    double v;
+    memcpy(&v, &b, sizeof(v));
+    return std::isinf(v) ? none : v;
+  };
+  out->sparsity_V = (double)stp[3] / (double)(h.J * h.R);
+  for (int i = 0; i < 3; ++i) out->inner_steps[i] = (int64_t)stp[i];
+  out->polar_near = (int64_t)dg[D_POLAR_NEAR];
+  out->polar_min_kept = ratio(dg[D_POLAR_KEPT], 1.0);
+  out->polar_max_dropped = ratio(dg[D_POLAR_DROP], 0.0);
+  out->basis_near = (int64_t)dg[D_BASIS_NEAR];
+  out->basis_min_kept = ratio(dg[D_BASIS_KEPT], 1.0);
+  out->basis_max_dropped = ratio(dg[D_BASIS_DROP], 0.0);
   return COPA_OK;
 }
 

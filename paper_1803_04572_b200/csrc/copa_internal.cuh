@@ -2,6 +2,7 @@
 // Product path (CUDA, sm_100a, FP64). Shares no code with oracle/ (see DESIGN.md §1).
 #pragma once
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdint.h>
 
 #include <vector>
@@ -11,16 +12,21 @@
 namespace copa {
 
 constexpr int kMaxR = 64;       // rank limit (local arrays in the per-patient kernels)
-constexpr int kMaxQ = 16;       // q = min(m_k, R) limit of the thread-per-patient polar
 constexpr int kMaxL = 16;       // smooth_l limit
 constexpr int kMaxDeg = 7;      // spline degree limit
 constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
 constexpr int kPhases = 11;       // timed phases of one outer iteration (copa_get_phase_times)
 constexpr int kMaxGroups = 8;     // label groups (fiber streams) of the smooth path
-constexpr int kWoS = 16;          // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
+constexpr int kWoS = 16;
+constexpr int64_t kCscChunk = 512;  // entries per chunk of the non-smooth F_V gather          // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
 
 enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
+
+// Rank-cut diagnostics (copa_stats; SURVEY 8(c) parity protocol): counts, and ratios as the bit
+// patterns of non-negative doubles (ordered like unsigned integers).
+enum DiagSlot : int { D_POLAR_NEAR = 0, D_POLAR_KEPT, D_POLAR_DROP, D_BASIS_NEAR, D_BASIS_KEPT, D_BASIS_DROP,
+                      kDiagSlots = 8 };
 
 // Scalar slots in Handle::scal
 enum Scal : int { S_NORMX = 0, S_RHO_H, S_RHO_W, S_RHO_V, S_FIT, S_CROSS, S_QUAD, S_E, S_COUNT = 16 };
@@ -29,6 +35,8 @@ struct Handle {
   copa_problem p;      // device pointers of the CSR input
   copa_options o;
   cudaStream_t stream;
+  int dev = 0;         // CUDA device of the handle (current device at init)
+  int sms = 148;       // its multiprocessor count (queried)
   int smooth;          // smooth_l > 0
   int l, d;            // basis size / degree (smooth)
   int64_t K, J, rows, nnz;
@@ -64,9 +72,6 @@ struct Handle {
   int64_t pa_nw = 0;
   int pa_ctas = 0;
   bool pa_vs = false;    // V̄ in shared memory in pass A
-  int pa_nhot = 0;       // else: rows of the pa_nhot heaviest labels staged in shared memory
-  int32_t* hot_slot;     // [Jl] label -> hot slot or -1
-  int32_t* hot_lab;      // [pa_nhot] hot slot -> label
   int64_t* block_k;      // [sc_ranges+1] patient range of each pass-B range
   double* fv_part;       // [sc_ranges x Jl x R] per-range F_V partials
   unsigned long long* fhist;  // [J] fibers per feature (init)
@@ -83,10 +88,22 @@ struct Handle {
   void* layout_tmp;
   size_t layout_tmp_bytes = 0;
   int32_t* row_patient;  // non-smooth: [rows]
+  // non-smooth: feature-major (CSC) copy of X for the deterministic F_V gather (k_plain.cu)
+  int64_t* csc_ptr;          // [J+1]
+  int32_t* csc_row;          // [nnz] row of each entry, column order
+  double* csc_val;           // [nnz]
+  int64_t* csc_chunk;        // [2 x cap] entry range of each gather chunk (one column per chunk)
+  int64_t* csc_chunk_first;  // [J+1] first chunk of each column
+  double* csc_part;          // [cap x R] chunk partials
+  void* csc_tmp;             // init-only scratch of the sort
+  size_t csc_tmp_bytes = 0;
+  int64_t csc_chunks = 0, csc_chunk_cap = 0;
   void* cub_temp;
   size_t cub_temp_bytes;
   int64_t* counts_scratch;
   double* fit_ring;    // device ring of per-iteration FIT values
+  unsigned long long* diag;   // [kDiagSlots] rank-cut diagnostics (see DiagSlot)
+  unsigned long long* steps;  // [4] inner ADMM steps of the H, W, V modes (last iteration) + zero count
   int own_inputs;      // copa_fit: CSR copied into the workspace
   // phase profiling (copa_set_profiling)
   bool profiling = false;
@@ -202,6 +219,68 @@ __device__ __forceinline__ int spline_eval(double t, double t1, double tn, int l
 
 __device__ __forceinline__ void set_err(int* err, int bit) { atomicOr(err, bit); }
 
+// Summary of one patient's singular-value ratios sigma_j / sigma_1 against a rank cut tau:
+// smallest kept ratio (+inf if none), largest dropped ratio (0 if none), any ratio within a factor
+// 100 of tau. ratio_note() folds one ratio in.
+struct RatioDiag {
+  double min_kept = INFINITY;
+  double max_drop = 0.0;
+  int near = 0;
+  __device__ __forceinline__ void note(double ratio, bool kept, double tau) {
+    if (kept) min_kept = fmin(min_kept, ratio);
+    else max_drop = fmax(max_drop, ratio);
+    if (tau > 0.0 && ratio >= 0.01 * tau && ratio <= 100.0 * tau) near = 1;
+  }
+};
+// Accumulate into diag[base + 0..2]: one atomic set per call.
+__device__ __forceinline__ void ratio_diag_commit(unsigned long long* diag, int base, const RatioDiag& d) {
+  if (d.near) atomicAdd(diag + base, (unsigned long long)d.near);
+  atomicMin(diag + base + 1, (unsigned long long)__double_as_longlong(d.min_kept));
+  atomicMax(diag + base + 2, (unsigned long long)__double_as_longlong(d.max_drop));
+}
+// Warp-collective version (all 32 lanes call it; lanes with nothing to report pass a default RatioDiag).
+__device__ __forceinline__ void ratio_diag_warp(unsigned long long* diag, int base, RatioDiag d) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d.min_kept = fmin(d.min_kept, __shfl_xor_sync(0xffffffffu, d.min_kept, o));
+    d.max_drop = fmax(d.max_drop, __shfl_xor_sync(0xffffffffu, d.max_drop, o));
+    d.near += __shfl_xor_sync(0xffffffffu, d.near, o);
+  }
+  if ((threadIdx.x & 31) == 0) ratio_diag_commit(diag, base, d);
+}
+
+// Inner-step counter of one ADMM row batch: warp sum, one atomic per warp (all lanes call it).
+__device__ __forceinline__ void steps_warp(unsigned long long* counter, int steps) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) steps += __shfl_xor_sync(0xffffffffu, steps, o);
+  if ((threadIdx.x & 31) == 0 && steps) atomicAdd(counter, (unsigned long long)steps);
+}
+
+// Per-row inner stop of reading R-inner-tol, accumulated like the oracle (no FMA contraction):
+// pr += (zb - z)^2, du += (zb - zb_prev)^2, nz += zb^2; stop when max(pr, du) <= tol^2 nz.
+struct RowResid {
+  double pr = 0.0, du = 0.0, nz = 0.0;
+  __device__ __forceinline__ void add(double zb_new, double z, double zb_prev) {
+    const double e = __dsub_rn(zb_new, z), dz = __dsub_rn(zb_new, zb_prev);
+    pr = __dadd_rn(pr, __dmul_rn(e, e));
+    du = __dadd_rn(du, __dmul_rn(dz, dz));
+    nz = __dadd_rn(nz, __dmul_rn(zb_new, zb_new));
+  }
+  __device__ __forceinline__ bool done(double tol) const {
+    return tol > 0.0 && fmax(pr, du) <= __dmul_rn(__dmul_rn(tol, tol), nz);
+  }
+};
+
+// Opt a kernel into the full 227 KB of dynamic shared memory, once per (kernel, device).
+template <auto Fn>
+inline void max_smem_attr(const Handle& h, int bytes = 227 * 1024) {
+  static unsigned long long done = 0;  // bit per device ordinal (< 64)
+  const unsigned long long bit = 1ull << (h.dev & 63);
+  if (__atomic_load_n(&done, __ATOMIC_ACQUIRE) & bit) return;
+  cudaFuncSetAttribute(Fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  __atomic_fetch_or(&done, bit, __ATOMIC_ACQ_REL);
+}
+
 // ------------------------------------------------------------------ launchers
 // init
 void launch_validate(Handle& h);
@@ -213,24 +292,22 @@ void launch_row_patient(Handle& h);
 void launch_sumsq(Handle& h, double* out);
 // iteration
 int launch_spmm(Handle& h);
-int launch_polar(Handle& h);
 int launch_fh(Handle& h);
 int launch_admm_H(Handle& h);
-int launch_passB1(Handle& h);
 int launch_scatter(Handle& h);
 int launch_admm_V(Handle& h);
 int launch_fit(Handle& h);
+void launch_count_zeros(Handle& h);  // zero entries of V̄ -> steps[3]
 // reductions: C (R x R) = sum_s A(s,:)^T (B(s,:) * w(s,:)); wsrc: 0 none, 1 W rows by patient of s
 int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C);
-void launch_U(Handle& h, double* U);
+// U rows of patients [k0, k1) into U (row i of the shard at U[(i - prp[k0]) R])
+void launch_U(Handle& h, double* U, int64_t k0, int64_t k1);
 // fiber passes (k_fibers.cu)
 void launch_spmm_fibers(Handle& h);   // pass A (k_passA.cu)
 void launch_relabel_V(Handle& h);
 void launch_layoutA(Handle& h);
 void plan_passA(Handle& h);
 void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
-void plan_passA_hot(const Handle& h, const unsigned long long* hist, const int32_t* inv, std::vector<int32_t>& slot,
-                    std::vector<int32_t>& lab);
 int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
@@ -241,6 +318,12 @@ void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::
                   std::vector<int32_t>& st_k, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k);
 // wide per-patient dense kernels (k_dense.cu)
 bool polar_wide_ok(const Handle& h);
+// general path (k_plain.cu)
+int launch_polar_warp(Handle& h);
+int launch_passB_warp(Handle& h);
+size_t csc_temp_bytes(const Handle& h);
+int build_csc(Handle& h);  // 0 ok, -1 CUDA error, -2 chunk table overflow
+int launch_scatter_csc(Handle& h);
 int launch_polar_wide(Handle& h);
 int launch_passB_wide(Handle& h);
 

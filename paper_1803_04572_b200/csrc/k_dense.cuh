@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
                                                        const double* __restrict__ Pp, const double* __restrict__ W,
                                                        const double* __restrict__ Hg, double tau,
                                                        double* __restrict__ Qt, int32_t* __restrict__ rank,
-                                                       double* __restrict__ FHwarp, int nextpf) {
+                                                       double* __restrict__ FHwarp, int nextpf,
+                                                       unsigned long long* __restrict__ diag) {
   constexpr int KS = RT ? (RT + 3) / 4 : (NT * 8 + 3) / 4;  // r steps of 4 covering R (an all-zero step
                                                              // costs a DMMA like any other)
   // fixed-shape slab path: unmasked fragment loads (needs l >= 7, one M tile, R % 4 == 0; see a_slab)
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
     }
     smax = sqrt(smax);
     int rk = 0;
+    RatioDiag dg;  // rank-cut diagnostics (copa_stats)
 #pragma unroll
     for (int j = 0; j < L; ++j) {
       double s = 0.0;
@@ -404,12 +406,14 @@ __global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict
       for (int i = 0; i < L; ++i) s = fma(Rf[j][i], Rf[j][i], s);
       const double sg = sqrt(s);
       const bool keep = smax > 0.0 && sg > tau * smax;
+      if (smax > 0.0 && j < mme) dg.note(sg / smax, keep, tau);
       rk += keep ? 1 : 0;
       const double sc = keep ? 1.0 / (sg * sqrt(sg)) : 0.0;
 #pragma unroll
       for (int i = 0; i < L; ++i) Rf[j][i] *= sc;
     }
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
+    ratio_diag_warp(diag, D_POLAR_NEAR, dg);
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
     for (int nt = 0; nt < NT; ++nt) {
       a_slab<MT, KS, BULK, SR, FAST>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
@@ -557,7 +561,7 @@ constexpr int kDenseThreads = 128;
 template <int L, int NT, int RT = 0, int LT = 0>
 static void polar_wide_inst(Handle& h) {
   constexpr int MT = (L + 7) / 8;
-  auto fn = k_polar_wide<L, MT, NT, RT, LT>;
+  constexpr auto fn = k_polar_wide<L, MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
   constexpr int SR = LT ? LT : MT * 8;
   const size_t slabd = (size_t)std::max(32 * SR * 8, kRing * (2 * h.l * h.R + h.R));
@@ -566,22 +570,17 @@ static void polar_wide_inst(Handle& h) {
   while (wpb > 1 && sizeof(double) * (hoff + wpb * per_warp) > 227 * 1024) wpb /= 2;
   const int threads = 32 * wpb;
   size_t smem = sizeof(double) * (hoff + wpb * per_warp);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  max_smem_attr<fn>(h);
   int64_t rounds = (h.K + 31) / 32;
   int64_t blocks = (rounds + wpb - 1) / wpb;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
-  if (const char* e = getenv("COPA_POLAR_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
-  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  int64_t cap = h.sms * (int64_t)(per_sm > 0 ? per_sm : 1);
   if (cap > kPartBlocks * 4 / wpb) cap = kPartBlocks * 4 / wpb;  // fh_warp holds kPartBlocks x 4 warps
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, threads, smem, h.stream>>>(h.m, h.K, h.R, h.l, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
-                                                    h.fh_warp, getenv("COPA_NEXT_PF") ? 1 : 0);
+                                                    h.fh_warp, 0, h.diag);
   const int RR = h.R * h.R;
   const int P = 64 * NT * NT;
   k_sum_fh1<<<dim3((P + 127) / 128, kFhChunks), 128, 0, h.stream>>>(h.fh_warp, (int)blocks * wpb, P, h.partial);
@@ -617,10 +616,11 @@ template <int MT, int NT, int RT, int LT>
 __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, const double* __restrict__ Pp,
                                                     const double* __restrict__ Qt, const double* __restrict__ Hg,
                                                     const double* __restrict__ GWi, const double* __restrict__ scal,
-                                                    int n_inner, int kind, double param, double* __restrict__ W,
-                                                    double* __restrict__ DW, double* __restrict__ Nst,
+                                                    int n_inner, int kind, double param, double tol,
+                                                    double* __restrict__ W, double* __restrict__ DW,
+                                                    double* __restrict__ Nst,
                                                     double* __restrict__ part /* [blocks][2][R R] */,
-                                                    int getenv_l1, int nextpf) {
+                                                    int l1_prefetch, int nextpf, unsigned long long* __restrict__ steps) {
   constexpr int RP = 8 * NT;
   constexpr int KS = RT ? (RT + 3) / 4 : (NT * 8 + 3) / 4;  // i steps of 4 covering R
   const int R = RT ? RT : R_;
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
     const int64_t base = rd * 32;
     const int np = (int)(K - base < 32 ? K - base : 32);
     {  // this round's rows into L1 (measured better than L2-only), the next round's into L2
-      const bool l1 = getenv_l1;
+      const bool l1 = l1_prefetch;
       if (l1) {
         warp_prefetch(Pp + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
         warp_prefetch(Qt + base * pstride, sizeof(double) * (size_t)(np * pstride), true);
@@ -746,9 +746,11 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
     __syncwarp();
     // ---- W-row ADMM (thread = patient)
     const int64_t kme = base + lane;
+    int nsteps = 0;
     if (kme < K) {
       for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
-      for (int it = 0; it < n_inner; ++it) {
+      while (nsteps < n_inner) {
+        RowResid res;  // per-row inner stop (reading R-inner-tol)
         double rhs[RP];
 #pragma unroll
         for (int r = 0; r < RP; ++r)
@@ -762,15 +764,19 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
               if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
             const double d0 = dv[r * 32 + lane];
             const double nb = prox(kind, param, rho, z - d0);
+            res.add(nb, z, wbv[r * 32 + lane]);
             dv[r * 32 + lane] = d0 + nb - z;
             wbv[r * 32 + lane] = nb;
           }
         }
+        ++nsteps;
+        if (res.done(tol)) break;
       }
       for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
     } else {
       for (int r = 0; r < R; ++r) wbv[r * 32 + lane] = 0.0;
     }
+    steps_warp(steps + 1, nsteps);
     __syncwarp();
     // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T  (MMA with K = patients)
 #pragma unroll
@@ -863,29 +869,23 @@ static __global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, 
 template <int MT, int NT, int RT = 0, int LT = 0>
 static void passB_wide_inst(Handle& h) {
   constexpr int RP = 8 * NT;
-  auto fn = k_passB_wide<MT, NT, RT, LT>;
+  constexpr auto fn = k_passB_wide<MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
   size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32 + MT * 8 * RP);
   size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
   size_t smem = sizeof(double) * 2 * hoff + (per_warp * (kDenseThreads / 32) > red ? per_warp * (kDenseThreads / 32) : red);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  max_smem_attr<fn>(h);
   int64_t rounds = (h.K + 31) / 32;
   int64_t blocks = (rounds + 3) / 4;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kDenseThreads, smem);
-  if (const char* e = getenv("COPA_PASSB_BPS")) per_sm = atoi(e) < per_sm ? atoi(e) : per_sm;
-  int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+  int64_t cap = h.sms * (int64_t)(per_sm > 0 ? per_sm : 1);
   if (cap > kPartBlocks) cap = kPartBlocks;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   fn<<<(unsigned)blocks, kDenseThreads, smem, h.stream>>>(h.K, h.R, h.l, h.Pp, h.Qt, h.H, h.GWi, h.scal,
-                                                         h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W, h.DW,
-                                                         h.Nst, h.partial, getenv("COPA_PASSB_NOL1") ? 0 : 1,
-                                                         getenv("COPA_NEXT_PF") ? 1 : 0);
+                                                         h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param,
+                                                         h.o.admm_tol, h.W, h.DW, h.Nst, h.partial, 1, 0, h.steps);
   const int RR = h.R * h.R;
   k_sum_rr2<<<(2 * RR + 255) / 256, 256, 0, h.stream>>>(h.partial, (int)blocks, RR, h.M, h.WtW);
 }

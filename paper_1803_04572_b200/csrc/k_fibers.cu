@@ -61,20 +61,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Producer-side wait: the producer shares an SM sub-partition with a consumer warp, so it backs off
-// with nanosleep instead of spinning on try_wait (a tight spin takes issue slots from that consumer).
-__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n .reg .pred P1;\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n selp.u32 %0, 1, 0, P1;\n}"
-      : "=r"(ok)
-      : "r"(smem_u32(b)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, unsigned ns) {
-  while (!mbar_try(b, parity)) __nanosleep(ns);
-}
 // try_wait with a suspend-time hint: the thread is parked until the phase completes (or the hint
 // expires), without issuing instructions in between.
 __device__ __forceinline__ void mbar_wait_park(uint64_t* b, uint32_t parity, uint32_t hint_ns) {
@@ -149,17 +135,15 @@ __host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
 
 constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
 
-constexpr int kPfFibers = 4096;   // pass-B L2 prefetch distance (fibers) ahead of the ring
-constexpr int kPfPatients = 64;   // and patients (N rows)
 
-// PRED: predicated F_V row updates (invalid lanes issue no shared-memory access; measured slower,
-// opt-in COPA_SC_PRED); default: invalid lanes are redirected to a per-lane scratch slot.
-template <int KS, int NT, int W, int TB, int LT, int RT, bool PRED = false>
+// F_V row updates are branch-free: invalid lanes are redirected to a per-lane scratch slot
+// (predicated updates measured slower: 26.6-27.1 vs 24.4 ms at Scale).
+template <int KS, int NT, int W, int TB, int LT, int RT>
 __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
     int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
     const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l_, int R_, int RS_, int FB, int PB,
-    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart, int dbg, int pf_scale, unsigned psleep) {
+    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart) {
   const int R = RT ? RT : R_;           // compile-time for the configured (R, l) shapes
   const int l = LT ? LT : l_;
   const int RS = RT ? ((RT + 1) & ~1) : RS_;
@@ -199,41 +183,16 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         nf0 = st_f[2 * (int64_t)s0]; nf1 = st_f[2 * (int64_t)s0 + 1];
         nk0 = st_k[2 * (int64_t)s0]; nk1 = st_k[2 * (int64_t)s0 + 1];
       }
-      // L2 prefetch frontier: fibers and N rows up to kPfFibers / kPfPatients beyond the stage
-      // being issued, so the bulk copies mostly hit L2 (the ring itself is only NS stages deep)
-      int64_t pf_f = nf0, pf_k = nk0, end_f = 0, end_k = 0;
-      if (ns > 0) {
-        end_f = st_f[2 * (int64_t)(s0 + ns - 1) + 1];
-        end_k = st_k[2 * (int64_t)(s0 + ns - 1) + 1];
-      }
       int slot = 0, phase = 1;  // the producer's first pass over the ring does not wait
       for (int i = 0; i < ns; ++i) {
         const int64_t f0 = nf0, f1 = nf1;
         const int32_t k0 = nk0, k1 = nk1;
-        {
-          const int64_t ft = min(f1 + (int64_t)(pf_scale * kPfFibers), end_f);
-          while (pf_f < ft) {
-            const int64_t n = min((int64_t)1024, ft - pf_f);
-            l2_prefetch(fiber_col + pf_f, 4ull * n);
-            l2_prefetch(fiber_val + pf_f * l, 8ull * n * l);
-            pf_f += n;
-          }
-          const int64_t kt = min((int64_t)k1 + (int64_t)(pf_scale * kPfPatients), end_k);
-          while (pf_k < kt) {
-            const int64_t n = min((int64_t)16, kt - pf_k);
-            l2_prefetch(Nst + pf_k * l * R, 8ull * n * l * R);
-            l2_prefetch(gptr + grp * K1 + pf_k, 8ull * (n + 1));
-            pf_k += n;
-          }
-        }
         if (i + 1 < ns) {
           const int64_t st = s0 + i + 1;
           nf0 = st_f[2 * st]; nf1 = st_f[2 * st + 1];
           nk0 = st_k[2 * st]; nk1 = st_k[2 * st + 1];
         }
-        if (psleep >= 1000000u) mbar_wait_park(empty + slot, phase, psleep);
-        else if (psleep) mbar_wait_sleep(empty + slot, phase, psleep);
-        else mbar_wait(empty + slot, phase);
+        mbar_wait_park(empty + slot, phase, 1000000u);  // parked, no issue slots taken from consumers
         unsigned char* base = slots + (size_t)slot * sg.bytes;
         int64_t* meta = (int64_t*)base;
         int32_t* mi = (int32_t*)(base + 16);
@@ -254,11 +213,6 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         // expected bytes first (same rounding as bulk_g2s_span), then the copies
         const uint32_t tx = al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn) +
                             al16((sp & 15) + bp) + al16((sw & 15) + bw);
-        if (dbg == 2) {  // timing experiment: no copies
-          mbar_arrive(full + slot);
-          if (++slot == NSt) { slot = 0; phase ^= 1; }
-          continue;
-        }
         mbar_arrive_tx(full + slot, tx);
         uint32_t t2 = 0;
         bulk_g2s_span(base + sg.gp, (const void*)sp, bp, full + slot, &t2);
@@ -302,7 +256,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
       const double* nS = smD + ((sb + sg.nrows + mi[4]) >> 3);
       // per-patient setup (sub-run bounds, B fragments B[t][g] = N(a = 4 ks + t, r = 8 nt + g)) is
       // loaded one patient ahead, off the critical path of the current patient's tiles
-      const int npat = dbg == 1 ? 0 : k1 - k0;
+      const int npat = k1 - k0;
       auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NT]) {
         const int64_t rs = gp[p];
         lo_ = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
@@ -361,13 +315,8 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
               const bool ok = col[b] >= 0 && 8 * nt + 2 * t < R;
-              if (PRED) {  // predicated: invalid lanes issue no shared-memory wavefront
-                idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : -1;
-                v[b][nt] = ok ? *reinterpret_cast<const double2*>(Fs + idx[b][nt]) : make_double2(0.0, 0.0);
-              } else {
-                idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
-                v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
-              }
+              idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
+              v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
             }
 #pragma unroll
           for (int b = 0; b < NB; ++b)
@@ -375,7 +324,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             for (int nt = 0; nt < NT; ++nt) {
               v[b][nt].x += cc[b][nt][0];
               v[b][nt].y += cc[b][nt][1];
-              if (!PRED || idx[b][nt] >= 0) *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
+              *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
             }
         };
         int tb = lo;
@@ -412,21 +361,14 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0, bool PRED = false>
+template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0>
 static void scatter_inst_w(Handle& h) {
-  auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT, PRED>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  constexpr auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT>;
+  max_smem_attr<fn>(h);
   const int ctas = h.sc_ranges * h.sc_G;
   fn<<<ctas, 32 * (W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js, h.sc_Jg,
                                                    h.st_f, h.st_k, h.cta_st, h.woff, h.l, h.R, h.sc_RS, h.sc_FB,
-                                                   h.sc_PB, h.sc_NS, h.Nst, h.fv_part,
-                                                   getenv("COPA_SC_DBG") ? atoi(getenv("COPA_SC_DBG")) : 0,
-                                                   getenv("COPA_SC_PF") ? atoi(getenv("COPA_SC_PF")) : 0,  // L2 frontier: off (no gain, +15 GB DRAM)
-                                                   getenv("COPA_SC_SLEEP") ? (unsigned)atoi(getenv("COPA_SC_SLEEP")) : 1000000u);  // >= 1e6: parked try_wait (26.47 vs 26.60 ms)
+                                                   h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
@@ -441,10 +383,7 @@ template <int KS>
 static void scatter_dispatch_n(Handle& h) {
   if (h.sc_W == 4) {
     if (KS == 2 && h.l == 7 && h.R == 20) {
-      if (getenv("COPA_SC_TB4")) scatter_inst_w<2, 3, 4, 4, 7, 20>(h);        // tile-batch experiments
-      else if (getenv("COPA_SC_TB2")) scatter_inst_w<2, 3, 4, 2, 7, 20>(h);   // (TB3: 26.8 vs 27.2 ms)
-      else if (getenv("COPA_SC_PRED")) scatter_inst_w<2, 3, 4, 3, 7, 20, true>(h);  // 26.6-27.1 vs 24.4 ms
-      else scatter_inst_w<2, 3, 4, 3, 7, 20>(h);
+      scatter_inst_w<2, 3, 4, 3, 7, 20>(h);  // 3-tile batches (TB 2/4 measured slower)
       return;
     }
     if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 2, 7, 15>(h); return; }
@@ -477,13 +416,11 @@ int launch_scatter_fibers(Handle& h) {
 void plan_scatter(Handle& h) {
   const size_t budget = 225 * 1024;
   h.sc_W = kScW;  // label sub-ranges per group = consumer warps of k_scatter_tma (2 or 4)
-  if (getenv("COPA_SC_W")) h.sc_W = atoi(getenv("COPA_SC_W")) == 2 ? 2 : 4;
   h.sc_RS = (h.R + 1) & ~1;
   h.sc_FB = 256;
   h.sc_ok = 0;
   const int pbs[3] = {16, 8, 4};
-  const int gmin = getenv("COPA_SC_GMIN") ? atoi(getenv("COPA_SC_GMIN")) : 1;  // tuning experiments
-  if (getenv("COPA_SC_FB")) h.sc_FB = atoi(getenv("COPA_SC_FB"));
+  const int gmin = 1;
   for (int pass = 0; pass < 2 && !h.sc_ok; ++pass)  // pass 0: >= 3 stages of >= 8 patients
     for (int G = gmin; G <= kMaxGroups && !h.sc_ok; ++G) {
       const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
@@ -507,7 +444,7 @@ void plan_scatter(Handle& h) {
     }
   // Larger stages (FB = 512: fewer per-stage overheads; measured 43 -> 40 ms at Scale, 2.26 -> 2.10 ms
   // at Medium) when they still fit at the same G with >= 3 slots of >= 8 patients.
-  if (h.sc_ok && !getenv("COPA_SC_FB")) {
+  if (h.sc_ok) {
     const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + (size_t)h.sc_W * 512 + 127) & ~(size_t)127;
     bool done = false;
     for (int NSt = 4; NSt >= 3 && !done; --NSt)
@@ -532,8 +469,7 @@ void plan_scatter(Handle& h) {
   h.Jl = (int64_t)h.sc_G * h.sc_Jg;
   int bps = h.sc_ok ? (int)((228 * 1024) / (h.sc_smem + 1024)) : 1;
   if (bps < 1) bps = 1;
-  const int waves = getenv("COPA_SC_WAVES") ? std::max(1, atoi(getenv("COPA_SC_WAVES"))) : 1;
-  int64_t ranges = (148 * (int64_t)bps * waves + h.sc_G - 1) / h.sc_G;
+  int64_t ranges = (h.sms * (int64_t)bps + h.sc_G - 1) / h.sc_G;
   if (ranges > h.K) ranges = h.K > 0 ? h.K : 1;
   h.sc_ranges = (int)ranges;
 }

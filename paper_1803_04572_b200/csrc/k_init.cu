@@ -53,8 +53,11 @@ void launch_validate(Handle& h) {
 // ------------------------------------------------------------------ fibers: count
 // Warp per patient; each warp owns a J-bit bitmap in shared memory. Also accumulates the number of
 // fibers per feature (hist, optional) used to relabel features into balanced ranges.
+// Runs before validation (copa_workspace_size sizes the workspace from it): every index is
+// bounds-checked so malformed input yields some count (rejected later by k_validate_*), never an
+// out-of-range access.
 __global__ void k_count_fibers(const int64_t* prp, const int64_t* rp, const int32_t* col, int64_t K, int words,
-                               int64_t* counts, unsigned long long* hist, int64_t J) {
+                               int64_t* counts, unsigned long long* hist, int64_t J, int64_t rows, int64_t nnz) {
   extern __shared__ unsigned smem_bits[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned* bits = smem_bits + wib * words;
@@ -66,10 +69,16 @@ __global__ void k_count_fibers(const int64_t* prp, const int64_t* rp, const int3
   for (int64_t k = blockIdx.x * (int64_t)nw + wib; k < K; k += nwarps) {
     for (int w = lane; w < words; w += 32) bits[w] = 0u;
     __syncwarp();
-    int64_t e0 = rp[prp[k]], e1 = rp[prp[k + 1]];
+    const int64_t a = prp[k], b = prp[k + 1];
+    int64_t e0 = 0, e1 = 0;
+    if (a >= 0 && b >= a && b <= rows) {
+      e0 = rp[a];
+      e1 = rp[b];
+      if (e0 < 0 || e1 < e0 || e1 > nnz) e0 = e1 = 0;
+    }
     for (int64_t e = e0 + lane; e < e1; e += 32) {
       int32_t j = col[e];
-      atomicOr(&bits[j >> 5], 1u << (j & 31));
+      if (j >= 0 && j < J) atomicOr(&bits[j >> 5], 1u << (j & 31));
     }
     __syncwarp();
     int c = 0;
@@ -101,15 +110,11 @@ void launch_count_fibers(Handle& h, int64_t* counts, unsigned long long* hist) {
   cudaMemsetAsync(counts, 0, sizeof(int64_t), h.stream);
   if (hist) cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * (size_t)h.J, h.stream);
   if (h.K == 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_count_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  max_smem_attr<k_count_fibers>(h, 200 * 1024);
   int64_t blocks = (h.K + warps - 1) / warps;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > h.sms * 16) blocks = h.sms * 16;
   k_count_fibers<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.K,
-                                                                    words, counts, hist, h.J);
+                                                                    words, counts, hist, h.J, h.rows, h.nnz);
 }
 
 // ------------------------------------------------------------------ basis (thread per patient)
@@ -117,7 +122,7 @@ void launch_count_fibers(Handle& h, int64_t* counts, unsigned long long* hist) {
 // rows of Rm gives sigma_j v_j; B_k column c (kept j) = v_j / sigma_j, so C_k = M_k B_k are the
 // left singular vectors of M_k with sigma_j > tau * sigma_max (reading R-spline-4).
 __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int l, int d, double tau, double* Bk,
-                        int32_t* m) {
+                        int32_t* m, unsigned long long* diag) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
   double Rm[kMaxL * kMaxL];
@@ -146,6 +151,11 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
     sig[j] = sqrt(s);
     smax = fmax(smax, sig[j]);
   }
+  if (smax > 0.0) {  // rank-cut diagnostics (copa_stats)
+    RatioDiag dg;
+    for (int j = 0; j < l; ++j) dg.note(sig[j] / smax, sig[j] > tau * smax, tau);
+    ratio_diag_commit(diag, D_BASIS_NEAR, dg);
+  }
   // keep in descending sigma order (stable): selection by repeated max
   int used[kMaxL];
   for (int j = 0; j < l; ++j) used[j] = 0;
@@ -170,7 +180,7 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
 // descending sigma (stable) — the order the selection loop above produces.
 template <int L>
 __global__ void __launch_bounds__(64) k_basis_reg(const int64_t* prp, const double* times, int64_t K, int d,
-                                                  double tau, double* Bk, int32_t* m) {
+                                                  double tau, double* Bk, int32_t* m, unsigned long long* diag) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool live = k < K;
   int64_t r0 = 0, r1 = 0;
@@ -199,8 +209,6 @@ __global__ void __launch_bounds__(64) k_basis_reg(const int64_t* prp, const doub
     givens_insert_reg<L>(Rm, a);
   }
   jacobi_rows_reg<L>(Rm);  // warp-collective convergence vote: every lane takes part
-  if (!live) return;
-  double* B = Bk + k * (int64_t)L * L;
   double sig[L], smax = 0.0;
 #pragma unroll
   for (int j = 0; j < L; ++j) {
@@ -210,6 +218,15 @@ __global__ void __launch_bounds__(64) k_basis_reg(const int64_t* prp, const doub
     sig[j] = sqrt(s);
     smax = fmax(smax, sig[j]);
   }
+  {  // rank-cut diagnostics (copa_stats), warp-collective
+    RatioDiag dg;
+    if (active && smax > 0.0)
+#pragma unroll
+      for (int j = 0; j < L; ++j) dg.note(sig[j] / smax, sig[j] > tau * smax, tau);
+    ratio_diag_warp(diag, D_BASIS_NEAR, dg);
+  }
+  if (!live) return;
+  double* B = Bk + k * (int64_t)L * L;
   int c = 0;
 #pragma unroll
   for (int j = 0; j < L; ++j) {
@@ -236,14 +253,14 @@ void launch_basis(Handle& h) {
   if (h.K == 0) return;
   const unsigned blocks = (unsigned)((h.K + 63) / 64);
   if (h.l == 7) {
-    k_basis_reg<7><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m);
+    k_basis_reg<7><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m, h.diag);
     return;
   }
   if (h.l == 9) {
-    k_basis_reg<9><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m);
+    k_basis_reg<9><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m, h.diag);
     return;
   }
-  k_basis<<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.l, h.d, h.o.basis_tol, h.Bk, h.m);
+  k_basis<<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.l, h.d, h.o.basis_tol, h.Bk, h.m, h.diag);
 }
 
 // ------------------------------------------------------------------ fibers: per-group counts
@@ -315,13 +332,9 @@ void launch_count_groups(Handle& h, int32_t* gcnt) {
   const int words = (int)((h.Jl + 31) / 32);
   const int warps = 8;
   const size_t smem = (size_t)warps * words * (sizeof(unsigned) + sizeof(int));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_count_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  max_smem_attr<k_count_groups>(h, 200 * 1024);
   int64_t blocks = (h.K + warps - 1) / warps;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > h.sms * 16) blocks = h.sms * 16;
   k_count_groups<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.perm,
                                                                     h.K, words, h.sc_G, h.sc_Jg, h.sc_W, h.sc_Js, gcnt,
                                                                     h.woff);
@@ -459,13 +472,9 @@ void launch_build_fibers(Handle& h) {
   if (h.K == 0) return;
   const int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
   const size_t smem = (size_t)kBfWarps * bf_warp_doubles(h.l, words) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_build_fibers, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  max_smem_attr<k_build_fibers>(h);
   int64_t blocks = (h.K + kBfWarps - 1) / kBfWarps;
-  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks > h.sms * 32) blocks = h.sms * 32;
   k_build_fibers<<<(unsigned)blocks, kBfWarps * 32, smem, h.stream>>>(
       h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m, h.gptr,
       h.sc_G, (int)h.sc_Jg, h.perm, h.fiber_col, h.fiber_val);

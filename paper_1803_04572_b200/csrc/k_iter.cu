@@ -8,6 +8,8 @@
 //          scatter F_V = sum_k X'_k^T N_k         (= Y_(2)(W ⊙ H))                        -> C2
 // V-ADMM   admm_V  G_V, rho_V, chol, n_inner steps per row of V̄
 // FIT      fit     E = normX - 2<F_V, V̄> + <sum_k N_k^T N_k, V̄^T V̄>
+#include <algorithm>
+
 #include "copa_internal.cuh"
 
 namespace copa {
@@ -38,111 +40,6 @@ int launch_spmm(Handle& h) {
     k_spmm_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R, h.V,
                                                                    h.Pp);
   }
-  return 1;
-}
-
-// ------------------------------------------------------------------ pass A: polar (thread per patient)
-// A_k = P'_k S_k H̄^T (m x R). Tall (m >= R): Givens-QR of the rows of A into Rf (R x R).
-// Wide (m < R): Givens-QR of the rows of A^T (= columns of A) into Rf (m x m).
-// One-sided Jacobi on the rows of Rf -> rows sigma_j v_j, v_j right singular vectors of the
-// tall side T. K = sum_{sigma_j > tau sigma_max} v_j v_j^T / sigma_j  (= (T^T T)^{-1/2} on the range);
-// polar(T) = T K, so Q~ = A K (tall) or K A (wide): the partial isometry U_r V_r^T (reading R-polar-2).
-__global__ void __launch_bounds__(64) k_polar(const int32_t* m, const int64_t* srow, int64_t K, int R,
-                                              const double* Pp, const double* W, const double* Hg, double tau,
-                                              double* Qt, int32_t* rank) {
-  __shared__ double Hs[kMaxR * kMaxR];
-  for (int i = threadIdx.x; i < R * R; i += blockDim.x) Hs[i] = Hg[i];
-  __syncthreads();
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const int mk = m[k];
-  if (mk == 0) { rank[k] = 0; return; }
-  const double* P = Pp + srow[k] * R;
-  double* Q = Qt + srow[k] * R;
-  double w[kMaxR];
-  for (int r = 0; r < R; ++r) w[r] = W[k * R + r];
-  const int tall = mk >= R;
-  const int q = tall ? R : mk;
-  double Rf[kMaxQ * kMaxQ];
-  for (int i = 0; i < q * kMaxQ; ++i) Rf[i] = 0.0;
-  double a[kMaxR];
-  double A[kMaxQ * kMaxR];  // wide case only: A (mk x R)
-  if (tall) {
-    for (int i = 0; i < mk; ++i) {
-      double pw[kMaxR];
-      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
-      for (int s = 0; s < R; ++s) {
-        double acc = 0.0;
-        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
-        a[s] = acc;
-      }
-      givens_insert(Rf, kMaxQ, a, R);
-    }
-  } else {
-    for (int i = 0; i < mk; ++i) {
-      double pw[kMaxR];
-      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
-      for (int s = 0; s < R; ++s) {
-        double acc = 0.0;
-        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
-        A[i * R + s] = acc;
-      }
-    }
-    for (int s = 0; s < R; ++s) {
-      for (int i = 0; i < mk; ++i) a[i] = A[i * R + s];
-      givens_insert(Rf, kMaxQ, a, mk);
-    }
-  }
-  jacobi_rows(Rf, kMaxQ, q);
-  double sig[kMaxQ], smax = 0.0;
-  for (int j = 0; j < q; ++j) {
-    double s = 0.0;
-    for (int i = 0; i < q; ++i) s = fma(Rf[j * kMaxQ + i], Rf[j * kMaxQ + i], s);
-    sig[j] = sqrt(s);
-    smax = fmax(smax, sig[j]);
-  }
-  double Km[kMaxQ * kMaxQ];
-  for (int i = 0; i < q * q; ++i) Km[i] = 0.0;
-  int r_k = 0;
-  for (int j = 0; j < q; ++j) {
-    if (!(smax > 0.0) || !(sig[j] > tau * smax)) continue;
-    ++r_k;
-    double inv3 = 1.0 / (sig[j] * sig[j] * sig[j]);
-    for (int x = 0; x < q; ++x) {
-      double vx = Rf[j * kMaxQ + x] * inv3;
-      for (int y = 0; y < q; ++y) Km[x * q + y] = fma(vx, Rf[j * kMaxQ + y], Km[x * q + y]);
-    }
-  }
-  rank[k] = r_k;
-  if (tall) {
-    for (int i = 0; i < mk; ++i) {
-      double pw[kMaxR];
-      for (int r = 0; r < R; ++r) pw[r] = P[(int64_t)i * R + r] * w[r];
-      for (int s = 0; s < R; ++s) {
-        double acc = 0.0;
-        for (int r = 0; r < R; ++r) acc = fma(pw[r], Hs[s * R + r], acc);
-        a[s] = acc;
-      }
-      for (int s = 0; s < R; ++s) {
-        double acc = 0.0;
-        for (int x = 0; x < R; ++x) acc = fma(a[x], Km[x * q + s], acc);
-        Q[(int64_t)i * R + s] = acc;
-      }
-    }
-  } else {
-    for (int i = 0; i < mk; ++i)
-      for (int s = 0; s < R; ++s) {
-        double acc = 0.0;
-        for (int x = 0; x < mk; ++x) acc = fma(Km[i * q + x], A[x * R + s], acc);
-        Q[(int64_t)i * R + s] = acc;
-      }
-  }
-}
-
-int launch_polar(Handle& h) {
-  if (h.K == 0) return 0;
-  k_polar<<<(unsigned)((h.K + 63) / 64), 64, 0, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol,
-                                                            h.Qt, h.rank);
   return 1;
 }
 
@@ -261,32 +158,42 @@ __device__ double block_G_rho(const double* G1, const double* G2, int R, double 
   return tr / R;
 }
 
-// One row of Alg.1 l.15-l.18 repeated n_inner times: z = (f + rho (zb + d)) (G + rho I)^-1;
-// zb = prox(z - d); d += zb - z.
-__device__ __forceinline__ void admm_row(const double* L, int R, const double* f, double* zb, double* dd, double rho,
-                                         int n_inner, int kind, double param) {
+// One row of Alg.1 l.15-l.18, up to n_inner times: z = (f + rho (zb + d)) (G + rho I)^-1;
+// zb = prox(z - d); d += zb - z; with tol > 0 the row stops early (reading R-inner-tol).
+// Returns the steps taken.
+__device__ __forceinline__ int admm_row(const double* L, int R, const double* f, double* zb, double* dd, double rho,
+                                        int n_inner, int kind, double param, double tol) {
   double z[kMaxR];
-  for (int it = 0; it < n_inner; ++it) {
+  int it = 0;
+  while (it < n_inner) {
     for (int r = 0; r < R; ++r) z[r] = f[r] + rho * (zb[r] + dd[r]);
     chol_solve(L, R, z);
+    RowResid res;
     for (int r = 0; r < R; ++r) {
       double nb = prox(kind, param, rho, z[r] - dd[r]);
+      res.add(nb, z[r], zb[r]);
       dd[r] += nb - z[r];
       zb[r] = nb;
     }
+    ++it;
+    if (res.done(tol)) break;
   }
+  return it;
 }
 
 // H-mode (1 block) + the W-mode setup that depends only on the new H̄.
 __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const double* VtV, const double* WtW,
-                                                double rho_fixed, int n_inner, int kind, double param, double* H,
-                                                double* DH, double* HtH, double* LW, double* GWi, double* scal,
-                                                int* err) {
+                                                double rho_fixed, int n_inner, int kind, double param, double tol,
+                                                double* H, double* DH, double* HtH, double* LW, double* GWi,
+                                                double* scal, int* err, unsigned long long* steps) {
   extern __shared__ double dyn_smem[];
   double* Gs = dyn_smem;
   double* Ls = dyn_smem + R * R;
   __shared__ int fail;
-  if (threadIdx.x == 0) fail = 0;
+  if (threadIdx.x == 0) {
+    fail = 0;
+    steps[0] = steps[1] = steps[2] = 0ull;  // this iteration's inner-step counters (H, W, V)
+  }
   __syncthreads();
   double rho = block_G_rho(VtV, WtW, R, rho_fixed, Gs);
   if (!(rho > 0.0)) { if (threadIdx.x == 0) set_err(err, ERR_DEGEN); return; }
@@ -296,7 +203,8 @@ __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const d
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
     double zb[kMaxR], dd[kMaxR], f[kMaxR];
     for (int r = 0; r < R; ++r) { zb[r] = H[i * R + r]; dd[r] = DH[i * R + r]; f[r] = FH[i * R + r]; }
-    admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param);
+    const int st = admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param, tol);
+    atomicAdd(steps, (unsigned long long)st);
     for (int r = 0; r < R; ++r) { H[i * R + r] = zb[r]; DH[i * R + r] = dd[r]; }
   }
   __syncthreads();
@@ -333,67 +241,13 @@ __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const d
 }
 
 static size_t small_smem(Handle& h) { return sizeof(double) * 2 * (size_t)h.R * h.R; }
-template <class F>
-static void set_smem_attr(F* fn) {
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * 2 * kMaxR * kMaxR));
-}
+constexpr int kSmallSmemMax = (int)(sizeof(double) * 2 * kMaxR * kMaxR);
 
 int launch_admm_H(Handle& h) {
-  static bool once = (set_smem_attr(k_admm_H), true);
-  (void)once;
-  k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind, h.o.on_H.param,
-                                    h.H, h.DH, h.HtH, h.LW, h.GWi, h.scal, h.err);
-  return 1;
-}
-
-// ------------------------------------------------------------------ pass B1: F_W, W-rows, N_k
-__global__ void __launch_bounds__(128) k_passB1(const int32_t* m, const int64_t* srow, int64_t K, int R,
-                                                const double* Pp, const double* Qt, const double* Hg,
-                                                const double* LWg, const double* scal, int n_inner, int kind,
-                                                double param, double* W, double* DW, double* Nst) {
-  extern __shared__ double dyn_smem[];
-  double* Hs = dyn_smem;
-  double* Ls = dyn_smem + R * R;
-  for (int i = threadIdx.x; i < R * R; i += blockDim.x) { Hs[i] = Hg[i]; Ls[i] = LWg[i]; }
-  __syncthreads();
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  const double rho = scal[S_RHO_W];
-  const int mk = m[k];
-  const double* P = Pp + srow[k] * R;
-  const double* Q = Qt + srow[k] * R;
-  double fw[kMaxR], t[kMaxR];
-  for (int r = 0; r < R; ++r) fw[r] = 0.0;
-  for (int a = 0; a < mk; ++a) {  // F_W(k, r) = sum_a (Q~ H̄)(a, r) P'(a, r)
-    for (int r = 0; r < R; ++r) t[r] = 0.0;
-    for (int i = 0; i < R; ++i) {
-      double qa = Q[(int64_t)a * R + i];
-      for (int r = 0; r < R; ++r) t[r] = fma(qa, Hs[i * R + r], t[r]);
-    }
-    for (int r = 0; r < R; ++r) fw[r] = fma(t[r], P[(int64_t)a * R + r], fw[r]);
-  }
-  double zb[kMaxR], dd[kMaxR];
-  for (int r = 0; r < R; ++r) { zb[r] = W[k * R + r]; dd[r] = DW[k * R + r]; }
-  admm_row(Ls, R, fw, zb, dd, rho, n_inner, kind, param);
-  for (int r = 0; r < R; ++r) { W[k * R + r] = zb[r]; DW[k * R + r] = dd[r]; }
-  double* N = Nst + srow[k] * R;
-  for (int a = 0; a < mk; ++a) {  // N_k = Q~_k H̄ S_k (new w̄_k)
-    for (int r = 0; r < R; ++r) t[r] = 0.0;
-    for (int i = 0; i < R; ++i) {
-      double qa = Q[(int64_t)a * R + i];
-      for (int r = 0; r < R; ++r) t[r] = fma(qa, Hs[i * R + r], t[r]);
-    }
-    for (int r = 0; r < R; ++r) N[(int64_t)a * R + r] = t[r] * zb[r];
-  }
-}
-
-int launch_passB1(Handle& h) {
-  if (h.K == 0) return 0;
-  static bool once = (set_smem_attr(k_passB1), true);
-  (void)once;
-  k_passB1<<<(unsigned)((h.K + 127) / 128), 128, small_smem(h), h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.LW, h.scal,
-                                                                h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param, h.W,
-                                                                h.DW, h.Nst);
+  max_smem_attr<k_admm_H>(h, kSmallSmemMax);
+  k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind,
+                                                h.o.on_H.param, h.o.admm_tol, h.H, h.DH, h.HtH, h.LW, h.GWi, h.scal,
+                                                h.err, h.steps);
   return 1;
 }
 
@@ -429,39 +283,24 @@ __global__ void k_scatter_fibers(const int64_t* gptr, int G, const int32_t* fibe
   }
 }
 
-__global__ void k_scatter_rows(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int R,
-                               const double* Nst, double* FV) {
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t >= rows * R) return;
-  int64_t i = t / R;
-  int r = (int)(t - i * R);
-  double z = Nst[t];
-  if (z == 0.0) return;
-  for (int64_t e = rp[i]; e < rp[i + 1]; ++e) atomicAdd(&FV[(int64_t)col[e] * R + r], val[e] * z);
-}
-
 int launch_scatter(Handle& h) {
+  if (!h.smooth) return launch_scatter_csc(h);  // deterministic gather over the CSC copy (k_plain.cu)
   cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
   if (h.K == 0) return 0;
-  if (h.smooth && scatter_smem_ok(h)) {
-    return launch_scatter_fibers(h);
-  } else if (h.smooth) {
-    int64_t blocks = (h.K + 7) / 8;
-    if (blocks > 148 * 32) blocks = 148 * 32;
-    k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.gptr, h.sc_G, h.fiber_col, h.fiber_val, h.m, h.srow,
-                                                             h.K, h.l, h.R, h.Nst, h.inv, h.FV);
-  } else {
-    int64_t n = h.rows * h.R;
-    k_scatter_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R,
-                                                                      h.Nst, h.FV);
-  }
+  if (scatter_smem_ok(h)) return launch_scatter_fibers(h);
+  // no F_V slice fits in shared memory (J R too large): FP64-atomic fallback (order-dependent rounding)
+  int64_t blocks = (h.K + 7) / 8;
+  if (blocks > h.sms * 32) blocks = h.sms * 32;
+  k_scatter_fibers<<<(unsigned)blocks, 256, 0, h.stream>>>(h.gptr, h.sc_G, h.fiber_col, h.fiber_val, h.m, h.srow,
+                                                           h.K, h.l, h.R, h.Nst, h.inv, h.FV);
   return 1;
 }
 
 // ------------------------------------------------------------------ V-mode ADMM (rows independent)
 __global__ void __launch_bounds__(128) k_admm_V(int64_t J, int R, const double* FV, const double* HtH,
                                                 const double* WtW, double rho_fixed, int n_inner, int kind,
-                                                double param, double* V, double* DV, double* scal, int* err) {
+                                                double param, double tol, double* V, double* DV, double* scal,
+                                                int* err, unsigned long long* steps) {
   extern __shared__ double dyn_smem[];
   double* Gs = dyn_smem;
   double* Ls = dyn_smem + R * R;
@@ -475,19 +314,35 @@ __global__ void __launch_bounds__(128) k_admm_V(int64_t J, int R, const double* 
   if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0 && blockIdx.x == 0) set_err(err, ERR_CHOL); return; }
   if (blockIdx.x == 0 && threadIdx.x == 0) scal[S_RHO_V] = rho;
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= J) return;
-  double zb[kMaxR], dd[kMaxR], f[kMaxR];
-  for (int r = 0; r < R; ++r) { zb[r] = V[j * R + r]; dd[r] = DV[j * R + r]; f[r] = FV[j * R + r]; }
-  admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param);
-  for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r]; DV[j * R + r] = dd[r]; }
+  int st = 0;
+  if (j < J) {
+    double zb[kMaxR], dd[kMaxR], f[kMaxR];
+    for (int r = 0; r < R; ++r) { zb[r] = V[j * R + r]; dd[r] = DV[j * R + r]; f[r] = FV[j * R + r]; }
+    st = admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param, tol);
+    for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r]; DV[j * R + r] = dd[r]; }
+  }
+  steps_warp(steps + 2, st);
+}
+
+// Zero entries of V̄ (SPARSITY), into steps[3].
+__global__ void k_count_zeros(const double* V, int64_t n, unsigned long long* out) {
+  int c = 0;
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x)
+    c += V[x] == 0.0;
+  steps_warp(out, c);
+}
+
+void launch_count_zeros(Handle& h) {
+  cudaMemsetAsync(h.steps + 3, 0, sizeof(unsigned long long), h.stream);
+  const int64_t n = h.J * h.R;
+  k_count_zeros<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, h.stream>>>(h.V, n, h.steps + 3);
 }
 
 int launch_admm_V(Handle& h) {
-  static bool once = (set_smem_attr(k_admm_V), true);
-  (void)once;
+  max_smem_attr<k_admm_V>(h, kSmallSmemMax);
   k_admm_V<<<(unsigned)((h.J + 127) / 128), 128, small_smem(h), h.stream>>>(h.J, h.R, h.FV, h.HtH, h.WtW, h.o.rho,
-                                                                 h.o.admm_inner, h.o.on_V.kind, h.o.on_V.param, h.V,
-                                                                 h.DV, h.scal, h.err);
+                                                                 h.o.admm_inner, h.o.on_V.kind, h.o.on_V.param,
+                                                                 h.o.admm_tol, h.V, h.DV, h.scal, h.err, h.steps);
   return 1;
 }
 
@@ -524,10 +379,11 @@ int launch_fit(Handle& h) {
 }
 
 // ------------------------------------------------------------------ U_k = C_k Q~_k H̄ (output)
-__global__ void k_U(const int64_t* prp, const double* times, int64_t K, int l, int d, const double* Bk,
+__global__ void k_U(const int64_t* prp, const double* times, int64_t k0, int64_t k1, int l, int d, const double* Bk,
                     const int32_t* m, const int64_t* srow, int R, const double* Qt, const double* H, double* U) {
-  int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (k >= K) return;
+  int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= k1) return;
+  U -= prp[k0] * R;  // row i of the shard -> U[(i - prp[k0]) R]
   int64_t r0 = prp[k], r1 = prp[k + 1];
   const int mk = m[k];
   const double* Q = Qt + srow[k] * R;
@@ -567,11 +423,11 @@ __global__ void k_U(const int64_t* prp, const double* times, int64_t K, int l, i
   }
 }
 
-void launch_U(Handle& h, double* U) {
-  if (h.K == 0) return;
-  k_U<<<(unsigned)((h.K + 127) / 128), 128, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K,
-                                                           h.smooth ? h.l : 0, h.d, h.Bk, h.m, h.srow, h.R, h.Qt,
-                                                           h.H, U);
+void launch_U(Handle& h, double* U, int64_t k0, int64_t k1) {
+  if (k1 <= k0) return;
+  k_U<<<(unsigned)((k1 - k0 + 127) / 128), 128, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, k0, k1,
+                                                               h.smooth ? h.l : 0, h.d, h.Bk, h.m, h.srow, h.R, h.Qt,
+                                                               h.H, U);
 }
 
 }  // namespace copa

@@ -75,36 +75,27 @@ __global__ void k_layoutA(const int64_t* __restrict__ gptr, int G, int64_t K, co
   }
 }
 
-template <int MT, int NT, int LT, int RT, bool VS, bool HOTV>
+template <int MT, int NT, int LT, int RT, bool VS>
 __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restrict__ fp,
                                                         const int64_t* __restrict__ warp_k,
                                                         const int32_t* __restrict__ acol,
                                                         const double* __restrict__ aval, int64_t K, int l_, int R_,
                                                         int64_t Jl, const double* __restrict__ Vl,
-                                                        double* __restrict__ Pp, const int32_t* __restrict__ hot_slot,
-                                                        const int32_t* __restrict__ hot_lab, int nhot) {
+                                                        double* __restrict__ Pp) {
   const int R = RT ? RT : R_;
   const int l = LT ? LT : l_;
   extern __shared__ __align__(128) unsigned char sraw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int cb = (chunk_bytes(l) + 127) & ~127;
-  // VS: all of V̄ (label order) in smem. HOTV: the nhot heaviest labels' rows + a label -> slot table.
+  // VS: all of V̄ (label order) in smem; otherwise gathers through L1/L2 (a hot-label smem cache
+  // measured slower at Scale: 12.1 vs 11.0 ms).
   double* Vs = (double*)sraw;
-  const size_t vbytes = VS ? (((size_t)Jl * R * 8 + 127) & ~(size_t)127)
-                           : (HOTV ? (((size_t)nhot * R * 8 + (size_t)Jl * 4 + 127) & ~(size_t)127) : 0);
-  int32_t* tab = (int32_t*)(Vs + (HOTV ? (size_t)nhot * R : 0));
+  const size_t vbytes = VS ? (((size_t)Jl * R * 8 + 127) & ~(size_t)127) : 0;
   uint64_t* bars = (uint64_t*)(sraw + vbytes) + wib * kANS;
   unsigned char* ring = sraw + vbytes + kAWarps * kANS * 8 + (size_t)wib * kANS * cb;
   if (VS) {
     for (int64_t x = threadIdx.x; x < Jl * R; x += blockDim.x) Vs[x] = Vl[x];
-  }
-  if (HOTV) {
-    for (int64_t x = threadIdx.x; x < (int64_t)nhot * R; x += blockDim.x) {
-      const int64_t sl = x / R, r = x - sl * R;
-      Vs[x] = Vl[(int64_t)hot_lab[sl] * R + r];
-    }
-    for (int64_t x = threadIdx.x; x < Jl; x += blockDim.x) tab[x] = hot_slot[x];
   }
   if (lane == 0) {
     for (int i = 0; i < kANS; ++i) mb_init(bars + i, 1);
@@ -190,9 +181,6 @@ __global__ void __launch_bounds__(32 * kAWarps) k_passA(const int64_t* __restric
       for (int nt = 0; nt < NT; ++nt) {
         if (VS) {
           bv[j][nt] = Vs[col * R + 8 * nt + g];
-        } else if (HOTV) {
-          const int sl = tab[col];
-          bv[j][nt] = sl >= 0 ? Vs[sl * R + 8 * nt + g] : __ldg(Vl + (int64_t)col * R + 8 * nt + g);
         } else {
           bv[j][nt] = __ldg(Vl + (int64_t)col * R + 8 * nt + g);
         }
@@ -238,29 +226,21 @@ template <int MT, int NT, int LT, int RT>
 static void passA_inst(Handle& h) {
   const int cb = (chunk_bytes(h.l) + 127) & ~127;
   const size_t ring = (size_t)kAWarps * kANS * (8 + cb);
-  const bool vs = h.pa_vs, hot = !vs && h.pa_nhot > 0;
-  const size_t vbytes = vs ? (((size_t)h.Jl * h.R * 8 + 127) & ~(size_t)127)
-                           : (hot ? (((size_t)h.pa_nhot * h.R * 8 + (size_t)h.Jl * 4 + 127) & ~(size_t)127) : 0);
+  const bool vs = h.pa_vs;
+  const size_t vbytes = vs ? (((size_t)h.Jl * h.R * 8 + 127) & ~(size_t)127) : 0;
   const size_t smem = vbytes + ring + 128;
-  auto set_attr = [](auto fn) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024); };
-  static bool attr = false;
-  if (!attr) {
-    set_attr(k_passA<MT, NT, LT, RT, true, false>);
-    set_attr(k_passA<MT, NT, LT, RT, false, true>);
-    set_attr(k_passA<MT, NT, LT, RT, false, false>);
-    attr = true;
-  }
   launch_relabel_V(h);  // V̄ in label order (read by every CTA: smem copy or L1/L2 gathers)
-  if (vs)
-    k_passA<MT, NT, LT, RT, true, false><<<h.pa_ctas, 32 * kAWarps, smem, h.stream>>>(
-        h.fiber_ptr, h.pa_wk, h.fa_col, h.fa_val, h.K, h.l, h.R, h.Jl, h.Vl, h.Pp, h.hot_slot, h.hot_lab, 0);
-  else if (hot)
-    k_passA<MT, NT, LT, RT, false, true><<<h.pa_ctas, 32 * kAWarps, smem, h.stream>>>(
-        h.fiber_ptr, h.pa_wk, h.fa_col, h.fa_val, h.K, h.l, h.R, h.Jl, h.Vl, h.Pp, h.hot_slot, h.hot_lab,
-        h.pa_nhot);
-  else
-    k_passA<MT, NT, LT, RT, false, false><<<h.pa_ctas, 32 * kAWarps, smem, h.stream>>>(
-        h.fiber_ptr, h.pa_wk, h.fa_col, h.fa_val, h.K, h.l, h.R, h.Jl, h.Vl, h.Pp, h.hot_slot, h.hot_lab, 0);
+  if (vs) {
+    constexpr auto fn = k_passA<MT, NT, LT, RT, true>;
+    max_smem_attr<fn>(h);
+    fn<<<h.pa_ctas, 32 * kAWarps, smem, h.stream>>>(h.fiber_ptr, h.pa_wk, h.fa_col, h.fa_val, h.K, h.l, h.R, h.Jl,
+                                                    h.Vl, h.Pp);
+  } else {
+    constexpr auto fn = k_passA<MT, NT, LT, RT, false>;
+    max_smem_attr<fn>(h);
+    fn<<<h.pa_ctas, 32 * kAWarps, smem, h.stream>>>(h.fiber_ptr, h.pa_wk, h.fa_col, h.fa_val, h.K, h.l, h.R, h.Jl,
+                                                    h.Vl, h.Pp);
+  }
 }
 
 template <int MT>
@@ -285,46 +265,19 @@ void launch_spmm_fibers(Handle& h) {
   else passA_n<2>(h);
 }
 
-// CTAs / warps of pass A and where V̄ lives: all of it in shared memory when it fits (VS); otherwise
-// the rows of the heaviest labels (by fiber mass; Zipf-like feature use puts most gathers there)
-// in the room left by two CTAs per SM, the rest through L1/L2.
+// CTAs / warps of pass A and where V̄ lives: all of it in shared memory when it fits (VS),
+// otherwise gathered through L1/L2.
 void plan_passA(Handle& h) {
   const int cb = (chunk_bytes(h.l) + 127) & ~127;
   const size_t ring = (size_t)kAWarps * kANS * (8 + cb);
   const size_t vbytes = ((size_t)h.Jl * h.R * 8 + 127) & ~(size_t)127;
-  h.pa_vs = (vbytes + ring + 128 <= 225 * 1024) && !getenv("COPA_SPMM_VGLOBAL");
-  h.pa_nhot = 0;
-  if (!h.pa_vs && getenv("COPA_SPMM_HOT")) {  // measured slower at Scale (12.1 vs 11.0 ms): opt-in
-    const int64_t room = (int64_t)(113 * 1024) - (int64_t)ring - 128 - h.Jl * 4 - 128;
-    const int64_t nh = room > 0 ? room / (8 * h.R) : 0;
-    h.pa_nhot = (int)(nh < h.Jl ? nh : h.Jl);
-  }
-  const size_t hb = h.pa_nhot > 0 ? (((size_t)h.pa_nhot * h.R * 8 + (size_t)h.Jl * 4 + 127) & ~(size_t)127) : 0;
-  const size_t smem = (h.pa_vs ? vbytes : hb) + ring + 128;
+  h.pa_vs = vbytes + ring + 128 <= 225 * 1024;
+  const size_t smem = (h.pa_vs ? vbytes : 0) + ring + 128;
   int per_sm = (int)((228 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
   if (per_sm > 2048 / (32 * kAWarps)) per_sm = 2048 / (32 * kAWarps);
-  h.pa_ctas = 148 * per_sm;
+  h.pa_ctas = h.sms * per_sm;
   h.pa_nw = (int64_t)h.pa_ctas * kAWarps;
-}
-
-// Hot-label table of pass A from the per-label fiber mass (host).
-void plan_passA_hot(const Handle& h, const unsigned long long* hist, const int32_t* inv, std::vector<int32_t>& slot,
-                    std::vector<int32_t>& lab) {
-  slot.assign((size_t)h.Jl, -1);
-  lab.clear();
-  if (h.pa_nhot <= 0) return;
-  std::vector<int32_t> order;
-  for (int64_t j = 0; j < h.Jl; ++j)
-    if (inv[j] >= 0) order.push_back((int32_t)j);
-  std::stable_sort(order.begin(), order.end(),
-                   [&](int32_t a, int32_t b) { return hist[inv[a]] > hist[inv[b]]; });
-  const int n = (int)std::min<int64_t>((int64_t)order.size(), h.pa_nhot);
-  for (int s = 0; s < n; ++s) {
-    slot[(size_t)order[(size_t)s]] = s;
-    lab.push_back(order[(size_t)s]);
-  }
-  while ((int)lab.size() < h.pa_nhot) lab.push_back(lab.empty() ? 0 : lab.back());  // padding slots
 }
 
 // Warp ranges of pass A: contiguous patient ranges with balanced fibers (host, from the prefix).
@@ -344,7 +297,7 @@ void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std
 void launch_layoutA(Handle& h) {
   if (h.K == 0) return;
   int64_t blocks = (h.K + 7) / 8;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > h.sms * 16) blocks = h.sms * 16;
   k_layoutA<<<(unsigned)blocks, 256, 0, h.stream>>>(h.gptr, h.sc_G, h.K, h.fiber_ptr, h.fiber_col, h.fiber_val, h.l,
                                                     h.fa_col, h.fa_val);
 }

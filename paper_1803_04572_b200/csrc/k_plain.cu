@@ -1,0 +1,561 @@
+// k_plain.cu — the general ("plain") path of one outer iteration, FP64, sm_100a: no smoothness, or
+// smoothness outside the wide kernels' range (l >= R or l > 12). Per-patient state rows: m_k rows
+// of P'_k, Q~_k, N_k (m_k = I_k without smoothness). Any R <= 64.
+//
+//   polar_warp   warp per patient: A_k = P'_k S_k H̄^T built row by row (lanes over columns);
+//                Givens QR of the tall side into an upper-triangular Rf (q x q, q = min(m_k, R),
+//                shared memory); one-sided Jacobi on the rows of Rf with one lane per disjoint row
+//                pair (round-robin ordering); Q~_k = A K or K A with K = V Σ^-1 V^T on the numerical
+//                range (the partial isometry U_r V_r^T, reading R-polar-2/3)      (Alg.1 l.4-5)
+//   passB_warp   warp per patient, lanes over r: T = Q~_k H̄, F_W(k,:) = colsum(T ∘ P'_k), the W-row ADMM
+//                with (G_W + rho I)^-1 (one lane per output column), N_k = T S_k      (l.12-19, W mode)
+//   scatter_csc  F_V = sum_k X_k^T N_k as a gather over a feature-major (CSC) copy of X built at init:
+//                F_V(j,:) = sum over column j's entries x_e N(row_e, :), warp per fixed-size chunk of
+//                a column, chunk partials summed in a fixed order (deterministic, no atomics)
+//                                                                                   (l.12, V mode)
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "copa_internal.cuh"
+
+namespace copa {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPlainWarps = 4;  // warps per block of the warp-per-patient kernels
+
+__host__ __device__ inline int odd_ld(int n) { return n | 1; }
+
+// Shared memory (doubles) per warp of k_polar_warp: Rf (R x LD) + A buffer (R x LD).
+__host__ __device__ inline size_t polar_warp_per_warp(int R) { return 2 * (size_t)R * odd_ld(R); }
+
+__device__ __forceinline__ double lane_pick(double v0, double v1, int j) {
+  return __shfl_sync(kFull, j < 32 ? v0 : v1, j & 31);
+}
+
+// Givens insert of the vector v (length q, lane t holds v[t] in v0 and v[t + 32] in v1) into the
+// upper-triangular Rf (q x q, stride LD): Rf^T Rf accumulates v v^T, no Gram matrix is formed.
+__device__ __forceinline__ void warp_givens_insert(double* Rf, int LD, int q, double v0, double v1) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < q; ++j) {
+    const double vj = lane_pick(v0, v1, j);
+    if (vj != 0.0) {
+      const double r = Rf[j * LD + j];
+      const double n2 = fma(r, r, vj * vj);
+      const double inv = rsqrt(n2);
+      const double cs = r * inv, sn = vj * inv;
+      int t = lane;
+      if (t > j && t < q) {
+        const double x = Rf[j * LD + t];
+        Rf[j * LD + t] = fma(cs, x, sn * v0);
+        v0 = fma(cs, v0, -sn * x);
+      }
+      t = lane + 32;
+      if (t > j && t < q) {
+        const double x = Rf[j * LD + t];
+        Rf[j * LD + t] = fma(cs, x, sn * v1);
+        v1 = fma(cs, v1, -sn * x);
+      }
+      __syncwarp();
+      if (lane == 0) Rf[j * LD + j] = n2 * inv;
+    }
+    __syncwarp();
+  }
+}
+
+// One-sided Jacobi on the q rows of Rf until mutually orthogonal: round-robin (tournament)
+// ordering, lane i rotates the i-th disjoint pair of a round. Rotation of rows x, y with
+// a = x.x, b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
+// sn = cs t (Hestenes; same rule as the thread-per-patient kernels).
+__device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
+  const int lane = threadIdx.x & 31;
+  const int N = (q & 1) ? q + 1 : q;
+  const double eps = 2.220446049250313e-16 * (double)q;
+  const double tol2 = eps * eps;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    int rotated = 0;
+    for (int rd = 0; rd < N - 1; ++rd) {
+      const int i = lane;
+      if (i < N / 2) {
+        const int p = i == 0 ? 0 : 1 + (i - 1 + rd) % (N - 1);
+        const int r = 1 + (N - 2 - i + rd) % (N - 1);
+        if (p < q && r < q) {
+          double* xp = Rf + p * LD;
+          double* xr = Rf + r * LD;
+          double a = 0.0, b = 0.0, c = 0.0;
+          for (int x = 0; x < q; ++x) {
+            const double u = xp[x], v = xr[x];
+            a = fma(u, u, a);
+            b = fma(v, v, b);
+            c = fma(u, v, c);
+          }
+          if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+            rotated = 1;
+            const double d = 0.5 * (b - a);
+            const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
+            const double cs = rsqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+            for (int x = 0; x < q; ++x) {
+              const double u = xp[x], v = xr[x];
+              xp[x] = fma(cs, u, -sn * v);
+              xr[x] = fma(sn, u, cs * v);
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    if (!__any_sync(kFull, rotated)) break;
+  }
+}
+
+// Row a of A_k = P'_k S_k H̄^T: lane s gets A(a, s) (v0: s = lane, v1: s = lane + 32).
+__device__ __forceinline__ void a_row(const double* __restrict__ P, const double* w, const double* HT, int LDH, int R,
+                                      double& v0, double& v1) {
+  const int lane = threadIdx.x & 31;
+  double s0 = 0.0, s1 = 0.0;
+  for (int r = 0; r < R; ++r) {
+    const double pw = P[r] * w[r];  // broadcast loads
+    if (lane < R) s0 = fma(pw, HT[r * LDH + lane], s0);
+    if (lane + 32 < R) s1 = fma(pw, HT[r * LDH + lane + 32], s1);
+  }
+  v0 = s0;
+  v1 = s1;
+}
+
+__global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* __restrict__ m,
+                                                                 const int64_t* __restrict__ srow, int64_t K, int R,
+                                                                 const double* __restrict__ Pp,
+                                                                 const double* __restrict__ Wg,
+                                                                 const double* __restrict__ Hg, double tau,
+                                                                 double* __restrict__ Qt, int32_t* __restrict__ rank,
+                                                                 unsigned long long* __restrict__ diag) {
+  extern __shared__ double smp[];
+  const int LD = odd_ld(R), LDH = odd_ld(R);
+  double* HT = smp;                       // H̄^T: HT[r LDH + s] = H̄(s, r)
+  double* wsh = HT + R * LDH;             // per warp: w̄_k (64)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nwb = blockDim.x >> 5;  // warps of this block (fewer at large R: shared memory)
+  double* Rf = wsh + nwb * 64 + (size_t)wib * polar_warp_per_warp(R);
+  double* Ab = Rf + (size_t)R * LD;
+  double* wk = wsh + wib * 64;
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    const int s = x / R, r = x - s * R;
+    HT[r * LDH + s] = Hg[x];
+  }
+  __syncthreads();
+  const int64_t nw = (int64_t)gridDim.x * nwb;
+  for (int64_t k = blockIdx.x * (int64_t)nwb + wib; k < K; k += nw) {
+    const int mk = m[k];
+    if (mk == 0) {
+      if (lane == 0) rank[k] = 0;
+      continue;
+    }
+    const double* P = Pp + srow[k] * R;
+    double* Q = Qt + srow[k] * R;
+    for (int r = lane; r < R; r += 32) wk[r] = Wg[k * R + r];
+    const bool tall = mk >= R;
+    const int q = tall ? R : mk;
+    for (int x = lane; x < q * LD; x += 32) Rf[x] = 0.0;
+    __syncwarp();
+    // ---- QR of the tall side: rows of A (tall) or columns of A (wide) inserted one by one
+    if (tall) {
+      for (int a = 0; a < mk; ++a) {
+        double v0, v1;
+        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
+        warp_givens_insert(Rf, LD, q, v0, v1);
+      }
+    } else {
+      for (int a = 0; a < mk; ++a) {  // A (m x R) into Ab, row a at Ab[a LD]
+        double v0, v1;
+        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
+        if (lane < R) Ab[a * LD + lane] = v0;
+        if (lane + 32 < R) Ab[a * LD + lane + 32] = v1;
+      }
+      __syncwarp();
+      for (int s = 0; s < R; ++s) {
+        const double v0 = lane < mk ? Ab[lane * LD + s] : 0.0;
+        const double v1 = lane + 32 < mk ? Ab[(lane + 32) * LD + s] : 0.0;
+        warp_givens_insert(Rf, LD, q, v0, v1);
+      }
+    }
+    // ---- SVD of the q x q factor: rows of Rf -> sigma_j v_j^T
+    warp_jacobi_rows(Rf, LD, q);
+    double n0 = 0.0, n1 = 0.0;  // sigma_j^2 of rows j = lane, lane + 32
+    if (lane < q)
+      for (int x = 0; x < q; ++x) n0 = fma(Rf[lane * LD + x], Rf[lane * LD + x], n0);
+    if (lane + 32 < q)
+      for (int x = 0; x < q; ++x) n1 = fma(Rf[(lane + 32) * LD + x], Rf[(lane + 32) * LD + x], n1);
+    double smax = fmax(n0, n1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) smax = fmax(smax, __shfl_xor_sync(kFull, smax, o));
+    smax = sqrt(smax);
+    const double sg0 = sqrt(n0), sg1 = sqrt(n1);
+    const bool keep0 = lane < q && smax > 0.0 && sg0 > tau * smax;
+    const bool keep1 = lane + 32 < q && smax > 0.0 && sg1 > tau * smax;
+    {
+      RatioDiag dg;
+      if (smax > 0.0) {
+        if (lane < q) dg.note(sg0 / smax, keep0, tau);
+        if (lane + 32 < q) dg.note(sg1 / smax, keep1, tau);
+      }
+      ratio_diag_warp(diag, D_POLAR_NEAR, dg);
+    }
+    const int rk = __popc(__ballot_sync(kFull, keep0)) + __popc(__ballot_sync(kFull, keep1));
+    if (lane == 0) rank[k] = rk;
+    // u_j = v_j / sqrt(sigma_j) (kept) or 0: K = sum_j u_j u_j^T = V Σ^-1 V^T on the range
+    {
+      const double c0 = keep0 ? 1.0 / (sg0 * sqrt(sg0)) : 0.0;
+      const double c1 = keep1 ? 1.0 / (sg1 * sqrt(sg1)) : 0.0;
+      if (lane < q)
+        for (int x = 0; x < q; ++x) Rf[lane * LD + x] *= c0;
+      if (lane + 32 < q)
+        for (int x = 0; x < q; ++x) Rf[(lane + 32) * LD + x] *= c1;
+    }
+    __syncwarp();
+    if (tall) {
+      // Q~(a, :) = A(a, :) K = sum_j (A(a, :) . u_j) u_j^T
+      for (int a = 0; a < mk; ++a) {
+        double v0, v1;
+        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
+        if (lane < R) Ab[lane] = v0;
+        if (lane + 32 < R) Ab[lane + 32] = v1;
+        __syncwarp();
+        double d0 = 0.0, d1 = 0.0;
+        if (lane < q)
+          for (int x = 0; x < q; ++x) d0 = fma(Ab[x], Rf[lane * LD + x], d0);
+        if (lane + 32 < q)
+          for (int x = 0; x < q; ++x) d1 = fma(Ab[x], Rf[(lane + 32) * LD + x], d1);
+        double q0 = 0.0, q1 = 0.0;
+        for (int j = 0; j < q; ++j) {
+          const double dj = lane_pick(d0, d1, j);
+          if (lane < R) q0 = fma(dj, Rf[j * LD + lane], q0);
+          if (lane + 32 < R) q1 = fma(dj, Rf[j * LD + lane + 32], q1);
+        }
+        if (lane < R) Q[(int64_t)a * R + lane] = q0;
+        if (lane + 32 < R) Q[(int64_t)a * R + lane + 32] = q1;
+        __syncwarp();
+      }
+    } else {
+      // Q~(:, s) = K A(:, s) = sum_j u_j (u_j . A(:, s)), column by column in place of A
+      for (int s = 0; s < R; ++s) {
+        double e0 = 0.0, e1 = 0.0;
+        if (lane < q)
+          for (int a = 0; a < mk; ++a) e0 = fma(Rf[lane * LD + a], Ab[a * LD + s], e0);
+        if (lane + 32 < q)
+          for (int a = 0; a < mk; ++a) e1 = fma(Rf[(lane + 32) * LD + a], Ab[a * LD + s], e1);
+        double q0 = 0.0, q1 = 0.0;
+        for (int j = 0; j < q; ++j) {
+          const double ej = lane_pick(e0, e1, j);
+          if (lane < mk) q0 = fma(ej, Rf[j * LD + lane], q0);
+          if (lane + 32 < mk) q1 = fma(ej, Rf[j * LD + lane + 32], q1);
+        }
+        __syncwarp();
+        if (lane < mk) Ab[lane * LD + s] = q0;
+        if (lane + 32 < mk) Ab[(lane + 32) * LD + s] = q1;
+        __syncwarp();
+      }
+      for (int a = 0; a < mk; ++a)
+        for (int s = lane; s < R; s += 32) Q[(int64_t)a * R + s] = Ab[a * LD + s];
+    }
+    __syncwarp();
+  }
+}
+
+int launch_polar_warp(Handle& h) {
+  if (h.K == 0) return 0;
+  const int R = h.R;
+  int nwb = kPlainWarps;
+  auto smem_of = [&](int w) {
+    return sizeof(double) * ((size_t)R * odd_ld(R) + (size_t)w * 64 + (size_t)w * polar_warp_per_warp(R));
+  };
+  while (nwb > 1 && smem_of(nwb) > 227 * 1024) --nwb;
+  const size_t smem = smem_of(nwb);
+  max_smem_attr<k_polar_warp>(h);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_polar_warp, 32 * nwb, smem);
+  int64_t blocks = (h.K + nwb - 1) / nwb;
+  const int64_t cap = (int64_t)h.sms * std::max(per_sm, 1);
+  if (blocks > cap) blocks = cap;
+  k_polar_warp<<<(unsigned)blocks, 32 * nwb, smem, h.stream>>>(h.m, h.srow, h.K, R, h.Pp, h.W, h.H, h.o.rank_tol,
+                                                               h.Qt, h.rank, h.diag);
+  return 1;
+}
+
+// ------------------------------------------------------------------ W pass (warp per patient)
+__global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* __restrict__ m,
+                                                                 const int64_t* __restrict__ srow, int64_t K, int R,
+                                                                 const double* __restrict__ Pp,
+                                                                 const double* __restrict__ Qt,
+                                                                 const double* __restrict__ Hg,
+                                                                 const double* __restrict__ GWi,
+                                                                 const double* __restrict__ scal, int n_inner,
+                                                                 int kind, double param, double tol,
+                                                                 double* __restrict__ W, double* __restrict__ DW,
+                                                                 double* __restrict__ Nst,
+                                                                 unsigned long long* __restrict__ steps) {
+  extern __shared__ double smb[];
+  double* Hs = smb;           // H̄ (R x R): Hs[i R + r]
+  double* GT = smb + R * R;   // (G_W + rho I)^-1 transposed: GT[q R + r] = Ginv(r, q)
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    Hs[x] = Hg[x];
+    const int r = x / R, q = x - r * R;
+    GT[q * R + r] = GWi[x];
+  }
+  __syncthreads();
+  const double rho = scal[S_RHO_W];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const bool has0 = lane < R, has1 = lane + 32 < R;
+  const int64_t nw = (int64_t)gridDim.x * kPlainWarps;
+  int my_steps = 0;
+  auto t_row = [&](const double* Qa, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
+    double s0 = 0.0, s1 = 0.0;
+    for (int i = 0; i < R; ++i) {
+      const double qa = Qa[i];
+      if (has0) s0 = fma(qa, Hs[i * R + lane], s0);
+      if (has1) s1 = fma(qa, Hs[i * R + lane + 32], s1);
+    }
+    t0 = s0;
+    t1 = s1;
+  };
+  for (int64_t k = blockIdx.x * (int64_t)kPlainWarps + wib; k < K; k += nw) {
+    const int mk = m[k];
+    const double* P = Pp + srow[k] * R;
+    const double* Q = Qt + srow[k] * R;
+    double f0 = 0.0, f1 = 0.0;  // F_W(k, r) = sum_a T(a, r) P'(a, r)
+    for (int a = 0; a < mk; ++a) {
+      double t0, t1;
+      t_row(Q + (int64_t)a * R, t0, t1);
+      if (has0) f0 = fma(t0, P[(int64_t)a * R + lane], f0);
+      if (has1) f1 = fma(t1, P[(int64_t)a * R + lane + 32], f1);
+    }
+    double w0 = has0 ? W[k * R + lane] : 0.0, w1 = has1 ? W[k * R + lane + 32] : 0.0;
+    double d0 = has0 ? DW[k * R + lane] : 0.0, d1 = has1 ? DW[k * R + lane + 32] : 0.0;
+    int it = 0;
+    while (it < n_inner) {  // Alg.1 l.15-l.18 on the row, z = (G_W + rho I)^-1 (f + rho (w̄ + d))
+      const double h0 = has0 ? f0 + rho * (w0 + d0) : 0.0;
+      const double h1 = has1 ? f1 + rho * (w1 + d1) : 0.0;
+      double z0 = 0.0, z1 = 0.0;
+      for (int qq = 0; qq < R; ++qq) {
+        const double hq = lane_pick(h0, h1, qq);
+        if (has0) z0 = fma(GT[qq * R + lane], hq, z0);
+        if (has1) z1 = fma(GT[qq * R + lane + 32], hq, z1);
+      }
+      RowResid res;
+      if (has0) {
+        const double nb = prox(kind, param, rho, z0 - d0);
+        res.add(nb, z0, w0);
+        d0 = d0 + nb - z0;
+        w0 = nb;
+      }
+      if (has1) {
+        const double nb = prox(kind, param, rho, z1 - d1);
+        res.add(nb, z1, w1);
+        d1 = d1 + nb - z1;
+        w1 = nb;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        res.pr += __shfl_xor_sync(kFull, res.pr, o);
+        res.du += __shfl_xor_sync(kFull, res.du, o);
+        res.nz += __shfl_xor_sync(kFull, res.nz, o);
+      }
+      ++it;
+      if (res.done(tol)) break;
+    }
+    my_steps += it;
+    if (has0) { W[k * R + lane] = w0; DW[k * R + lane] = d0; }
+    if (has1) { W[k * R + lane + 32] = w1; DW[k * R + lane + 32] = d1; }
+    double* N = Nst + srow[k] * R;  // N_k = T S_k (new w̄_k)
+    for (int a = 0; a < mk; ++a) {
+      double t0, t1;
+      t_row(Q + (int64_t)a * R, t0, t1);
+      if (has0) N[(int64_t)a * R + lane] = t0 * w0;
+      if (has1) N[(int64_t)a * R + lane + 32] = t1 * w1;
+    }
+  }
+  if (lane == 0 && my_steps) atomicAdd(steps + 1, (unsigned long long)my_steps);
+}
+
+int launch_passB_warp(Handle& h) {
+  if (h.K == 0) return 0;
+  const size_t smem = sizeof(double) * 2 * (size_t)h.R * h.R;
+  max_smem_attr<k_passB_warp>(h);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_passB_warp, 32 * kPlainWarps, smem);
+  int64_t blocks = (h.K + kPlainWarps - 1) / kPlainWarps;
+  const int64_t cap = (int64_t)h.sms * std::max(per_sm, 1);
+  if (blocks > cap) blocks = cap;
+  k_passB_warp<<<(unsigned)blocks, 32 * kPlainWarps, smem, h.stream>>>(
+      h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.GWi, h.scal, h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param,
+      h.o.admm_tol, h.W, h.DW, h.Nst, h.steps);
+  return 1;
+}
+
+// ------------------------------------------------------------------ feature-major copy of X (init)
+// Stable radix sort of the nonzeros by column (keys) carrying their index; entries of one column
+// stay in row order. csc_row[e] = row of the e-th entry in column order, csc_val[e] its value.
+__global__ void k_nnz_rows(const int64_t* __restrict__ rp, int64_t rows, int32_t* __restrict__ row_of) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  for (int64_t e = rp[i]; e < rp[i + 1]; ++e) row_of[e] = (int32_t)i;
+}
+
+__global__ void k_iota(int32_t* __restrict__ x, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (int32_t)i;
+}
+
+__global__ void k_csc_fill(const int32_t* __restrict__ perm, const int32_t* __restrict__ row_of,
+                           const double* __restrict__ val, int64_t nnz, int32_t* __restrict__ csc_row,
+                           double* __restrict__ csc_val) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const int32_t src = perm[e];
+  csc_row[e] = row_of[src];
+  csc_val[e] = val[src];
+}
+
+__global__ void k_col_counts(const int32_t* __restrict__ sorted_cols, int64_t nnz, int64_t J,
+                             int64_t* __restrict__ cptr /*[J+1]*/) {
+  // cptr[j] = first position of column j in the sorted order (binary search per column)
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j > J) return;
+  int64_t lo = 0, hi = nnz;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (sorted_cols[mid] < j) lo = mid + 1;
+    else hi = mid;
+  }
+  cptr[j] = lo;
+}
+
+size_t csc_temp_bytes(const Handle& h) {
+  if (h.nnz == 0) return 256;
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, (int)h.nnz);
+  return tb + 4 * sizeof(int32_t) * (size_t)h.nnz + 1024;
+}
+
+// Builds csc_ptr/csc_row/csc_val and the chunk table of the F_V gather (host planning).
+int build_csc(Handle& h) {
+  if (h.nnz == 0) {
+    cudaMemsetAsync(h.csc_ptr, 0, sizeof(int64_t) * (size_t)(h.J + 1), h.stream);
+    h.csc_chunks = 0;
+    return 0;
+  }
+  const int64_t n = h.nnz;
+  char* t = (char*)h.csc_tmp;
+  int32_t* keys_out = (int32_t*)t;
+  int32_t* idx_in = keys_out + n;
+  int32_t* idx_out = idx_in + n;
+  int32_t* row_of = idx_out + n;
+  void* cub_tmp = (void*)(row_of + n);
+  size_t tb = h.csc_tmp_bytes - 4 * sizeof(int32_t) * (size_t)n;
+  const unsigned g = (unsigned)((n + 255) / 256);
+  k_iota<<<g, 256, 0, h.stream>>>(idx_in, n);
+  k_nnz_rows<<<(unsigned)((h.rows + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.rows, row_of);
+  int end_bit = 1;
+  while ((int64_t(1) << end_bit) <= h.J) ++end_bit;
+  cub::DeviceRadixSort::SortPairs(cub_tmp, tb, h.p.col, keys_out, idx_in, idx_out, (int)n, 0, end_bit, h.stream);
+  k_csc_fill<<<g, 256, 0, h.stream>>>(idx_out, row_of, h.p.val, n, h.csc_row, h.csc_val);
+  k_col_counts<<<(unsigned)((h.J + 1 + 255) / 256), 256, 0, h.stream>>>(keys_out, n, h.J, h.csc_ptr);
+  std::vector<int64_t> cptr((size_t)h.J + 1);
+  if (cudaMemcpyAsync(cptr.data(), h.csc_ptr, sizeof(int64_t) * cptr.size(), cudaMemcpyDeviceToHost, h.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(h.stream) != cudaSuccess)
+    return -1;
+  std::vector<int64_t> ch;  // chunk c: entries [ch[2c], ch[2c+1]) of one column
+  std::vector<int64_t> first((size_t)h.J + 1);  // first chunk of column j
+  for (int64_t j = 0; j < h.J; ++j) {
+    first[(size_t)j] = (int64_t)ch.size() / 2;
+    for (int64_t a = cptr[(size_t)j]; a < cptr[(size_t)j + 1]; a += kCscChunk) {
+      ch.push_back(a);
+      ch.push_back(std::min<int64_t>(a + kCscChunk, cptr[(size_t)j + 1]));
+    }
+  }
+  first[(size_t)h.J] = (int64_t)ch.size() / 2;
+  h.csc_chunks = (int64_t)ch.size() / 2;
+  if (h.csc_chunks > h.csc_chunk_cap) return -2;
+  if (h.csc_chunks > 0)
+    cudaMemcpyAsync(h.csc_chunk, ch.data(), sizeof(int64_t) * ch.size(), cudaMemcpyHostToDevice, h.stream);
+  cudaMemcpyAsync(h.csc_chunk_first, first.data(), sizeof(int64_t) * first.size(), cudaMemcpyHostToDevice, h.stream);
+  if (cudaStreamSynchronize(h.stream) != cudaSuccess) return -1;
+  return 0;
+}
+
+// ------------------------------------------------------------------ F_V gather over the CSC copy
+// Warp per chunk: lanes over r, entries in column order (row order within the column), 4 entries
+// in flight; the chunk's partial row goes to part[c]. Then F_V(j, :) = sum of column j's chunk
+// partials in chunk order.
+__global__ void __launch_bounds__(256) k_scatter_csc(const int64_t* __restrict__ chunk, int64_t nchunks, int R,
+                                                     const int32_t* __restrict__ csc_row,
+                                                     const double* __restrict__ csc_val,
+                                                     const double* __restrict__ Nst, double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const bool has0 = lane < R, has1 = lane + 32 < R;
+  for (int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); c < nchunks; c += nw) {
+    const int64_t e0 = chunk[2 * c], e1 = chunk[2 * c + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int64_t e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      int32_t rw[4];
+      double x[4], n0[4], n1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        rw[u] = csc_row[e + u];
+        x[u] = csc_val[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double* Nr = Nst + (int64_t)rw[u] * R;
+        n0[u] = has0 ? Nr[lane] : 0.0;
+        n1[u] = has1 ? Nr[lane + 32] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a0 = fma(x[u], n0[u], a0);
+        a1 = fma(x[u], n1[u], a1);
+      }
+    }
+    for (; e < e1; ++e) {
+      const double* Nr = Nst + (int64_t)csc_row[e] * R;
+      const double x = csc_val[e];
+      if (has0) a0 = fma(x, Nr[lane], a0);
+      if (has1) a1 = fma(x, Nr[lane + 32], a1);
+    }
+    if (has0) part[c * R + lane] = a0;
+    if (has1) part[c * R + lane + 32] = a1;
+  }
+}
+
+__global__ void k_sum_chunks(int64_t J, int R, const double* __restrict__ part,
+                             const int64_t* __restrict__ chunk_first /*[J+1] first chunk of column j*/,
+                             double* __restrict__ FV) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= J * R) return;
+  const int64_t j = x / R, r = x - j * R;
+  double s = 0.0;
+  for (int64_t c = chunk_first[j]; c < chunk_first[j + 1]; ++c) s += part[c * R + r];
+  FV[x] = s;
+}
+
+int launch_scatter_csc(Handle& h) {
+  if (h.csc_chunks == 0) {
+    cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
+    return 0;
+  }
+  int64_t blocks = (h.csc_chunks + 7) / 8;
+  if (blocks > (int64_t)h.sms * 8) blocks = (int64_t)h.sms * 8;
+  k_scatter_csc<<<(unsigned)blocks, 256, 0, h.stream>>>(h.csc_chunk, h.csc_chunks, h.R, h.csc_row, h.csc_val, h.Nst,
+                                                        h.csc_part);
+  const int64_t n = h.J * h.R;
+  k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.J, h.R, h.csc_part,
+                                                                  h.csc_chunk_first, h.FV);
+  return 2;
+}
+
+}  // namespace copa

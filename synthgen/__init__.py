@@ -114,6 +114,18 @@ CONFIGS = {
                     n_inner=5, n_outer=5),
 }
 
+# Derived workloads of SURVEY 8(f) (not BASELINE configs; same seeded data as their base config):
+#   N4 non-smooth high rank: Large's data and constraints without the spline basis (R = 40 polar on
+#   the raw I_k x R factors: tall QR + 40 x 40 Jacobi for I_k >= 40);
+#   N4 unconstrained PARAFAC2: Small's data with the identity prox on every factor (a CP-ALS-like
+#   step, the SPARTan-style model of PAPER.md:535).
+CONFIGS["large_plain"] = dataclasses.replace(
+    CONFIGS["large"], name="large_plain", smooth_l=0,
+    baseline=CONFIGS["large"].baseline + " [SURVEY 8(f) N4 variant: no smoothness]")
+CONFIGS["small_unconstrained"] = dataclasses.replace(
+    CONFIGS["small"], name="small_unconstrained", con_H=(NONE, 0.0), con_W=(NONE, 0.0), con_V=(NONE, 0.0),
+    baseline=CONFIGS["small"].baseline + " [SURVEY 8(f) N4 variant: unconstrained, identity prox]")
+
 
 @dataclasses.dataclass
 class Problem:

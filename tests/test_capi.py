@@ -41,13 +41,13 @@ def test_limits_and_phase_names(copa):
     assert names[0] == "spmm" and "scatter" in names and L.copa_phase_name(99) == b""
 
 
-def _structs(copa, R=5, J=10, K=2, smooth=0, kind_V=1, param_V=0.0, admm=5):
+def _structs(copa, R=5, J=10, K=2, smooth=0, kind_V=1, param_V=0.0, admm=5, admm_tol=0.0):
     m = copa.copa
     p = m._Problem(K_local=K, K_global=K, J=J, R=R, rows=4, nnz=4, patient_row_ptr=8, row_ptr=8, col=8, val=8,
                    visit_time=8 if smooth else None)
     o = m._Options(on_H=m._Constraint(0, 0.0), on_W=m._Constraint(1, 0.0), on_V=m._Constraint(kind_V, param_V),
                    smooth_l=smooth, smooth_degree=3, rho=0.0, admm_inner=admm, rank_tol=1e-10, basis_tol=1e-6,
-                   H0=8, V0=8, W0_local=8, allreduce=m.ALLREDUCE_FN(), allreduce_ctx=None, stream=None)
+                   admm_tol=admm_tol, H0=8, V0=8, W0_local=8, allreduce=m.ALLREDUCE_FN(), allreduce_ctx=None, stream=None)
     return p, o
 
 
@@ -60,7 +60,7 @@ def _structs(copa, R=5, J=10, K=2, smooth=0, kind_V=1, param_V=0.0, admm=5):
     ({"kind_V": 2, "param_V": -1.0}, -1),  # negative lambda
     ({"kind_V": 4, "param_V": 0.0}, -1),   # mu must be > 0
     ({"smooth": 17}, -9),                # l beyond the limit
-    ({"R": 20, "smooth": 0}, -9),        # plain path: tall q = R > 16 unsupported in this build
+    ({"admm_tol": -1.0}, -1),            # negative inner-stop tolerance
 ])
 def test_host_side_validation(copa, kw, status):
     p, o = _structs(copa, **kw)

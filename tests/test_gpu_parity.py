@@ -88,3 +88,36 @@ def test_constraint_variants(copa_mod, name, K, cons):
     fg += g.iterate(4)
     fo += o.iterate(4)
     assert max(abs(a - b) for a, b in zip(fg, fo)) <= 1e-7, (fg, fo)
+
+
+# N4: the second workload — non-smooth R = 40 (tall QR + 40 x 40 Jacobi per patient
+# for I_k >= 40, the wide factorisation otherwise) and unconstrained PARAFAC2
+# (identity prox on every factor).
+N4_CASES = [("large_plain", 1200), ("small_unconstrained", 3000)]
+
+
+@pytest.mark.parametrize("name,K", N4_CASES)
+def test_n4_one_iteration_factors(copa_mod, name, K):
+    p, g, o = _pair(copa_mod, name, K)
+    fg = g.iterate(1)
+    fo = o.iterate(1)
+    H, V, W = [t.cpu().numpy() for t in g.factors()]
+    errs = {"H": rel(H, o.H), "V": rel(V, o.V), "W": rel(W, o.W), "Q": rel(g.debug_state()["Qt"].cpu().numpy(), o.Q),
+            "U": rel(g.U().cpu().numpy(), o.U_all())}
+    print(f"[margin] {name}: FIT {abs(fg[0] - fo[0]):.2e} " + " ".join(f"{k} {v:.2e}" for k, v in errs.items()))
+    assert abs(fg[0] - fo[0]) <= 1e-9
+    for k, e in errs.items():
+        assert e <= 1e-9, (name, k, e, errs)
+    st = g.stats()
+    print(f"[rank-cut] {name}: near {st['polar_near']} min-kept {st['polar_min_kept']:.2e} "
+          f"max-dropped {st['polar_max_dropped']:.2e}")
+
+
+@pytest.mark.parametrize("name,K", N4_CASES)
+def test_n4_fit_after_ten_iterations(copa_mod, name, K):
+    p, g, o = _pair(copa_mod, name, K)
+    fg = g.iterate(10)
+    fo = o.iterate(10)
+    err = max(abs(a - b) for a, b in zip(fg, fo))
+    print(f"[margin] {name} FIT(10): {err:.2e} / 1e-7")
+    assert err <= 1e-7, (fg, fo)

@@ -10,6 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import synthgen
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -90,3 +92,29 @@ def test_two_rank_gloo():
     for name in ("small", "medium"):
         a, b = res[0][name]["shard_nnz"], res[1][name]["shard_nnz"]
         assert abs(a - b) <= 0.05 * (a + b)  # nnz-balanced
+
+
+@pytest.mark.parametrize("name,K,kw", [("tiny", None, {}), ("medium", 600, {}), ("small", 800, {"admm_tol": 1e-3})])
+def test_sharded_oracle_matches_serial(name, K, kw):
+    """oracle/sharded.py (the full-size parity reference and the all-cores CPU baseline) equals the
+    serial oracle: the per-patient sums are only regrouped by shard (rounding-level differences)."""
+    import oracle
+    from oracle.sharded import ShardedOracle
+    cfg = synthgen.CONFIGS[name]
+    p = synthgen.generate(cfg, K=K)
+    o = oracle.Oracle(p, opts=oracle.options_from_config(cfg, **kw))
+    so = ShardedOracle(cfg, procs=3, K=p.K, **kw)
+    try:
+        fo = o.iterate(3)
+        fs = so.iterate(3)
+        assert max(abs(a - b) for a, b in zip(fo, fs)) <= 1e-12
+        W, DW = so.W_all()
+        for a, b in ((so.H, o.H), (so.V, o.V), (W, o.W), (DW, o.DW), (so.DV, o.DV)):
+            assert np.linalg.norm(a - b) <= 1e-11 * max(np.linalg.norm(b), 1e-300)
+        assert so.inner_steps[-1] == o.inner_steps[-1]
+        ks = [0, p.K // 2, p.K - 1]
+        U = so.U_rows(ks)
+        for k in ks:
+            assert np.allclose(U[k], o.U(k), rtol=0, atol=1e-11 * max(1.0, np.abs(o.U(k)).max()))
+    finally:
+        so.close()
