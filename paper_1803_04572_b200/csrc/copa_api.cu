@@ -383,6 +383,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
     cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
     launch_layoutA(h);
+    launch_fiber_rowoff(h);  // pass B addresses F_V rows by precomputed offsets (k_fibers.cu)
     tm.mark("layoutA");
   } else {
     launch_row_patient(h);
@@ -486,6 +487,42 @@ static copa_status iterate_once(Handle& h) {
   return COPA_OK;
 }
 
+// One outer iteration, replayed from a CUDA graph when possible (the small workloads are
+// launch-bound). The graph is captured on the second call of a single-rank, non-profiled handle
+// (the first call runs eagerly, so one-off host work such as function attributes is done) and
+// replayed afterwards; every kernel argument is a workspace pointer or an option, so the graph
+// stays valid for the handle's lifetime. Multi-rank iterations call the allreduce callback and
+// run eagerly.
+static copa_status iterate_step(Handle& h) {
+  if (h.o.allreduce || h.profiling || h.graph_failed || !h.use_graph) return iterate_once(h);
+  if (!h.graph_exec) {
+    if (h.eager_done < 1) {
+      ++h.eager_done;
+      return iterate_once(h);
+    }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      h.graph_failed = true;
+      return iterate_once(h);
+    }
+    copa_status st = iterate_once(h);
+    const cudaError_t ce = cudaStreamEndCapture(h.stream, &g);
+    if (st != COPA_OK || ce != cudaSuccess || !g ||
+        cudaGraphInstantiate(&h.graph_exec, g, 0) != cudaSuccess) {
+      cudaGetLastError();
+      if (g) cudaGraphDestroy(g);
+      h.graph_exec = nullptr;
+      h.graph_failed = true;
+      if (st != COPA_OK) return st;
+      return iterate_once(h);  // nothing ran during the capture
+    }
+    h.graph = g;
+  }
+  CUDA_TRY(cudaGraphLaunch(h.graph_exec, h.stream), "graph launch");
+  return COPA_OK;
+}
+
 copa_status copa_iterate(copa_handle* H, int32_t n_outer, double* fit_host) {
   if (!H) return fail(COPA_E_ARG, "null handle");
   if (n_outer < 0) return fail(COPA_E_ARG, "n_outer < 0");
@@ -494,7 +531,7 @@ copa_status copa_iterate(copa_handle* H, int32_t n_outer, double* fit_host) {
   while (done < n_outer) {
     int32_t chunk = n_outer - done < 1024 ? n_outer - done : 1024;
     for (int32_t t = 0; t < chunk; ++t) {
-      copa_status st = iterate_once(h);
+      copa_status st = iterate_step(h);
       if (st != COPA_OK) return st;
       cudaMemcpyAsync(h.fit_ring + t, h.scal + S_FIT, sizeof(double), cudaMemcpyDeviceToDevice, h.stream);
       ++h.iterations;
@@ -518,7 +555,7 @@ copa_status copa_iterate_until(copa_handle* H, int32_t max_outer, double outer_t
   if (n_done) *n_done = 0;
   double prev = 0.0;
   for (int32_t t = 0; t < max_outer; ++t) {
-    copa_status st = iterate_once(h);
+    copa_status st = iterate_step(h);
     if (st != COPA_OK) return st;
     ++h.iterations;
     double fit = 0.0;
@@ -695,6 +732,8 @@ copa_status copa_debug_state(copa_handle* H, double* Pp, double* Qt, int32_t* m,
 void copa_destroy(copa_handle* H) {
   if (!H) return;
   for (auto e : H->h.events) cudaEventDestroy(e);
+  if (H->h.graph_exec) cudaGraphExecDestroy(H->h.graph_exec);
+  if (H->h.graph) cudaGraphDestroy(H->h.graph);
   delete H;
 }
 

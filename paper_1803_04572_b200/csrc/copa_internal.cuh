@@ -105,6 +105,12 @@ struct Handle {
   unsigned long long* diag;   // [kDiagSlots] rank-cut diagnostics (see DiagSlot)
   unsigned long long* steps;  // [4] inner ADMM steps of the H, W, V modes (last iteration) + zero count
   int own_inputs;      // copa_fit: CSR copied into the workspace
+  // CUDA graph of one outer iteration (single rank, not profiling; copa_api.cu iterate_step)
+  bool use_graph = true;
+  bool graph_failed = false;
+  int eager_done = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
   // phase profiling (copa_set_profiling)
   bool profiling = false;
   std::vector<cudaEvent_t> events;
@@ -306,6 +312,7 @@ void launch_U(Handle& h, double* U, int64_t k0, int64_t k1);
 void launch_spmm_fibers(Handle& h);   // pass A (k_passA.cu)
 void launch_relabel_V(Handle& h);
 void launch_layoutA(Handle& h);
+void launch_fiber_rowoff(Handle& h);
 void plan_passA(Handle& h);
 void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
 int launch_scatter_fibers(Handle& h);

@@ -76,6 +76,8 @@ __device__ __forceinline__ void givens_insert_reg(double (&Rf)[L][L], double (&c
 // layout); a sweep (L-1 or L rounds) meets every pair once. Rotation of rows x, y with a = x.x,
 // b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
 // sn = cs t; x <- cs x - sn y, y <- sn x + cs y (the classical zeta = d/c form, Hestenes).
+constexpr double kJacobiDoneCos2 = 1e-24;  // (1e-12)^2, see jacobi_rows_reg
+
 template <int L>
 __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
   constexpr int N = (L % 2) ? L + 1 : L;  // players, with a dummy (index L) when L is odd
@@ -83,6 +85,7 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
   constexpr double tol2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
+    double maxcos2 = 0.0;  // largest (x.y)^2 / (|x|^2 |y|^2) rotated away in this sweep
 #pragma unroll
     for (int rd = 0; rd < N - 1; ++rd) {
       double cs[N / 2], sn[N / 2];
@@ -102,6 +105,7 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
           }
           if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
             rotated = 1;
+            maxcos2 = fmax(maxcos2, (c * c) / (a * b));
             const double d = 0.5 * (b - a);
             const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
             cs[i] = rsqrt(fma(t, t, 1.0));
@@ -123,7 +127,10 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
         }
       }
     }
-    if (__all_sync(0xffffffffu, rotated == 0)) break;
+    // converged when no pair needed a rotation, or when every rotation of this sweep was below
+    // 1e-12 in cosine (the sweep has left the rows orthogonal to ~1e-24 (quadratic convergence); a
+    // further sweep would only confirm it)
+    if (__all_sync(0xffffffffu, rotated == 0 || maxcos2 < kJacobiDoneCos2)) break;
   }
 }
 
@@ -612,6 +619,30 @@ static void polar_wide_n(Handle& h) {
 // thread per patient: 5 ADMM row steps z = Ginv (f + rho (w̄ + d)), w̄ = prox(z - d), d += w̄ - z with
 //   Ginv = (G_W + rho I)^-1 formed once from the cached Cholesky factor (k_admm_H)          (l.13-19)
 //   N_p = T_p S_p (new w̄_p) -> HBM, M += N_p^T N_p (MMA via the warp's smem scratch), W̄^T W̄ += w̄ w̄^T
+// W-row ADMM with the per-row stop of reading R-inner-tol (used when admm_tol > 0): the same steps
+// as the fixed-count loop in k_passB_wide on the [r * 32] strided shared-memory rows of one lane.
+static __device__ __noinline__ int w_row_admm_tol(const double* Gs, int R, const double* fw, double* wb, double* dd,
+                                           double rho, int n_inner, int kind, double param, double tol) {
+  double rhs[kMaxR];
+  int it = 0;
+  while (it < n_inner) {
+    for (int r = 0; r < R; ++r) rhs[r] = fw[r * 32] + rho * (wb[r * 32] + dd[r * 32]);
+    RowResid res;
+    for (int r = 0; r < R; ++r) {
+      double z = 0.0;
+      for (int q = 0; q < R; ++q) z = fma(Gs[r * R + q], rhs[q], z);
+      const double d0 = dd[r * 32];
+      const double nb = prox(kind, param, rho, z - d0);
+      res.add(nb, z, wb[r * 32]);
+      dd[r * 32] = d0 + nb - z;
+      wb[r * 32] = nb;
+    }
+    ++it;
+    if (res.done(tol)) break;
+  }
+  return it;
+}
+
 template <int MT, int NT, int RT, int LT>
 __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, const double* __restrict__ Pp,
                                                     const double* __restrict__ Qt, const double* __restrict__ Hg,
@@ -749,28 +780,31 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
     int nsteps = 0;
     if (kme < K) {
       for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
-      while (nsteps < n_inner) {
-        RowResid res;  // per-row inner stop (reading R-inner-tol)
-        double rhs[RP];
+      if (tol > 0.0) {
+        // per-row inner stop (reading R-inner-tol); out of line, so that the fixed-step loop below keeps
+        // its register allocation
+        nsteps = w_row_admm_tol(Gs, R, fwv + lane, wbv + lane, dv + lane, rho, n_inner, kind, param, tol);
+      } else {
+        for (int it = 0; it < n_inner; ++it) {
+          double rhs[RP];
 #pragma unroll
-        for (int r = 0; r < RP; ++r)
-          rhs[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
+          for (int r = 0; r < RP; ++r)
+            rhs[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
 #pragma unroll
-        for (int r = 0; r < RP; ++r) {
-          if (r < R) {
-            double z = 0.0;
+          for (int r = 0; r < RP; ++r) {
+            if (r < R) {
+              double z = 0.0;
 #pragma unroll
-            for (int q = 0; q < RP; ++q)
-              if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
-            const double d0 = dv[r * 32 + lane];
-            const double nb = prox(kind, param, rho, z - d0);
-            res.add(nb, z, wbv[r * 32 + lane]);
-            dv[r * 32 + lane] = d0 + nb - z;
-            wbv[r * 32 + lane] = nb;
+              for (int q = 0; q < RP; ++q)
+                if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
+              const double d0 = dv[r * 32 + lane];
+              const double nb = prox(kind, param, rho, z - d0);
+              dv[r * 32 + lane] = d0 + nb - z;
+              wbv[r * 32 + lane] = nb;
+            }
           }
         }
-        ++nsteps;
-        if (res.done(tol)) break;
+        nsteps = n_inner;
       }
       for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
     } else {

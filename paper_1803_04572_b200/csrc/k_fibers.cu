@@ -134,6 +134,7 @@ __host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
 }
 
 constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
+constexpr int kScrD = 128;       // per-warp scratch doubles behind the F_V slice (redirected row updates)
 
 
 // F_V row updates are branch-free: invalid lanes are redirected to a per-lane scratch slot
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
   const int64_t rng = blockIdx.x / G;
   const SlotGeom sg = slot_geom(FB, PB, l, R);
   double* Fs = (double*)smraw;  // Jg x RS, then W x 64 doubles of per-warp scratch (branch-free RMW)
-  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * 512 + 127) & ~127ull);
+  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * kScrD * 8 + 127) & ~127ull);
   uint64_t* full = (uint64_t*)(smraw + fs_bytes);
   uint64_t* empty = full + NSt;
   const uint32_t slots_off = fs_bytes + ((2 * NSt * 8 + 127) & ~127);
@@ -229,9 +230,9 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     // comes from the staged offsets; tiles of 8 fibers (one patient, distinct labels) run TB at a
     // time: loads and MMAs of the batch first, then the read-modify-writes.
     const int g = lane >> 2, t = lane & 3;
-    const int64_t jbase = grp * Jg;
     const int per = l * R;
-    const int scr = (int)Jg * RS + w * 64 + 2 * lane;  // this lane's scratch slot (index into Fs)
+    const int scr = (int)Jg * RS + w * kScrD + 2 * lane;  // this lane's scratch slot (index into Fs; + 8 nt stays
+                                                          // inside the warp's kScrD doubles)
     int offn[KS][NT];   // lane's B-fragment offsets inside an N_k block (-1: padding)
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
@@ -284,14 +285,14 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         // all row loads of a batch may precede its stores.
         auto run_tiles = [&](int tb, auto tbc) {
           constexpr int NB = decltype(tbc)::value;
-          int32_t col[NB];
+          int base[NB];  // F_V slice index of this lane's (fiber, columns 2t, 2t + 1) in tile 0 (or scratch)
           double av[NB][KS];
           double cc[NB][NT][2];
 #pragma unroll
           for (int b = 0; b < NB; ++b) {
             const int f = tb + 8 * b + g;
             const bool ok = f < hi;
-            col[b] = ok ? colS[f] : -1;
+            base[b] = ok ? colS[f] + 2 * t : scr;  // fibers carry their F_V row offset (label - g Jg) RS
 #pragma unroll
             for (int ks = 0; ks < KS; ++ks) {
               const int a = 4 * ks + t;
@@ -306,16 +307,15 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
             for (int b = 0; b < NB; ++b)
 #pragma unroll
               for (int nt = 0; nt < NT; ++nt) dmma(cc[b][nt][0], cc[b][nt][1], av[b][ks], bfr[ks][nt]);
-          // branch-free row updates: lanes without a valid (fiber, column) pair hit their scratch
-          // slot. Shared-memory indices (not pointers) so the accesses stay plain LDS/STS.
+          // branch-free row updates: tile nt at base + 8 nt (an immediate offset); columns >= R of
+          // the last tile and lanes without a fiber go to the lane's scratch slot.
           int idx[NB][NT];
           double2 v[NB][NT];
 #pragma unroll
           for (int b = 0; b < NB; ++b)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
-              const bool ok = col[b] >= 0 && 8 * nt + 2 * t < R;
-              idx[b][nt] = ok ? (col[b] - (int)jbase) * RS + 8 * nt + 2 * t : scr;
+              idx[b][nt] = (8 * nt + 8 <= R || 8 * nt + 2 * t < R) ? base[b] + 8 * nt : scr;
               v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
             }
 #pragma unroll
@@ -425,7 +425,7 @@ void plan_scatter(Handle& h) {
     for (int G = gmin; G <= kMaxGroups && !h.sc_ok; ++G) {
       const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
       const int64_t Jg = Js * h.sc_W;
-      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + (size_t)h.sc_W * 512 + 127) & ~(size_t)127;
+      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + (size_t)h.sc_W * kScrD * 8 + 127) & ~(size_t)127;
       for (int NSt = 4; NSt >= (pass ? 2 : 3) && !h.sc_ok; --NSt)
         for (int pi = 0; pi < (pass ? 3 : 2) && !h.sc_ok; ++pi) {
           const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
@@ -445,7 +445,7 @@ void plan_scatter(Handle& h) {
   // Larger stages (FB = 512: fewer per-stage overheads; measured 43 -> 40 ms at Scale, 2.26 -> 2.10 ms
   // at Medium) when they still fit at the same G with >= 3 slots of >= 8 patients.
   if (h.sc_ok) {
-    const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + (size_t)h.sc_W * 512 + 127) & ~(size_t)127;
+    const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + (size_t)h.sc_W * kScrD * 8 + 127) & ~(size_t)127;
     bool done = false;
     for (int NSt = 4; NSt >= 3 && !done; --NSt)
       for (int pi = 0; pi < 2 && !done; ++pi) {
@@ -475,6 +475,22 @@ void plan_scatter(Handle& h) {
 }
 
 bool scatter_smem_ok(const Handle& h) { return h.sc_ok != 0; }
+
+// Init (after layoutA has copied the labels): the g-stream labels become F_V slice offsets
+// (label - g Jg) RS, so pass B addresses a fiber's F_V row without index arithmetic.
+__global__ void k_fiber_rowoff(const int64_t* __restrict__ gptr, int64_t K, int G, int64_t Jg, int RS,
+                               int32_t* __restrict__ fiber_col) {
+  for (int g = 0; g < G; ++g) {
+    const int64_t f0 = gptr[(int64_t)g * (K + 1)], f1 = gptr[(int64_t)g * (K + 1) + K];
+    for (int64_t f = f0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < f1; f += (int64_t)gridDim.x * blockDim.x)
+      fiber_col[f] = (int32_t)((fiber_col[f] - g * Jg) * RS);
+  }
+}
+
+void launch_fiber_rowoff(Handle& h) {
+  if (!h.sc_ok || h.K == 0) return;
+  k_fiber_rowoff<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.gptr, h.K, h.sc_G, h.sc_Jg, h.sc_RS, h.fiber_col);
+}
 
 int64_t stage_cap(const Handle& h) {
   return h.F / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "copa_internal.cuh"
+#include "k_dense.cuh"  // register Givens / Jacobi helpers
 
 namespace copa {
 
@@ -36,32 +37,43 @@ __device__ __forceinline__ double lane_pick(double v0, double v1, int j) {
 
 // Givens insert of the vector v (length q, lane t holds v[t] in v0 and v[t + 32] in v1) into the
 // upper-triangular Rf (q x q, stride LD): Rf^T Rf accumulates v v^T, no Gram matrix is formed.
-__device__ __forceinline__ void warp_givens_insert(double* Rf, int LD, int q, double v0, double v1) {
+// Lane t owns column t (and t + 32) of Rf above the diagonal; the diagonal lives in registers
+// (lane j holds Rf(j, j) in d0, Rf(j + 32, j + 32) in d1), so no two lanes touch the same word and
+// the insertion needs no barrier; warp_givens_flush() stores the diagonal afterwards.
+__device__ __forceinline__ void warp_givens_insert(double* Rf, int LD, int q, double v0, double v1, double& d0,
+                                                   double& d1) {
   const int lane = threadIdx.x & 31;
+  const bool own0 = lane < q, own1 = lane + 32 < q;
   for (int j = 0; j < q; ++j) {
+    const double x0 = (own0 && lane > j) ? Rf[j * LD + lane] : 0.0;
+    const double x1 = (own1 && lane + 32 > j) ? Rf[j * LD + lane + 32] : 0.0;
     const double vj = lane_pick(v0, v1, j);
+    const double r = lane_pick(d0, d1, j);
     if (vj != 0.0) {
-      const double r = Rf[j * LD + j];
       const double n2 = fma(r, r, vj * vj);
       const double inv = rsqrt(n2);
       const double cs = r * inv, sn = vj * inv;
-      int t = lane;
-      if (t > j && t < q) {
-        const double x = Rf[j * LD + t];
-        Rf[j * LD + t] = fma(cs, x, sn * v0);
-        v0 = fma(cs, v0, -sn * x);
+      if (own0 && lane > j) {
+        Rf[j * LD + lane] = fma(cs, x0, sn * v0);
+        v0 = fma(cs, v0, -sn * x0);
       }
-      t = lane + 32;
-      if (t > j && t < q) {
-        const double x = Rf[j * LD + t];
-        Rf[j * LD + t] = fma(cs, x, sn * v1);
-        v1 = fma(cs, v1, -sn * x);
+      if (own1 && lane + 32 > j) {
+        Rf[j * LD + lane + 32] = fma(cs, x1, sn * v1);
+        v1 = fma(cs, v1, -sn * x1);
       }
-      __syncwarp();
-      if (lane == 0) Rf[j * LD + j] = n2 * inv;
+      if (lane == (j & 31)) {
+        if (j < 32) d0 = n2 * inv;
+        else d1 = n2 * inv;
+      }
     }
-    __syncwarp();
   }
+}
+
+__device__ __forceinline__ void warp_givens_flush(double* Rf, int LD, int q, double d0, double d1) {
+  const int lane = threadIdx.x & 31;
+  if (lane < q) Rf[lane * LD + lane] = d0;
+  if (lane + 32 < q) Rf[(lane + 32) * LD + lane + 32] = d1;
+  __syncwarp();
 }
 
 // One-sided Jacobi on the q rows of Rf until mutually orthogonal: round-robin (tournament)
@@ -75,6 +87,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
   const double tol2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0;
+    double maxcos2 = 0.0;
     for (int rd = 0; rd < N - 1; ++rd) {
       const int i = lane;
       if (i < N / 2) {
@@ -92,6 +105,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
           }
           if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
             rotated = 1;
+            maxcos2 = fmax(maxcos2, (c * c) / (a * b));
             const double d = 0.5 * (b - a);
             const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
             const double cs = rsqrt(fma(t, t, 1.0));
@@ -106,17 +120,30 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
       }
       __syncwarp();
     }
-    if (!__any_sync(kFull, rotated)) break;
+    if (__all_sync(kFull, rotated == 0 || maxcos2 < kJacobiDoneCos2)) break;  // as jacobi_rows_reg
   }
 }
 
-// Row a of A_k = P'_k S_k H̄^T: lane s gets A(a, s) (v0: s = lane, v1: s = lane + 32).
-__device__ __forceinline__ void a_row(const double* __restrict__ P, const double* w, const double* HT, int LDH, int R,
+// A row of the patient's state (R values) in the warp's registers: lane t holds x[t] and x[t + 32]
+// (one coalesced load per row; the values are then broadcast with shuffles, no dependent loads).
+struct RowReg {
+  double x0, x1;
+  __device__ __forceinline__ void load(const double* __restrict__ row, int R) {
+    const int lane = threadIdx.x & 31;
+    x0 = lane < R ? row[lane] : 0.0;
+    x1 = lane + 32 < R ? row[lane + 32] : 0.0;
+  }
+};
+
+// Row a of A_k = P'_k S_k H̄^T from the row P'_k(a, :) in registers: lane s gets A(a, s)
+// (v0: s = lane, v1: s = lane + 32); w0/w1 = w̄_k in the same lane layout.
+__device__ __forceinline__ void a_row(const RowReg& p, double w0, double w1, const double* HT, int LDH, int R,
                                       double& v0, double& v1) {
   const int lane = threadIdx.x & 31;
+  const double pw0 = p.x0 * w0, pw1 = p.x1 * w1;
   double s0 = 0.0, s1 = 0.0;
   for (int r = 0; r < R; ++r) {
-    const double pw = P[r] * w[r];  // broadcast loads
+    const double pw = lane_pick(pw0, pw1, r);
     if (lane < R) s0 = fma(pw, HT[r * LDH + lane], s0);
     if (lane + 32 < R) s1 = fma(pw, HT[r * LDH + lane + 32], s1);
   }
@@ -134,12 +161,10 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
   extern __shared__ double smp[];
   const int LD = odd_ld(R), LDH = odd_ld(R);
   double* HT = smp;                       // H̄^T: HT[r LDH + s] = H̄(s, r)
-  double* wsh = HT + R * LDH;             // per warp: w̄_k (64)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwb = blockDim.x >> 5;  // warps of this block (fewer at large R: shared memory)
-  double* Rf = wsh + nwb * 64 + (size_t)wib * polar_warp_per_warp(R);
+  double* Rf = HT + R * LDH + (size_t)wib * polar_warp_per_warp(R);
   double* Ab = Rf + (size_t)R * LD;
-  double* wk = wsh + wib * 64;
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
     const int s = x / R, r = x - s * R;
     HT[r * LDH + s] = Hg[x];
@@ -154,22 +179,29 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
     }
     const double* P = Pp + srow[k] * R;
     double* Q = Qt + srow[k] * R;
-    for (int r = lane; r < R; r += 32) wk[r] = Wg[k * R + r];
+    const double w0 = lane < R ? Wg[k * R + lane] : 0.0, w1 = lane + 32 < R ? Wg[k * R + lane + 32] : 0.0;
     const bool tall = mk >= R;
     const int q = tall ? R : mk;
     for (int x = lane; x < q * LD; x += 32) Rf[x] = 0.0;
     __syncwarp();
+    double dg0 = 0.0, dg1 = 0.0;  // diagonal of Rf (see warp_givens_insert)
     // ---- QR of the tall side: rows of A (tall) or columns of A (wide) inserted one by one
     if (tall) {
+      RowReg nxt;
+      nxt.load(P, R);
       for (int a = 0; a < mk; ++a) {
+        const RowReg cur = nxt;
+        if (a + 1 < mk) nxt.load(P + (int64_t)(a + 1) * R, R);  // next row in flight
         double v0, v1;
-        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
-        warp_givens_insert(Rf, LD, q, v0, v1);
+        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
+        warp_givens_insert(Rf, LD, q, v0, v1, dg0, dg1);
       }
     } else {
       for (int a = 0; a < mk; ++a) {  // A (m x R) into Ab, row a at Ab[a LD]
+        RowReg cur;
+        cur.load(P + (int64_t)a * R, R);
         double v0, v1;
-        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
+        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
         if (lane < R) Ab[a * LD + lane] = v0;
         if (lane + 32 < R) Ab[a * LD + lane + 32] = v1;
       }
@@ -177,9 +209,10 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
       for (int s = 0; s < R; ++s) {
         const double v0 = lane < mk ? Ab[lane * LD + s] : 0.0;
         const double v1 = lane + 32 < mk ? Ab[(lane + 32) * LD + s] : 0.0;
-        warp_givens_insert(Rf, LD, q, v0, v1);
+        warp_givens_insert(Rf, LD, q, v0, v1, dg0, dg1);
       }
     }
+    warp_givens_flush(Rf, LD, q, dg0, dg1);
     // ---- SVD of the q x q factor: rows of Rf -> sigma_j v_j^T
     warp_jacobi_rows(Rf, LD, q);
     double n0 = 0.0, n1 = 0.0;  // sigma_j^2 of rows j = lane, lane + 32
@@ -216,9 +249,13 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
     __syncwarp();
     if (tall) {
       // Q~(a, :) = A(a, :) K = sum_j (A(a, :) . u_j) u_j^T
+      RowReg nxt;
+      nxt.load(P, R);
       for (int a = 0; a < mk; ++a) {
+        const RowReg cur = nxt;
+        if (a + 1 < mk) nxt.load(P + (int64_t)(a + 1) * R, R);
         double v0, v1;
-        a_row(P + (int64_t)a * R, wk, HT, LDH, R, v0, v1);
+        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
         if (lane < R) Ab[lane] = v0;
         if (lane + 32 < R) Ab[lane + 32] = v1;
         __syncwarp();
@@ -263,13 +300,160 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
   }
 }
 
+// ------------------------------------------------------------------ polar, thread per patient (R <= 10)
+// Small ranks: the q x q algebra of one patient fits in registers (L = compile-time bound on R, rows
+// and columns beyond R or m_k are zero), so one thread runs one patient's QR, Jacobi and Q~ = A K /
+// K A with the register helpers of the smooth path (k_dense.cuh: givens_insert_reg, jacobi_rows_reg).
+// Same algebra as k_polar_warp; A's rows (tall) or columns (wide) are recomputed from P'_k (L1).
+template <int L>
+__global__ void __launch_bounds__(128) k_polar_thread(const int32_t* __restrict__ m, const int64_t* __restrict__ srow,
+                                                      int64_t K, int R, const double* __restrict__ Pp,
+                                                      const double* __restrict__ Wg, const double* __restrict__ Hg,
+                                                      double tau, double* __restrict__ Qt, int32_t* __restrict__ rank,
+                                                      unsigned long long* __restrict__ diag) {
+  __shared__ double Hs[L * L];  // H̄ zero-padded to L x L: Hs[s L + r] = H̄(s, r)
+  for (int x = threadIdx.x; x < L * L; x += blockDim.x) {
+    const int s = x / L, r = x - s * L;
+    Hs[x] = (s < R && r < R) ? Hg[s * R + r] : 0.0;
+  }
+  __syncthreads();
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = k < K;
+  const int mk = live ? m[k] : 0;
+  const bool tall = mk >= R;
+  const double* P = live ? Pp + srow[k] * R : Pp;
+  double w[L];
+#pragma unroll
+  for (int r = 0; r < L; ++r) w[r] = (live && r < R) ? Wg[k * R + r] : 0.0;
+  // A(a, s) = sum_r P'(a, r) w(r) H̄(s, r)
+  auto a_row = [&](int a, double (&v)[L]) {
+    double pw[L];
+#pragma unroll
+    for (int r = 0; r < L; ++r) pw[r] = r < R ? P[(int64_t)a * R + r] * w[r] : 0.0;
+#pragma unroll
+    for (int s = 0; s < L; ++s) {
+      double acc = 0.0;
+#pragma unroll
+      for (int r = 0; r < L; ++r) acc = fma(pw[r], Hs[s * L + r], acc);
+      v[s] = acc;
+    }
+  };
+  auto a_col = [&](int s, double (&v)[L]) {  // column s of A (m_k < L entries, zero beyond)
+#pragma unroll
+    for (int a = 0; a < L; ++a) {
+      double acc = 0.0;
+      if (a < mk)
+#pragma unroll
+        for (int r = 0; r < L; ++r)
+          if (r < R) acc = fma(P[(int64_t)a * R + r] * w[r], Hs[s * L + r], acc);
+      v[a] = acc;
+    }
+  };
+  double Rf[L][L];
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
+  if (tall) {
+    for (int a = 0; a < mk; ++a) {
+      double v[L];
+      a_row(a, v);
+      givens_insert_reg<L>(Rf, v);
+    }
+  } else if (mk > 0) {
+    for (int s = 0; s < R; ++s) {
+      double v[L];
+      a_col(s, v);
+      givens_insert_reg<L>(Rf, v);
+    }
+  }
+  jacobi_rows_reg<L>(Rf);  // warp-collective convergence vote: every lane takes part
+  double sg[L], smax = 0.0;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < L; ++i) s2 = fma(Rf[j][i], Rf[j][i], s2);
+    sg[j] = sqrt(s2);
+    smax = fmax(smax, sg[j]);
+  }
+  const int q = tall ? R : mk;
+  int rk = 0;
+  RatioDiag dg;
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const bool keep = smax > 0.0 && sg[j] > tau * smax;
+    if (smax > 0.0 && j < q) dg.note(sg[j] / smax, keep, tau);
+    rk += keep ? 1 : 0;
+    const double c = keep ? 1.0 / (sg[j] * sqrt(sg[j])) : 0.0;  // u_j = v_j / sqrt(sigma_j)
+#pragma unroll
+    for (int i = 0; i < L; ++i) Rf[j][i] *= c;
+  }
+  ratio_diag_warp(diag, D_POLAR_NEAR, dg);
+  if (!live) return;
+  rank[k] = mk > 0 ? rk : 0;
+  double* Q = Qt + srow[k] * R;
+  if (tall) {  // Q~(a, :) = sum_j (A(a, :) . u_j) u_j^T
+    for (int a = 0; a < mk; ++a) {
+      double v[L], d[L];
+      a_row(a, v);
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int x = 0; x < L; ++x) acc = fma(v[x], Rf[j][x], acc);
+        d[j] = acc;
+      }
+#pragma unroll
+      for (int s = 0; s < L; ++s) {
+        if (s < R) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < L; ++j) acc = fma(d[j], Rf[j][s], acc);
+          Q[(int64_t)a * R + s] = acc;
+        }
+      }
+    }
+  } else if (mk > 0) {  // Q~(:, s) = sum_j u_j (u_j . A(:, s))
+    for (int s = 0; s < R; ++s) {
+      double v[L], e[L];
+      a_col(s, v);
+#pragma unroll
+      for (int j = 0; j < L; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int a = 0; a < L; ++a) acc = fma(Rf[j][a], v[a], acc);
+        e[j] = acc;
+      }
+#pragma unroll
+      for (int a = 0; a < L; ++a) {
+        if (a < mk) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < L; ++j) acc = fma(e[j], Rf[j][a], acc);
+          Q[(int64_t)a * R + s] = acc;
+        }
+      }
+    }
+  }
+}
+
+template <int L>
+static void polar_thread_inst(Handle& h) {
+  const unsigned blocks = (unsigned)((h.K + 127) / 128);
+  k_polar_thread<L><<<blocks, 128, 0, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
+                                                  h.diag);
+}
+
 int launch_polar_warp(Handle& h) {
   if (h.K == 0) return 0;
   const int R = h.R;
+  if (R <= 4) { polar_thread_inst<4>(h); return 1; }    // small ranks: thread per patient, registers
+  if (R <= 6) { polar_thread_inst<6>(h); return 1; }
+  if (R <= 8) { polar_thread_inst<8>(h); return 1; }
+  if (R <= 10) { polar_thread_inst<10>(h); return 1; }
   int nwb = kPlainWarps;
-  auto smem_of = [&](int w) {
-    return sizeof(double) * ((size_t)R * odd_ld(R) + (size_t)w * 64 + (size_t)w * polar_warp_per_warp(R));
-  };
+  auto smem_of = [&](int w) { return sizeof(double) * ((size_t)R * odd_ld(R) + (size_t)w * polar_warp_per_warp(R)); };
   while (nwb > 1 && smem_of(nwb) > 227 * 1024) --nwb;
   const size_t smem = smem_of(nwb);
   max_smem_attr<k_polar_warp>(h);
@@ -309,10 +493,10 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
   const bool has0 = lane < R, has1 = lane + 32 < R;
   const int64_t nw = (int64_t)gridDim.x * kPlainWarps;
   int my_steps = 0;
-  auto t_row = [&](const double* Qa, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
+  auto t_row = [&](const RowReg& qr, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
     double s0 = 0.0, s1 = 0.0;
     for (int i = 0; i < R; ++i) {
-      const double qa = Qa[i];
+      const double qa = lane_pick(qr.x0, qr.x1, i);
       if (has0) s0 = fma(qa, Hs[i * R + lane], s0);
       if (has1) s1 = fma(qa, Hs[i * R + lane + 32], s1);
     }
@@ -324,11 +508,17 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
     const double* P = Pp + srow[k] * R;
     const double* Q = Qt + srow[k] * R;
     double f0 = 0.0, f1 = 0.0;  // F_W(k, r) = sum_a T(a, r) P'(a, r)
-    for (int a = 0; a < mk; ++a) {
-      double t0, t1;
-      t_row(Q + (int64_t)a * R, t0, t1);
-      if (has0) f0 = fma(t0, P[(int64_t)a * R + lane], f0);
-      if (has1) f1 = fma(t1, P[(int64_t)a * R + lane + 32], f1);
+    {
+      RowReg nq, np;
+      if (mk > 0) { nq.load(Q, R); np.load(P, R); }
+      for (int a = 0; a < mk; ++a) {
+        const RowReg cq = nq, cp = np;
+        if (a + 1 < mk) { nq.load(Q + (int64_t)(a + 1) * R, R); np.load(P + (int64_t)(a + 1) * R, R); }
+        double t0, t1;
+        t_row(cq, t0, t1);
+        if (has0) f0 = fma(t0, cp.x0, f0);
+        if (has1) f1 = fma(t1, cp.x1, f1);
+      }
     }
     double w0 = has0 ? W[k * R + lane] : 0.0, w1 = has1 ? W[k * R + lane + 32] : 0.0;
     double d0 = has0 ? DW[k * R + lane] : 0.0, d1 = has1 ? DW[k * R + lane + 32] : 0.0;
@@ -368,9 +558,13 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
     if (has0) { W[k * R + lane] = w0; DW[k * R + lane] = d0; }
     if (has1) { W[k * R + lane + 32] = w1; DW[k * R + lane + 32] = d1; }
     double* N = Nst + srow[k] * R;  // N_k = T S_k (new w̄_k)
+    RowReg nq;
+    if (mk > 0) nq.load(Q, R);
     for (int a = 0; a < mk; ++a) {
+      const RowReg cq = nq;
+      if (a + 1 < mk) nq.load(Q + (int64_t)(a + 1) * R, R);
       double t0, t1;
-      t_row(Q + (int64_t)a * R, t0, t1);
+      t_row(cq, t0, t1);
       if (has0) N[(int64_t)a * R + lane] = t0 * w0;
       if (has1) N[(int64_t)a * R + lane + 32] = t1 * w1;
     }
