@@ -82,6 +82,7 @@ size_t carve(Handle& h, char* base) {
   }
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   h.diag = c.take<unsigned long long>(kDiagSlots);
+  h.porder = c.take<int32_t>(h.K);
   h.steps = c.take<unsigned long long>(4);
   if (h.smooth) {
     const int G = h.sc_G;
@@ -394,6 +395,10 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       return rc == -2 ? fail(COPA_E_WORKSPACE, "internal: CSC chunk table exceeds its bound")
                       : cuda_fail(cudaGetLastError(), "CSC build");
     }
+  }
+  if (!polar_wide_ok(h) && plan_polar_order(h) != 0) {
+    delete H;
+    return cuda_fail(cudaGetLastError(), "polar order");
   }
   cudaMemcpyAsync(h.H, o->H0, sizeof(double) * RR, cudaMemcpyDefault, s);
   cudaMemcpyAsync(h.V, o->V0, sizeof(double) * (size_t)(h.J * h.R), cudaMemcpyDefault, s);

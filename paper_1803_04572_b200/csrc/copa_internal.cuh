@@ -88,6 +88,7 @@ struct Handle {
   void* layout_tmp;
   size_t layout_tmp_bytes = 0;
   int32_t* row_patient;  // non-smooth: [rows]
+  int32_t* porder;       // [K] patient order of the thread-per-patient polar (ascending m_k)
   // non-smooth: feature-major (CSC) copy of X for the deterministic F_V gather (k_plain.cu)
   int64_t* csc_ptr;          // [J+1]
   int32_t* csc_row;          // [nnz] row of each entry, column order
@@ -327,6 +328,8 @@ void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::
 bool polar_wide_ok(const Handle& h);
 // general path (k_plain.cu)
 int launch_polar_warp(Handle& h);
+bool polar_thread_ok(const Handle& h);
+int plan_polar_order(Handle& h);  // 0 ok, -1 CUDA error
 int launch_passB_warp(Handle& h);
 size_t csc_temp_bytes(const Handle& h);
 int build_csc(Handle& h);  // 0 ok, -1 CUDA error, -2 chunk table overflow

@@ -84,8 +84,7 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
   constexpr double eps = 2.220446049250313e-16 * (double)L;
   constexpr double tol2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    int rotated = 0;
-    double maxcos2 = 0.0;  // largest (x.y)^2 / (|x|^2 |y|^2) rotated away in this sweep
+    int rotated = 0, big = 0;  // big: some rotation of this sweep had (x.y)^2 > 1e-24 |x|^2 |y|^2
 #pragma unroll
     for (int rd = 0; rd < N - 1; ++rd) {
       double cs[N / 2], sn[N / 2];
@@ -105,7 +104,7 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
           }
           if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
             rotated = 1;
-            maxcos2 = fmax(maxcos2, (c * c) / (a * b));
+            big |= c * c > kJacobiDoneCos2 * (a * b);
             const double d = 0.5 * (b - a);
             const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
             cs[i] = rsqrt(fma(t, t, 1.0));
@@ -130,7 +129,7 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
     // converged when no pair needed a rotation, or when every rotation of this sweep was below
     // 1e-12 in cosine (the sweep has left the rows orthogonal to ~1e-24 (quadratic convergence); a
     // further sweep would only confirm it)
-    if (__all_sync(0xffffffffu, rotated == 0 || maxcos2 < kJacobiDoneCos2)) break;
+    if (__all_sync(0xffffffffu, rotated == 0 || !big)) break;
   }
 }
 

@@ -241,6 +241,29 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         const int a = 4 * ks + t, r = 8 * nt + g;
         offn[ks][nt] = (a < l && r < R) ? a * R + r : -1;
       }
+    // One tile (8 fibers of one patient sub-run) in flight: the loads and MMAs of the next tile are
+    // issued before the F_V read-modify-write of the pending one, so the MMA latency overlaps the
+    // shared-memory updates (a tile's MMAs never touch F_V; updates stay in tile order).
+    int pbase = scr;
+    double pcc[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) pcc[nt][0] = pcc[nt][1] = 0.0;
+    auto commit = [&]() {
+      int idx[NT];
+      double2 v[NT];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        // tile nt at base + 8 nt (an immediate offset); columns >= R of the last tile -> scratch
+        idx[nt] = (8 * nt + 8 <= R || 8 * nt + 2 * t < R) ? pbase + 8 * nt : scr;
+        v[nt] = *reinterpret_cast<const double2*>(Fs + idx[nt]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        v[nt].x += pcc[nt][0];
+        v[nt].y += pcc[nt][1];
+        *reinterpret_cast<double2*>(Fs + idx[nt]) = v[nt];
+      }
+    };
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
       mbar_wait(full + slot, phase);
@@ -280,65 +303,34 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
           for (int nt = 0; nt < NT; ++nt) bfr[ks][nt] = nbfr[ks][nt];
         if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
         if (lo >= hi) continue;
-        // TB tiles at a time while >= TB tiles remain, then single tiles (no MMAs on empty tiles).
-        // Tiles of one sub-run belong to one patient => distinct labels => distinct F_V rows, so
-        // all row loads of a batch may precede its stores.
-        auto run_tiles = [&](int tb, auto tbc) {
-          constexpr int NB = decltype(tbc)::value;
-          int base[NB];  // F_V slice index of this lane's (fiber, columns 2t, 2t + 1) in tile 0 (or scratch)
-          double av[NB][KS];
-          double cc[NB][NT][2];
+        for (int tb = lo; tb < hi; tb += 8) {
+          const int f = tb + g;
+          const bool ok = f < hi;
+          const int base = ok ? colS[f] + 2 * t : scr;  // fibers carry their F_V row offset (label - g Jg) RS
+          double av[KS];
 #pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const int f = tb + 8 * b + g;
-            const bool ok = f < hi;
-            base[b] = ok ? colS[f] + 2 * t : scr;  // fibers carry their F_V row offset (label - g Jg) RS
-#pragma unroll
-            for (int ks = 0; ks < KS; ++ks) {
-              const int a = 4 * ks + t;
-              av[b][ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
-            }
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) cc[b][nt][0] = cc[b][nt][1] = 0.0;
+          for (int ks = 0; ks < KS; ++ks) {
+            const int a = 4 * ks + t;
+            av[ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
           }
+          double cc[NT][2];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
+            for (int nt = 0; nt < NT; ++nt) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
+          commit();  // the previous tile (or a zero update of the scratch slot)
+          pbase = base;
 #pragma unroll
-              for (int nt = 0; nt < NT; ++nt) dmma(cc[b][nt][0], cc[b][nt][1], av[b][ks], bfr[ks][nt]);
-          // branch-free row updates: tile nt at base + 8 nt (an immediate offset); columns >= R of
-          // the last tile and lanes without a fiber go to the lane's scratch slot.
-          int idx[NB][NT];
-          double2 v[NB][NT];
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              idx[b][nt] = (8 * nt + 8 <= R || 8 * nt + 2 * t < R) ? base[b] + 8 * nt : scr;
-              v[b][nt] = *reinterpret_cast<const double2*>(Fs + idx[b][nt]);
-            }
-#pragma unroll
-          for (int b = 0; b < NB; ++b)
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              v[b][nt].x += cc[b][nt][0];
-              v[b][nt].y += cc[b][nt][1];
-              *reinterpret_cast<double2*>(Fs + idx[b][nt]) = v[b][nt];
-            }
-        };
-        int tb = lo;
-        for (; tb + 8 * (TB - 1) < hi; tb += 8 * TB) run_tiles(tb, std::integral_constant<int, TB>());
-        if (TB > 2 && tb + 8 < hi) {
-          run_tiles(tb, std::integral_constant<int, 2>());
-          tb += 16;
+          for (int nt = 0; nt < NT; ++nt) { pcc[nt][0] = cc[nt][0]; pcc[nt][1] = cc[nt][1]; }
         }
-        for (; tb < hi; tb += 8) run_tiles(tb, std::integral_constant<int, 1>());
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
       if (++slot == NSt) { slot = 0; phase ^= 1; }
     }
+    commit();  // the last tile
   }
   __syncthreads();
   double* out = FVpart + rng * (G * Jg) * (int64_t)R + (int64_t)grp * Jg * R;

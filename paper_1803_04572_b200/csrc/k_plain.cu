@@ -86,8 +86,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
   const double eps = 2.220446049250313e-16 * (double)q;
   const double tol2 = eps * eps;
   for (int sweep = 0; sweep < 40; ++sweep) {
-    int rotated = 0;
-    double maxcos2 = 0.0;
+    int rotated = 0, big = 0;
     for (int rd = 0; rd < N - 1; ++rd) {
       const int i = lane;
       if (i < N / 2) {
@@ -105,7 +104,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
           }
           if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
             rotated = 1;
-            maxcos2 = fmax(maxcos2, (c * c) / (a * b));
+            big |= c * c > kJacobiDoneCos2 * (a * b);
             const double d = 0.5 * (b - a);
             const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
             const double cs = rsqrt(fma(t, t, 1.0));
@@ -120,7 +119,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
       }
       __syncwarp();
     }
-    if (__all_sync(kFull, rotated == 0 || maxcos2 < kJacobiDoneCos2)) break;  // as jacobi_rows_reg
+    if (__all_sync(kFull, rotated == 0 || !big)) break;  // as jacobi_rows_reg
   }
 }
 
@@ -310,15 +309,17 @@ __global__ void __launch_bounds__(128) k_polar_thread(const int32_t* __restrict_
                                                       int64_t K, int R, const double* __restrict__ Pp,
                                                       const double* __restrict__ Wg, const double* __restrict__ Hg,
                                                       double tau, double* __restrict__ Qt, int32_t* __restrict__ rank,
-                                                      unsigned long long* __restrict__ diag) {
+                                                      unsigned long long* __restrict__ diag,
+                                                      const int32_t* __restrict__ order) {
   __shared__ double Hs[L * L];  // H̄ zero-padded to L x L: Hs[s L + r] = H̄(s, r)
   for (int x = threadIdx.x; x < L * L; x += blockDim.x) {
     const int s = x / L, r = x - s * L;
     Hs[x] = (s < R && r < R) ? Hg[s * R + r] : 0.0;
   }
   __syncthreads();
-  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const bool live = k < K;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = t < K;
+  const int64_t k = live ? (int64_t)order[t] : 0;  // patients in order of m_k: a warp's 32 loops have similar lengths
   const int mk = live ? m[k] : 0;
   const bool tall = mk >= R;
   const double* P = live ? Pp + srow[k] * R : Pp;
@@ -442,7 +443,25 @@ template <int L>
 static void polar_thread_inst(Handle& h) {
   const unsigned blocks = (unsigned)((h.K + 127) / 128);
   k_polar_thread<L><<<blocks, 128, 0, h.stream>>>(h.m, h.srow, h.K, h.R, h.Pp, h.W, h.H, h.o.rank_tol, h.Qt, h.rank,
-                                                  h.diag);
+                                                  h.diag, h.porder);
+}
+
+bool polar_thread_ok(const Handle& h) { return h.R <= 10; }
+
+// Patient order of the thread-per-patient polar: ascending m_k (stable), from the device m (init).
+int plan_polar_order(Handle& h) {
+  if (h.K == 0 || !polar_thread_ok(h)) return 0;
+  std::vector<int32_t> m((size_t)h.K), order((size_t)h.K);
+  if (cudaMemcpyAsync(m.data(), h.m, sizeof(int32_t) * m.size(), cudaMemcpyDeviceToHost, h.stream) != cudaSuccess ||
+      cudaStreamSynchronize(h.stream) != cudaSuccess)
+    return -1;
+  for (int64_t k = 0; k < h.K; ++k) order[(size_t)k] = (int32_t)k;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return m[(size_t)a] < m[(size_t)b]; });
+  if (cudaMemcpyAsync(h.porder, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, h.stream) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(h.stream) != cudaSuccess)
+    return -1;
+  return 0;
 }
 
 int launch_polar_warp(Handle& h) {
