@@ -78,13 +78,13 @@ size_t carve(Handle& h, char* base) {
   }
   {
     const int64_t RP = 8 * ((R + 7) / 8);
-    h.fh_warp = c.take<double>(h.smooth ? (int64_t)kPartBlocks * 4 * RP * RP : 1);
+    h.fh_warp = c.take<double>(h.fib ? (int64_t)kPartBlocks * 4 * RP * RP : 1);
   }
   h.fit_ring = c.take<double>(1024);  // device ring of per-iteration FIT values
   h.diag = c.take<unsigned long long>(kDiagSlots);
   h.porder = c.take<int32_t>(h.K);
   h.steps = c.take<unsigned long long>(4);
-  if (h.smooth) {
+  if (h.fib) {
     const int G = h.sc_G;
     h.Fcap = h.F + 8;
     h.Bk = c.take<double>(h.K * h.l * h.l);
@@ -110,6 +110,11 @@ size_t carve(Handle& h, char* base) {
     h.layout_tmp_bytes = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;  // per-group run lengths
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
+    if (h.rowproj) {
+      h.Bk = c.take<double>(h.K * h.l * h.l);
+      h.Prow = c.take<double>(h.rows * R);
+      h.Nrow = c.take<double>(h.rows * R);
+    }
     h.row_patient = c.take<int32_t>(h.rows);
     h.csc_ptr = c.take<int64_t>(h.J + 1);
     h.csc_row = c.take<int32_t>(h.nnz);
@@ -143,7 +148,7 @@ copa_status check_args(const copa_problem* p, const copa_options* o) {
     return fail(COPA_E_ARG, "tolerances must be >= 0");
   if (o->smooth_l < 0) return fail(COPA_E_ARG, "smooth_l < 0");
   if (o->smooth_l > 0) {
-    if (o->smooth_l > kMaxL) return fail(COPA_E_UNSUPPORTED, "smooth_l > 16 not supported");
+    if (o->smooth_l > kMaxL) return fail(COPA_E_UNSUPPORTED, "smooth_l > 64 not supported");
     if (o->smooth_degree < 0 || o->smooth_degree > kMaxDeg || o->smooth_degree >= o->smooth_l)
       return fail(COPA_E_ARG, "smooth_degree must be in [0, min(7, l-1)]");
     if (p->K_local > 0 && !p->visit_time) return fail(COPA_E_ARG, "smoothness requires visit times");
@@ -161,6 +166,8 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.dev) == cudaSuccess && sms > 0) h.sms = sms;
   else cudaGetLastError();
   h.smooth = o->smooth_l > 0;
+  h.fib = h.smooth && o->smooth_l <= kMaxFiberL;
+  h.rowproj = h.smooth && !h.fib;
   h.l = o->smooth_l;
   h.d = o->smooth_degree;
   h.K = p->K_local;
@@ -170,7 +177,7 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
   h.R = p->R;
   h.S = h.smooth ? h.K * h.l : h.rows;
   h.Jl = h.J;
-  if (h.smooth) {
+  if (h.fib) {
     plan_scatter(h);
     plan_passA(h);
   }
@@ -179,7 +186,7 @@ void fill_sizes(Handle& h, const copa_problem* p, const copa_options* o) {
 copa_status count_fibers(Handle& h, int64_t* F_out, size_t* cub_bytes) {
   *F_out = 0;
   *cub_bytes = 0;
-  if (!h.smooth) return COPA_OK;
+  if (!h.fib) return COPA_OK;
   size_t tb = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tb, (int64_t*)nullptr, (int64_t*)nullptr, (int)(h.K + 1));
   *cub_bytes = tb;
@@ -314,7 +321,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
   tm.mark("memset+validate");
-  if (h.smooth) {
+  if (h.fib) {
     if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
     launch_count_fibers(h, h.fiber_ptr, h.fhist);
     size_t tb = h.cub_temp_bytes;
@@ -389,6 +396,12 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
   } else {
     launch_row_patient(h);
     if (h.K == 0) cudaMemsetAsync(h.srow, 0, sizeof(int64_t), s);
+    if (h.rowproj) {  // state rows k l (srow), m_k = l'_k from the per-patient basis
+      if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
+      launch_basis(h);
+      cudaMemsetAsync(h.Prow, 0, sizeof(double) * (size_t)(h.rows * h.R), s);
+      cudaMemsetAsync(h.Nrow, 0, sizeof(double) * (size_t)(h.rows * h.R), s);
+    }
     const int rc = build_csc(h);
     if (rc != 0) {
       delete H;
@@ -788,7 +801,7 @@ copa_status copa_fit_workspace_size(const copa_problem* p, const copa_options* o
   fill_sizes(h, p, o);
   // upper bound on fibers from the host CSR: sum_k min(J, nnz_k)
   int64_t F = 0;
-  if (h.smooth) {
+  if (h.fib) {
     for (int64_t k = 0; k < p->K_local; ++k) {
       int64_t nk = p->row_ptr[p->patient_row_ptr[k + 1]] - p->row_ptr[p->patient_row_ptr[k]];
       F += nk < p->J ? nk : p->J;

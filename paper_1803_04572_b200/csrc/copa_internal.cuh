@@ -12,7 +12,8 @@
 namespace copa {
 
 constexpr int kMaxR = 64;       // rank limit (local arrays in the per-patient kernels)
-constexpr int kMaxL = 16;       // smooth_l limit
+constexpr int kMaxL = 64;       // smooth_l limit (row-projection path above kMaxFiberL)
+constexpr int kMaxFiberL = 16;  // smooth_l limit of the projected-fiber layout (k_fibers.cu, k_passA.cu)
 constexpr int kMaxDeg = 7;      // spline degree limit
 constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
@@ -38,6 +39,9 @@ struct Handle {
   int dev = 0;         // CUDA device of the handle (current device at init)
   int sms = 148;       // its multiprocessor count (queried)
   int smooth;          // smooth_l > 0
+  int fib;             // smooth with the projected-fiber layout (l <= kMaxFiberL)
+  int rowproj;         // smooth with l > kMaxFiberL: row passes + sparse M_k projection (k_rowproj.cu)
+  double *Prow, *Nrow; // rowproj: [rows x R] X_k V and C_k N'_k per visit row
   int l, d;            // basis size / degree (smooth)
   int64_t K, J, rows, nnz;
   int R;
@@ -333,7 +337,11 @@ int plan_polar_order(Handle& h);  // 0 ok, -1 CUDA error
 int launch_passB_warp(Handle& h);
 size_t csc_temp_bytes(const Handle& h);
 int build_csc(Handle& h);  // 0 ok, -1 CUDA error, -2 chunk table overflow
-int launch_scatter_csc(Handle& h);
+int launch_scatter_csc(Handle& h, const double* Nrows);
+// row-projection path (k_rowproj.cu): smooth l > kMaxFiberL
+void launch_basis_warp(Handle& h);
+int launch_rowproj_P(Handle& h);
+int launch_rowproj_N(Handle& h);
 int launch_polar_wide(Handle& h);
 int launch_passB_wide(Handle& h);
 

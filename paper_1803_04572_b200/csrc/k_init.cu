@@ -125,10 +125,10 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
                         int32_t* m, unsigned long long* diag) {
   int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (k >= K) return;
-  double Rm[kMaxL * kMaxL];
-  double a[kMaxL];
+  double Rm[kMaxFiberL * kMaxFiberL];
+  double a[kMaxFiberL];
   double N[kMaxDeg + 1];
-  for (int i = 0; i < l * kMaxL; ++i) Rm[i] = 0.0;
+  for (int i = 0; i < l * kMaxFiberL; ++i) Rm[i] = 0.0;
   int64_t r0 = prp[k], r1 = prp[k + 1];
   double t1 = times[r0], tn = times[r1 - 1];
   double* B = Bk + k * (int64_t)l * l;
@@ -141,13 +141,13 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
     int mu = spline_eval(times[i], t1, tn, l, d, N);
     for (int b = 0; b < l; ++b) a[b] = 0.0;
     for (int r = 0; r <= d; ++r) a[mu - d + r] = N[r];
-    givens_insert(Rm, kMaxL, a, l);
+    givens_insert(Rm, kMaxFiberL, a, l);
   }
-  jacobi_rows(Rm, kMaxL, l);
-  double sig[kMaxL], smax = 0.0;
+  jacobi_rows(Rm, kMaxFiberL, l);
+  double sig[kMaxFiberL], smax = 0.0;
   for (int j = 0; j < l; ++j) {
     double s = 0.0;
-    for (int i = 0; i < l; ++i) s = fma(Rm[j * kMaxL + i], Rm[j * kMaxL + i], s);
+    for (int i = 0; i < l; ++i) s = fma(Rm[j * kMaxFiberL + i], Rm[j * kMaxFiberL + i], s);
     sig[j] = sqrt(s);
     smax = fmax(smax, sig[j]);
   }
@@ -157,7 +157,7 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
     ratio_diag_commit(diag, D_BASIS_NEAR, dg);
   }
   // keep in descending sigma order (stable): selection by repeated max
-  int used[kMaxL];
+  int used[kMaxFiberL];
   for (int j = 0; j < l; ++j) used[j] = 0;
   int c = 0;
   for (int it = 0; it < l; ++it) {
@@ -167,7 +167,7 @@ __global__ void k_basis(const int64_t* prp, const double* times, int64_t K, int 
     used[best] = 1;
     if (!(smax > 0.0) || !(sig[best] > tau * smax)) break;
     double inv2 = 1.0 / (sig[best] * sig[best]);
-    for (int i = 0; i < l; ++i) B[i * l + c] = Rm[best * kMaxL + i] * inv2;
+    for (int i = 0; i < l; ++i) B[i * l + c] = Rm[best * kMaxFiberL + i] * inv2;
     ++c;
   }
   for (int cc = c; cc < l; ++cc)
@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(64) k_basis_reg(const int64_t* prp, const doub
 
 void launch_basis(Handle& h) {
   if (h.K == 0) return;
+  if (h.rowproj) { launch_basis_warp(h); return; }
   const unsigned blocks = (unsigned)((h.K + 63) / 64);
   if (h.l == 7) {
     k_basis_reg<7><<<blocks, 64, 0, h.stream>>>(h.p.patient_row_ptr, h.p.visit_time, h.K, h.d, h.o.basis_tol, h.Bk, h.m, h.diag);

@@ -33,8 +33,10 @@ __global__ void k_spmm_rows(const int64_t* rp, const int32_t* col, const double*
 
 int launch_spmm(Handle& h) {
   if (h.K == 0) return 0;
-  if (h.smooth) {
+  if (h.fib) {
     launch_spmm_fibers(h);
+  } else if (h.rowproj) {
+    return launch_rowproj_P(h);  // X_k V per visit row, then B_k^T (M_k^T P_k) (k_rowproj.cu)
   } else {
     int64_t n = h.rows * h.R;
     k_spmm_rows<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows, h.R, h.V,
@@ -261,9 +263,9 @@ __global__ void k_scatter_fibers(const int64_t* gptr, int G, const int32_t* fibe
   for (int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); k < K; k += nwarps) {
     const int mk = m[k];
     const double* N = Nst + srow[k] * R;
-    double n0[kMaxL], n1[kMaxL];
+    double n0[kMaxFiberL], n1[kMaxFiberL];
     const int r0 = lane, r1 = lane + 32;
-    for (int a = 0; a < kMaxL; ++a) {
+    for (int a = 0; a < kMaxFiberL; ++a) {
       n0[a] = (a < mk && r0 < R) ? N[a * R + r0] : 0.0;
       n1[a] = (a < mk && r1 < R) ? N[a * R + r1] : 0.0;
     }
@@ -284,7 +286,8 @@ __global__ void k_scatter_fibers(const int64_t* gptr, int G, const int32_t* fibe
 }
 
 int launch_scatter(Handle& h) {
-  if (!h.smooth) return launch_scatter_csc(h);  // deterministic gather over the CSC copy (k_plain.cu)
+  if (!h.smooth) return launch_scatter_csc(h, h.Nst);  // deterministic gather over the CSC copy (k_plain.cu)
+  if (h.rowproj) return launch_rowproj_N(h) + launch_scatter_csc(h, h.Nrow);  // C_k N'_k per row, then gather
   cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
   if (h.K == 0) return 0;
   if (scatter_smem_ok(h)) return launch_scatter_fibers(h);

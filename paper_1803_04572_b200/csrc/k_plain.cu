@@ -756,14 +756,14 @@ __global__ void k_sum_chunks(int64_t J, int R, const double* __restrict__ part,
   FV[x] = s;
 }
 
-int launch_scatter_csc(Handle& h) {
+int launch_scatter_csc(Handle& h, const double* Nrows) {
   if (h.csc_chunks == 0) {
     cudaMemsetAsync(h.FV, 0, sizeof(double) * (size_t)(h.J * h.R), h.stream);
     return 0;
   }
   int64_t blocks = (h.csc_chunks + 7) / 8;
   if (blocks > (int64_t)h.sms * 8) blocks = (int64_t)h.sms * 8;
-  k_scatter_csc<<<(unsigned)blocks, 256, 0, h.stream>>>(h.csc_chunk, h.csc_chunks, h.R, h.csc_row, h.csc_val, h.Nst,
+  k_scatter_csc<<<(unsigned)blocks, 256, 0, h.stream>>>(h.csc_chunk, h.csc_chunks, h.R, h.csc_row, h.csc_val, Nrows,
                                                         h.csc_part);
   const int64_t n = h.J * h.R;
   k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.J, h.R, h.csc_part,

@@ -122,6 +122,11 @@ CONFIGS = {
 CONFIGS["large_plain"] = dataclasses.replace(
     CONFIGS["large"], name="large_plain", smooth_l=0,
     baseline=CONFIGS["large"].baseline + " [SURVEY 8(f) N4 variant: no smoothness]")
+#   N2 smoothness in the paper's regime: Medium's data with l = 33 basis functions at R = 15 (the
+#   paper's CHOA setting), l > R.
+CONFIGS["medium_l33"] = dataclasses.replace(
+    CONFIGS["medium"], name="medium_l33", smooth_l=33,
+    baseline=CONFIGS["medium"].baseline + " [SURVEY 8(f) N2 variant: l = 33 basis functions, PAPER.md:584]")
 CONFIGS["small_unconstrained"] = dataclasses.replace(
     CONFIGS["small"], name="small_unconstrained", con_H=(NONE, 0.0), con_W=(NONE, 0.0), con_V=(NONE, 0.0),
     baseline=CONFIGS["small"].baseline + " [SURVEY 8(f) N4 variant: unconstrained, identity prox]")

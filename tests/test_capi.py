@@ -59,7 +59,7 @@ def _structs(copa, R=5, J=10, K=2, smooth=0, kind_V=1, param_V=0.0, admm=5, admm
     ({"kind_V": 7}, -1),                 # unknown constraint
     ({"kind_V": 2, "param_V": -1.0}, -1),  # negative lambda
     ({"kind_V": 4, "param_V": 0.0}, -1),   # mu must be > 0
-    ({"smooth": 17}, -9),                # l beyond the limit
+    ({"smooth": 65}, -9),                # l beyond the limit (64)
     ({"admm_tol": -1.0}, -1),            # negative inner-stop tolerance
 ])
 def test_host_side_validation(copa, kw, status):

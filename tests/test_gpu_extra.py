@@ -193,7 +193,8 @@ def test_fiber_build_dense_rows_and_wide_patients(copa):
 
 
 @pytest.mark.parametrize("R,l,J", [(3, 0, 120), (16, 0, 120), (8, 5, 120), (24, 9, 120), (40, 12, 120), (20, 16, 120),
-                                   (64, 16, 120), (20, 7, 4000), (40, 7, 30000), (8, 12, 120)])
+                                   (64, 16, 120), (20, 7, 4000), (40, 7, 30000), (8, 12, 120), (10, 20, 120),
+                                   (40, 48, 300), (5, 60, 120)])
 def test_shape_sweep(copa, R, l, J):
     """Kernel template/limit coverage: tall and wide polar, MMA tile counts, smooth l up to 16, and
     pass B's label groups: J = 4000 needs G = 4 F_V slices; J = 30000 (R = 40) fits no smem slice

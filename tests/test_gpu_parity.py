@@ -94,16 +94,20 @@ def test_constraint_variants(copa_mod, name, K, cons):
 # for I_k >= 40, the wide factorisation otherwise) and unconstrained PARAFAC2
 # (identity prox on every factor).
 N4_CASES = [("large_plain", 1200), ("small_unconstrained", 3000)]
+# N2: smoothness with l = 33 > R = 15, the row-projection path
+# (k_rowproj.cu: sparse M_k recomputed from the visit times, B_k per patient)
+N2_CASES = [("medium_l33", 3000)]
 
 
-@pytest.mark.parametrize("name,K", N4_CASES)
+@pytest.mark.parametrize("name,K", N4_CASES + N2_CASES)
 def test_n4_one_iteration_factors(copa_mod, name, K):
     p, g, o = _pair(copa_mod, name, K)
     fg = g.iterate(1)
     fo = o.iterate(1)
     H, V, W = [t.cpu().numpy() for t in g.factors()]
-    errs = {"H": rel(H, o.H), "V": rel(V, o.V), "W": rel(W, o.W), "Q": rel(g.debug_state()["Qt"].cpu().numpy(), o.Q),
-            "U": rel(g.U().cpu().numpy(), o.U_all())}
+    errs = {"H": rel(H, o.H), "V": rel(V, o.V), "W": rel(W, o.W), "U": rel(g.U().cpu().numpy(), o.U_all())}
+    if p.cfg.smooth_l == 0:  # Q~ itself is basis-dependent under smoothness (reading R-spline-5)
+        errs["Q"] = rel(g.debug_state()["Qt"].cpu().numpy(), o.Q)
     print(f"[margin] {name}: FIT {abs(fg[0] - fo[0]):.2e} " + " ".join(f"{k} {v:.2e}" for k, v in errs.items()))
     assert abs(fg[0] - fo[0]) <= 1e-9
     for k, e in errs.items():
@@ -113,7 +117,7 @@ def test_n4_one_iteration_factors(copa_mod, name, K):
           f"max-dropped {st['polar_max_dropped']:.2e}")
 
 
-@pytest.mark.parametrize("name,K", N4_CASES)
+@pytest.mark.parametrize("name,K", N4_CASES + N2_CASES)
 def test_n4_fit_after_ten_iterations(copa_mod, name, K):
     p, g, o = _pair(copa_mod, name, K)
     fg = g.iterate(10)
