@@ -149,7 +149,11 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
   const int l = LT ? LT : l_;
   const int RS = RT ? ((RT + 1) & ~1) : RS_;
   extern __shared__ __align__(128) unsigned char smraw[];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // thread index in a register the compiler cannot rebuild from SR_TID (it otherwise re-reads the
+  // special register inside the per-patient loop)
+  int tid;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+  const int lane = tid & 31, w = tid >> 5;
   const int grp = blockIdx.x % G;
   const int64_t rng = blockIdx.x / G;
   const SlotGeom sg = slot_geom(FB, PB, l, R);
@@ -229,18 +233,20 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     // all R columns of those F_V rows: no two warps write the same row. Its sub-run of each run
     // comes from the staged offsets; tiles of 8 fibers (one patient, distinct labels) run TB at a
     // time: loads and MMAs of the batch first, then the read-modify-writes.
-    const int g = lane >> 2, t = lane & 3;
+    const int ln = lane;
+    const int g = ln >> 2, t = ln & 3;
     const int per = l * R;
-    const int scr = (int)Jg * RS + w * kScrD + 2 * lane;  // this lane's scratch slot (index into Fs; + 8 nt stays
-                                                          // inside the warp's kScrD doubles)
-    int offn[KS][NT];   // lane's B-fragment offsets inside an N_k block (-1: padding)
+    const int scr = (int)Jg * RS + w * kScrD + 2 * ln;  // this lane's scratch slot (index into Fs; + 8 nt stays
+                                                        // inside the warp's kScrD doubles)
+    // B fragment B[t][g] = N(a = 4 ks + t, r = 8 nt + g) at nb0 + 4 ks R + 8 nt of a patient's N block
+    // (compile-time offsets for the configured shapes); lanes outside (a < l, r < R) load nothing
+    const int nb0 = t * R + g;
+    unsigned nok = 0;  // bit (ks NT + nt): the lane's fragment is inside N
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int a = 4 * ks + t, r = 8 * nt + g;
-        offn[ks][nt] = (a < l && r < R) ? a * R + r : -1;
-      }
+      for (int nt = 0; nt < NT; ++nt)
+        if (4 * ks + t < l && 8 * nt + g < R) nok |= 1u << (ks * NT + nt);
     // One tile (8 fibers of one patient sub-run) in flight: the loads and MMAs of the next tile are
     // issued before the F_V read-modify-write of the pending one, so the MMA latency overlaps the
     // shared-memory updates (a tile's MMAs never touch F_V; updates stay in tile order).
@@ -285,11 +291,12 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
         const int64_t rs = gp[p];
         lo_ = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
         hi_ = (int)(min(rs + wo[p * kWoS + w + 1], f1) - f0);
-        const double* Np = nS + (int64_t)p * per;
+        const double* Np = nS + (int64_t)p * per + nb0;
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) b[ks][nt] = offn[ks][nt] >= 0 ? Np[offn[ks][nt]] : 0.0;
+          for (int nt = 0; nt < NT; ++nt)
+            b[ks][nt] = (nok >> (ks * NT + nt)) & 1u ? Np[4 * ks * R + 8 * nt] : 0.0;
       };
       int nlo = 0, nhi = 0;
       double nbfr[KS][NT];
@@ -303,16 +310,15 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
           for (int nt = 0; nt < NT; ++nt) bfr[ks][nt] = nbfr[ks][nt];
         if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
         if (lo >= hi) continue;
+#pragma unroll 2
         for (int tb = lo; tb < hi; tb += 8) {
           const int f = tb + g;
           const bool ok = f < hi;
           const int base = ok ? colS[f] + 2 * t : scr;  // fibers carry their F_V row offset (label - g Jg) RS
+          const double* vf = valS + f * l + t;
           double av[KS];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
-            const int a = 4 * ks + t;
-            av[ks] = (ok && a < l) ? valS[f * l + a] : 0.0;
-          }
+          for (int ks = 0; ks < KS; ++ks) av[ks] = (ok && 4 * ks + t < l) ? vf[4 * ks] : 0.0;
           double cc[NT][2];
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) cc[nt][0] = cc[nt][1] = 0.0;

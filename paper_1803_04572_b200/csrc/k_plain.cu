@@ -96,7 +96,8 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
           double* xp = Rf + p * LD;
           double* xr = Rf + r * LD;
           double a = 0.0, b = 0.0, c = 0.0;
-          for (int x = 0; x < q; ++x) {
+#pragma unroll 8
+          for (int x = 0; x < q; ++x) {  // unrolled: the shared-memory loads of 8 elements in flight
             const double u = xp[x], v = xr[x];
             a = fma(u, u, a);
             b = fma(v, v, b);
@@ -109,6 +110,7 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
             const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
             const double cs = rsqrt(fma(t, t, 1.0));
             const double sn = cs * t;
+#pragma unroll 8
             for (int x = 0; x < q; ++x) {
               const double u = xp[x], v = xr[x];
               xp[x] = fma(cs, u, -sn * v);
