@@ -60,6 +60,7 @@ size_t carve(Handle& h, char* base) {
   h.VtV = c.take<double>(RR);
   h.LW = c.take<double>(RR);
   h.GWi = c.take<double>(RR);
+  h.HT = c.take<double>(RR);
   h.comm2 = c.take<double>(h.J * R + 2 * RR);
   if (base) { h.FV = h.comm2; h.WtW = h.comm2 + h.J * R; h.M = h.WtW + RR; }
   h.V = c.take<double>(h.J * R);

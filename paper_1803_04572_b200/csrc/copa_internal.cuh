@@ -22,6 +22,8 @@ constexpr int kMaxGroups = 8;     // label groups (fiber streams) of the smooth 
 constexpr int kWoS = 16;
 constexpr int64_t kCscChunk = 512;  // entries per chunk of the non-smooth F_V gather          // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
 
+constexpr double kJacobiNegl2 = 1e-30;  // see the note at jacobi_rows
+
 enum ErrBits : int { ERR_CHOL = 1, ERR_DEGEN = 2, ERR_NONFINITE = 4, ERR_SHAPE = 8, ERR_INPUT_NONFINITE = 16 };
 
 // Rank-cut diagnostics (copa_stats; SURVEY 8(c) parity protocol): counts, and ratios as the bit
@@ -52,6 +54,7 @@ struct Handle {
   int* err;
   double* scal;
   double *H, *DH, *FH, *HtH, *VtV, *LW, *GWi, *partial;  // GWi = (G_W + rho I)^-1
+  double* HT;          // H̄^T (general polar, refreshed per launch)
   double* fh_warp;     // smooth: per-warp F_H partials of the polar kernel [kPartBlocks x 4 x (8 ceil(R/8))^2]
   double *comm2;       // [FV (J R) | WtW (R R) | M (R R)]
   double *FV, *WtW, *M;
@@ -144,6 +147,21 @@ __device__ __forceinline__ double prox(int kind, double param, double rho, doubl
   }
 }
 
+// Jacobi rotation of two rows x, y (a = x.x, b = y.y, c = x.y) that makes them orthogonal:
+// x <- cs x - sn y, y <- sn x + cs y with tan(2 theta) = 2c / (b - a) (Hestenes). With d = (b - a)/2,
+// h = sqrt(c^2 + d^2), u = |d| / h = cos(2 theta): cs = sqrt((1 + u)/2) = (1 + u) q and
+// sn = sign(d) c / (2 h cs) = sign(d) c (1/h) q with q = 1/sqrt(2 (1 + u)) — two reciprocal square
+// roots and no division or square root (the FP64 division and square root are long instruction
+// sequences; this is the same rotation as t = sign(d) c / (|d| + h), cs = 1/sqrt(1 + t^2), sn = cs t).
+__device__ __forceinline__ void jacobi_rot(double a, double b, double c, double& cs, double& sn) {
+  const double d = 0.5 * (b - a);
+  const double rh = rsqrt(fma(c, c, d * d));
+  const double u = fabs(d) * rh;
+  const double q = rsqrt(fma(2.0, u, 2.0));
+  cs = (1.0 + u) * q;
+  sn = copysign(1.0, d) * c * rh * q;
+}
+
 // Insert row a[0..q) into the upper-triangular Rf (q x q, row-major, stride ld) with Givens
 // rotations, so that Rf^T Rf accumulates a a^T without ever forming a Gram matrix.
 __device__ __forceinline__ void givens_insert(double* Rf, int ld, double* a, int q) {
@@ -162,11 +180,20 @@ __device__ __forceinline__ void givens_insert(double* Rf, int ld, double* a, int
   }
 }
 
+// Rows of a Jacobi sweep whose squared norm is below kJacobiNegl2 times the total (the trace of
+// the Gram, invariant under the rotations) are rounding residue of a rank-deficient factor: sigma_j
+// below 1e-15 sqrt(trace) is far under both rank cuts (1e-10, 1e-6 sigma_1), and rotating them
+// changes the other rows by ~1e-15 relative. They are left alone — otherwise residue rows keep an
+// O(1) cosine to each other and the sweep never converges (all 40 sweeps for a rank-deficient
+// tall factor, and a warp waits for its slowest patient).
 // One-sided (Hestenes) Jacobi on the q row-vectors of Wm (q x q, stride ld): rotates pairs of
 // rows until mutually orthogonal. Afterwards row j = sigma_j v_j where v_j are the right singular
 // vectors of the upper-triangular factor whose rows were given (polar kernel).
 __device__ __forceinline__ void jacobi_rows(double* Wm, int ld, int q) {
   const double tol = 2.220446049250313e-16 * (double)q;
+  double tr = 0.0;  // trace of the Gram (invariant): residue-row threshold
+  for (int i = 0; i < q * ld; ++i) tr = fma(Wm[i], Wm[i], tr);
+  const double negl = kJacobiNegl2 * tr;
   for (int sweep = 0; sweep < 60; ++sweep) {
     int rotated = 0;
     for (int p = 0; p < q - 1; ++p) {
@@ -178,13 +205,11 @@ __device__ __forceinline__ void jacobi_rows(double* Wm, int ld, int q) {
           b = fma(y, y, b);
           c = fma(x, y, c);
         }
-        if (a == 0.0 || b == 0.0) continue;
+        if (a <= negl || b <= negl) continue;
         if (fabs(c) <= tol * sqrt(a * b)) continue;
         rotated = 1;
-        double zeta = (b - a) / (2.0 * c);
-        double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-        double cs = rsqrt(fma(t, t, 1.0));
-        double sn = cs * t;
+        double cs, sn;
+        jacobi_rot(a, b, c, cs, sn);
         for (int i = 0; i < q; ++i) {
           double x = Wm[p * ld + i], y = Wm[r * ld + i];
           Wm[p * ld + i] = cs * x - sn * y;

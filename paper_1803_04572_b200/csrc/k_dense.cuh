@@ -73,9 +73,8 @@ __device__ __forceinline__ void givens_insert_reg(double (&Rf)[L][L], double (&c
 // One-sided Jacobi on the rows of Wm (L x L, registers) until mutually orthogonal. Round-robin
 // (tournament) ordering: every round rotates floor(L/2) disjoint row pairs, whose dot products and
 // rotation parameters are independent (instruction-level parallelism in the thread-per-patient
-// layout); a sweep (L-1 or L rounds) meets every pair once. Rotation of rows x, y with a = x.x,
-// b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
-// sn = cs t; x <- cs x - sn y, y <- sn x + cs y (the classical zeta = d/c form, Hestenes).
+// layout); a sweep (L-1 or L rounds) meets every pair once. Each rotation is jacobi_rot()
+// (copa_internal.cuh: Hestenes' angle from two reciprocal square roots).
 constexpr double kJacobiDoneCos2 = 1e-24;  // (1e-12)^2, see jacobi_rows_reg
 
 template <int L>
@@ -83,6 +82,12 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
   constexpr int N = (L % 2) ? L + 1 : L;  // players, with a dummy (index L) when L is odd
   constexpr double eps = 2.220446049250313e-16 * (double)L;
   constexpr double tol2 = eps * eps;
+  double tr = 0.0;  // trace of the Gram (invariant under the rotations): residue-row threshold
+#pragma unroll
+  for (int p = 0; p < L; ++p)
+#pragma unroll
+    for (int x = 0; x < L; ++x) tr = fma(Wm[p][x], Wm[p][x], tr);
+  const double negl = kJacobiNegl2 * tr;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0, big = 0;  // big: some rotation of this sweep had (x.y)^2 > 1e-24 |x|^2 |y|^2
 #pragma unroll
@@ -102,13 +107,10 @@ __device__ __forceinline__ void jacobi_rows_reg(double (&Wm)[L][L]) {
             b = fma(Wm[q][x], Wm[q][x], b);
             c = fma(Wm[p][x], Wm[q][x], c);
           }
-          if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+          if (a > negl && b > negl && c * c > tol2 * (a * b)) {
             rotated = 1;
             big |= c * c > kJacobiDoneCos2 * (a * b);
-            const double d = 0.5 * (b - a);
-            const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
-            cs[i] = rsqrt(fma(t, t, 1.0));
-            sn[i] = cs[i] * t;
+            jacobi_rot(a, b, c, cs[i], sn[i]);
           }
         }
       }

@@ -77,14 +77,18 @@ __device__ __forceinline__ void warp_givens_flush(double* Rf, int LD, int q, dou
 }
 
 // One-sided Jacobi on the q rows of Rf until mutually orthogonal: round-robin (tournament)
-// ordering, lane i rotates the i-th disjoint pair of a round. Rotation of rows x, y with
-// a = x.x, b = y.y, c = x.y: d = (b - a)/2, t = sign(d) c / (|d| + sqrt(c^2 + d^2)), cs = 1/sqrt(1 + t^2),
-// sn = cs t (Hestenes; same rule as the thread-per-patient kernels).
+// ordering, lane i rotates the i-th disjoint pair of a round with jacobi_rot() (copa_internal.cuh).
 __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
   const int lane = threadIdx.x & 31;
   const int N = (q & 1) ? q + 1 : q;
   const double eps = 2.220446049250313e-16 * (double)q;
   const double tol2 = eps * eps;
+  double tr = 0.0;  // trace of the Gram (invariant): residue-row threshold (kJacobiNegl2)
+  for (int x = lane; x < q; x += 32)
+    for (int y = 0; y < q; ++y) tr = fma(Rf[x * LD + y], Rf[x * LD + y], tr);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(kFull, tr, o);
+  const double negl = kJacobiNegl2 * tr;
   for (int sweep = 0; sweep < 40; ++sweep) {
     int rotated = 0, big = 0;
     for (int rd = 0; rd < N - 1; ++rd) {
@@ -103,13 +107,11 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
             b = fma(v, v, b);
             c = fma(u, v, c);
           }
-          if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+          if (a > negl && b > negl && c * c > tol2 * (a * b)) {
             rotated = 1;
             big |= c * c > kJacobiDoneCos2 * (a * b);
-            const double d = 0.5 * (b - a);
-            const double t = copysign(1.0, d) * c / (fabs(d) + sqrt(fma(c, c, d * d)));
-            const double cs = rsqrt(fma(t, t, 1.0));
-            const double sn = cs * t;
+            double cs, sn;
+            jacobi_rot(a, b, c, cs, sn);
 #pragma unroll 8
             for (int x = 0; x < q; ++x) {
               const double u = xp[x], v = xr[x];
@@ -156,21 +158,15 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
                                                                  const int64_t* __restrict__ srow, int64_t K, int R,
                                                                  const double* __restrict__ Pp,
                                                                  const double* __restrict__ Wg,
-                                                                 const double* __restrict__ Hg, double tau,
+                                                                 const double* __restrict__ HT, double tau,
                                                                  double* __restrict__ Qt, int32_t* __restrict__ rank,
                                                                  unsigned long long* __restrict__ diag) {
   extern __shared__ double smp[];
-  const int LD = odd_ld(R), LDH = odd_ld(R);
-  double* HT = smp;                       // H̄^T: HT[r LDH + s] = H̄(s, r)
+  const int LD = odd_ld(R), LDH = R;  // HT: H̄^T in global memory (L1-resident), HT[r R + s] = H̄(s, r)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwb = blockDim.x >> 5;  // warps of this block (fewer at large R: shared memory)
-  double* Rf = HT + R * LDH + (size_t)wib * polar_warp_per_warp(R);
+  double* Rf = smp + (size_t)wib * polar_warp_per_warp(R);
   double* Ab = Rf + (size_t)R * LD;
-  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
-    const int s = x / R, r = x - s * R;
-    HT[r * LDH + s] = Hg[x];
-  }
-  __syncthreads();
   const int64_t nw = (int64_t)gridDim.x * nwb;
   for (int64_t k = blockIdx.x * (int64_t)nwb + wib; k < K; k += nw) {
     const int mk = m[k];
@@ -466,6 +462,11 @@ int plan_polar_order(Handle& h) {
   return 0;
 }
 
+__global__ void k_transpose(const double* __restrict__ A, int R, double* __restrict__ AT) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < R * R) AT[(x % R) * R + x / R] = A[x];
+}
+
 int launch_polar_warp(Handle& h) {
   if (h.K == 0) return 0;
   const int R = h.R;
@@ -474,7 +475,7 @@ int launch_polar_warp(Handle& h) {
   if (R <= 8) { polar_thread_inst<8>(h); return 1; }
   if (R <= 10) { polar_thread_inst<10>(h); return 1; }
   int nwb = kPlainWarps;
-  auto smem_of = [&](int w) { return sizeof(double) * ((size_t)R * odd_ld(R) + (size_t)w * polar_warp_per_warp(R)); };
+  auto smem_of = [&](int w) { return sizeof(double) * (size_t)w * polar_warp_per_warp(R); };
   while (nwb > 1 && smem_of(nwb) > 227 * 1024) --nwb;
   const size_t smem = smem_of(nwb);
   max_smem_attr<k_polar_warp>(h);
@@ -483,9 +484,10 @@ int launch_polar_warp(Handle& h) {
   int64_t blocks = (h.K + nwb - 1) / nwb;
   const int64_t cap = (int64_t)h.sms * std::max(per_sm, 1);
   if (blocks > cap) blocks = cap;
-  k_polar_warp<<<(unsigned)blocks, 32 * nwb, smem, h.stream>>>(h.m, h.srow, h.K, R, h.Pp, h.W, h.H, h.o.rank_tol,
+  k_transpose<<<(unsigned)((R * R + 255) / 256), 256, 0, h.stream>>>(h.H, R, h.HT);
+  k_polar_warp<<<(unsigned)blocks, 32 * nwb, smem, h.stream>>>(h.m, h.srow, h.K, R, h.Pp, h.W, h.HT, h.o.rank_tol,
                                                                h.Qt, h.rank, h.diag);
-  return 1;
+  return 2;
 }
 
 // ------------------------------------------------------------------ W pass (warp per patient)

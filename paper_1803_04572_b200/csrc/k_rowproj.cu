@@ -80,6 +80,12 @@ __global__ void __launch_bounds__(32 * kRpWarps) k_basis_warp(const int64_t* __r
     {
       const int N = (l & 1) ? l + 1 : l;
       const double eps = 2.220446049250313e-16 * (double)l, tol2 = eps * eps;
+      double tr = 0.0;  // trace of the Gram (invariant): residue-row threshold (kJacobiNegl2)
+      for (int x = lane; x < l; x += 32)
+        for (int y = 0; y < l; ++y) tr = fma(Rm[x * LD + y], Rm[x * LD + y], tr);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(kFullR, tr, o);
+      const double negl = kJacobiNegl2 * tr;
       for (int sweep = 0; sweep < 40; ++sweep) {
         int rotated = 0;
         for (int rd = 0; rd < N - 1; ++rd) {
@@ -91,11 +97,10 @@ __global__ void __launch_bounds__(32 * kRpWarps) k_basis_warp(const int64_t* __r
               double* xr = Rm + r * LD;
               double a = 0.0, b = 0.0, c = 0.0;
               for (int x = 0; x < l; ++x) { a = fma(xp[x], xp[x], a); b = fma(xr[x], xr[x], b); c = fma(xp[x], xr[x], c); }
-              if (a != 0.0 && b != 0.0 && c * c > tol2 * (a * b)) {
+              if (a > negl && b > negl && c * c > tol2 * (a * b)) {
                 rotated = 1;
-                const double dd = 0.5 * (b - a);
-                const double t = copysign(1.0, dd) * c / (fabs(dd) + sqrt(fma(c, c, dd * dd)));
-                const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
+                double cs, sn;
+                jacobi_rot(a, b, c, cs, sn);
                 for (int x = 0; x < l; ++x) {
                   const double u = xp[x], v = xr[x];
                   xp[x] = fma(cs, u, -sn * v);

@@ -99,6 +99,32 @@ N4_CASES = [("large_plain", 1200), ("small_unconstrained", 3000)]
 N2_CASES = [("medium_l33", 3000)]
 
 
+def _q_parity(p, Qg, o):
+    """Q~_k parity with the conditioning of the partial isometry: a kept direction
+    with sigma_r = rho sigma_1 is determined only to ~eps / rho, so patients whose smallest kept
+    ratio rho is below 1e-6 are checked against that first-order bound (x 1e3) one by one, and the
+    rest, stacked, at north_star's 1e-9. Returns the stacked error of the well-conditioned patients."""
+    from tests.helpers import dense_slices
+    Xs = dense_slices(p)
+    R = p.cfg.R
+    good_g, good_o = [], []
+    n_ill = 0
+    for k in range(p.K):
+        A = Xs[k] @ p.V0[:, :R] @ np.diag(p.W0[k, :R]) @ p.H0[:R, :R].T
+        s = np.linalg.svd(A, compute_uv=False)
+        kept = s[s > 1e-10 * s[0]] if s[0] > 0 else s[:0]
+        rho = kept[-1] / s[0] if len(kept) else 1.0
+        a, b = o.m_off[k], o.m_off[k + 1]
+        if rho >= 1e-6:
+            good_g.append(Qg[a:b]); good_o.append(o.Q[a:b])
+        else:
+            n_ill += 1
+            err = np.linalg.norm(Qg[a:b] - o.Q[a:b])
+            assert err <= 1e3 * 2.2e-16 / rho, (k, err, rho)
+    print(f"[Q parity] {n_ill} of {p.K} patients with a kept sigma ratio < 1e-6 checked against eps/ratio")
+    return rel(np.concatenate(good_g), np.concatenate(good_o))
+
+
 @pytest.mark.parametrize("name,K", N4_CASES + N2_CASES)
 def test_n4_one_iteration_factors(copa_mod, name, K):
     p, g, o = _pair(copa_mod, name, K)
@@ -107,7 +133,7 @@ def test_n4_one_iteration_factors(copa_mod, name, K):
     H, V, W = [t.cpu().numpy() for t in g.factors()]
     errs = {"H": rel(H, o.H), "V": rel(V, o.V), "W": rel(W, o.W), "U": rel(g.U().cpu().numpy(), o.U_all())}
     if p.cfg.smooth_l == 0:  # Q~ itself is basis-dependent under smoothness (reading R-spline-5)
-        errs["Q"] = rel(g.debug_state()["Qt"].cpu().numpy(), o.Q)
+        errs["Q"] = _q_parity(p, g.debug_state()["Qt"].cpu().numpy(), o)
     print(f"[margin] {name}: FIT {abs(fg[0] - fo[0]):.2e} " + " ".join(f"{k} {v:.2e}" for k, v in errs.items()))
     assert abs(fg[0] - fo[0]) <= 1e-9
     for k, e in errs.items():
