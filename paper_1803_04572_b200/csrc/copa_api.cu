@@ -1,6 +1,7 @@
 // copa_api.cu — the C ABI (include/copa.h): validation, workspace layout, orchestration of one
 // outer iteration on one stream, and the allreduce hand-off points C1/C2.
 #include <cub/cub.cuh>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: phase ranges for nsys/ncu timelines
 
 #include <chrono>
 #include <cmath>
@@ -278,6 +279,7 @@ struct InitTimer {
   cudaStream_t s = nullptr;
   std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
   void mark(const char* name) {
+    nvtxMarkA(name);  // init stage boundary on the NVTX timeline
     if (!on) return;
     cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
@@ -473,9 +475,11 @@ static void phase_collect(Handle& h) {
 
 #define PHASE(ph, expr)                                                    \
   do {                                                                     \
+    nvtxRangePushA(kPhaseNames[ph]);                                       \
     phase_begin(h, ph);                                                    \
     h.launches += (expr);                                                  \
     phase_end(h);                                                          \
+    nvtxRangePop();                                                        \
     const cudaError_t pe_ = cudaGetLastError();                            \
     if (pe_ != cudaSuccess) return cuda_fail(pe_, kPhaseNames[ph]);         \
   } while (0)
