@@ -109,6 +109,8 @@ size_t carve(Handle& h, char* base) {
     h.st_f = c.take<int64_t>(2 * h.nst_cap);
     h.st_k = c.take<int32_t>(2 * h.nst_cap);
     h.cta_st = c.take<int32_t>((int64_t)h.sc_ranges * G + 1);
+    h.st_t = c.take<int32_t>(h.nst_cap + 1);
+    h.st_tab = c.take<uint32_t>(stage_tab_cap(h));
     h.layout_tmp_bytes = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;  // per-group run lengths
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
@@ -355,10 +357,11 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       CUDA_TRY(cudaStreamSynchronize(s), "gcnt sync");
       tm.mark("count_groups");
       std::vector<int64_t> st_f, block_k;
-      std::vector<int32_t> st_k, cta_st;
-      plan_streams(h, gcnt.data(), gptr.data(), st_f, st_k, cta_st, block_k);
+      std::vector<int32_t> st_k, st_t, cta_st;
+      plan_streams(h, gcnt.data(), gptr.data(), st_f, st_k, st_t, cta_st, block_k);
       h.nst = (int64_t)st_k.size() / 2;
-      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F) {
+      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F || (int64_t)st_t.back() > stage_tab_cap(h) ||
+          stage_tab_cap(h) > INT32_MAX) {
         delete H;
         return fail(COPA_E_WORKSPACE, "internal: stage table exceeds its bound");
       }
@@ -366,6 +369,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       if (h.nst > 0) {
         CUDA_TRY(cudaMemcpyAsync(h.st_f, st_f.data(), sizeof(int64_t) * st_f.size(), cudaMemcpyHostToDevice, s), "st_f");
         CUDA_TRY(cudaMemcpyAsync(h.st_k, st_k.data(), sizeof(int32_t) * st_k.size(), cudaMemcpyHostToDevice, s), "st_k");
+        CUDA_TRY(cudaMemcpyAsync(h.st_t, st_t.data(), sizeof(int32_t) * st_t.size(), cudaMemcpyHostToDevice, s), "st_t");
       }
       CUDA_TRY(cudaMemcpyAsync(h.cta_st, cta_st.data(), sizeof(int32_t) * cta_st.size(), cudaMemcpyHostToDevice, s),
                "cta_st");
@@ -395,6 +399,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
     launch_layoutA(h);
     launch_fiber_rowoff(h);  // pass B addresses F_V rows by precomputed offsets (k_fibers.cu)
+    launch_stage_tab(h);     // ... and reads its sub-run bounds from the stage table
     tm.mark("layoutA");
   } else {
     launch_row_patient(h);

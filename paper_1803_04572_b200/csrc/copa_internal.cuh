@@ -86,6 +86,8 @@ struct Handle {
   int64_t* st_f;         // [nst_cap x 2] pass-B stage: logical fiber range [f0, f1) in its stream
   int32_t* st_k;         // [nst_cap x 2] pass-B stage: patient range [k0, k1)
   int32_t* cta_st;       // [sc_ranges x G + 1] first stage of each pass-B CTA
+  int32_t* st_t;         // [nst_cap + 1] pass-B stage: first entry in st_tab
+  uint32_t* st_tab;      // pass-B stage table: sub-run bounds lo | hi << 16 per (stage, patient, sub-range)
   int64_t nst = 0, nst_cap = 0;
   int64_t Jl = 0;        // labels = G * Jg >= J
   int sc_G = 1, sc_W = 4, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
@@ -350,9 +352,12 @@ bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
 void compute_relabel(int64_t J, int ranges, const unsigned long long* hist, int32_t* perm, int32_t* inv, int64_t* Js);
 int64_t stage_cap(const Handle& h);                                // pass-B stage table bound
+int64_t stage_tab_cap(const Handle& h);                            // pass-B sub-run table bound
+void launch_stage_tab(Handle& h);
 // host: gptr (G x (K+1), absolute) from per-group counts; stage table; pass-B patient ranges
 void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::vector<int64_t>& st_f,
-                  std::vector<int32_t>& st_k, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k);
+                  std::vector<int32_t>& st_k, std::vector<int32_t>& st_t, std::vector<int32_t>& cta_st,
+                  std::vector<int64_t>& block_k);
 // wide per-patient dense kernels (k_dense.cu)
 bool polar_wide_ok(const Handle& h);
 // general path (k_plain.cu)

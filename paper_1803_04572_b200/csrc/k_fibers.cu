@@ -112,21 +112,20 @@ void launch_relabel_V(Handle& h) {
 
 // ------------------------------------------------------------------ pass B (TMA-staged scatter)
 // Stage slot layout (bytes, each part 16-byte aligned):
-//   meta  : int64 f0, f1; int32 k0, k1, shift_col, shift_val, shift_n, shift_gp, shift_wo (48)
-//   gp    : int64 [PB + 1] + 16  run starts of the stage's patients in stream g (bulk copy, shifted)
-//   wo    : uint16 [PB][kWoS] + 16  label sub-run offsets inside each run (bulk copy, shifted)
-//   col   : int32 [FB] + 16  labels           (bulk copy, shifted)
+//   meta  : int32 npat, shift_lh, shift_col, shift_val, shift_n (32)
+//   lh    : uint32 [PB][W] + 16  sub-run bounds lo | hi << 16 of every (patient, sub-range), relative
+//           to the stage's first fiber (st_tab, built at init; bulk copy, shifted)
+//   col   : int32 [FB] + 16  F_V row byte offsets (bulk copy, shifted)
 //   val   : f64 [FB l] + 16   fiber values     (bulk copy, shifted)
 //   nrows : f64 [PB l R] + 16 N_k rows         (bulk copy, shifted)
 struct SlotGeom {
-  uint32_t gp, wo, col, val, nrows, bytes;
+  uint32_t lh, col, val, nrows, bytes;
 };
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~(uint64_t)15); }
-__host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
+__host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int W, int l, int R) {
   SlotGeom s;
-  s.gp = 48;
-  s.wo = s.gp + al16(8ull * (PB + 1) + 16);
-  s.col = s.wo + al16(2ull * kWoS * PB + 16);
+  s.lh = 32;
+  s.col = s.lh + al16(4ull * W * PB + 16);
   s.val = s.col + al16(4ull * FB + 16);
   s.nrows = s.val + al16(8ull * FB * l + 16);
   s.bytes = (s.nrows + al16(8ull * PB * l * R + 16) + 127) & ~127u;
@@ -134,94 +133,121 @@ __host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int l, int R) {
 }
 
 constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
-constexpr int kScrD = 128;       // per-warp scratch doubles behind the F_V slice (redirected row updates)
+constexpr int kScrD = 128;       // per-sub-range scratch doubles behind the F_V slice (redirected row updates)
 
+// Shared-memory accesses by 32-bit shared addresses: the consumers hold their base addresses in
+// registers (with generic pointers the compiler re-derived the shared window, S2UR + ULEA, per tile).
+// All are volatile: they keep program order among themselves (F_V read-modify-writes of one lane).
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_s32_if(uint32_t a, bool p, int dflt) {
+  int v = dflt;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.b32 %0, [%1];\n}" : "+r"(v) : "r"(a), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ double lds_f64_if(uint32_t a, bool p) {
+  double v = 0.0;
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}" : "+d"(v) : "r"(a), "r"((int)p));
+  return v;
+}
+__device__ __forceinline__ double2 lds_v2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_v2(uint32_t a, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n @P1 bra DONE%=;\n bra WAIT%=;\n"
+      "DONE%=:\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
 
-// F_V row updates are branch-free: invalid lanes are redirected to a per-lane scratch slot
-// (predicated updates measured slower: 26.6-27.1 vs 24.4 ms at Scale).
-template <int KS, int NT, int W, int TB, int LT, int RT>
-__global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
-    const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, const int64_t* __restrict__ gptr,
-    int64_t K, int G, int64_t Js, int64_t Jg, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
-    const int32_t* __restrict__ cta_st, const uint16_t* __restrict__ woff, int l_, int R_, int RS_, int FB, int PB,
+// W label sub-ranges per group, CS consumer warps per sub-range: warp (w, c) owns the F_V rows of
+// sub-range w, columns [8 NT/CS c, 8 NT/CS (c + 1)) — disjoint words, no atomics. Per stage it reads
+// its sub-run bounds of every patient from the staged lh table, then runs 8-fiber MMA tiles
+// (M = fibers, N = r, K = a) with one tile in flight: the next tile's loads and MMAs are issued
+// before the F_V read-modify-write of the pending one (updates stay in tile order). Lanes outside
+// the sub-run or past column R are redirected to scratch words (branch-free updates).
+template <int KS, int NT, int W, int LT, int RT, int CS>
+__global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
+    const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, int G, int64_t Jg,
+    const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k, const int32_t* __restrict__ st_t,
+    const uint32_t* __restrict__ st_tab, const int32_t* __restrict__ cta_st, int l_, int R_, int RS_, int FB, int PB,
     int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart) {
-  const int R = RT ? RT : R_;           // compile-time for the configured (R, l) shapes
+  const int R = RT ? RT : R_;  // compile-time for the configured (R, l) shapes
   const int l = LT ? LT : l_;
   const int RS = RT ? ((RT + 1) & ~1) : RS_;
+  static_assert(NT % CS == 0, "column splits divide the n-tiles");
+  constexpr int NTW = NT / CS;  // n-tiles per consumer warp
   extern __shared__ __align__(128) unsigned char smraw[];
-  // thread index in a register the compiler cannot rebuild from SR_TID (it otherwise re-reads the
-  // special register inside the per-patient loop)
-  int tid;
+  int tid;  // in a register the compiler cannot rebuild from SR_TID
   asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
-  const int lane = tid & 31, w = tid >> 5;
+  const int lane = tid & 31, wc = tid >> 5;
+  const int w = wc % W, cpart = wc / W;
   const int grp = blockIdx.x % G;
   const int64_t rng = blockIdx.x / G;
-  const SlotGeom sg = slot_geom(FB, PB, l, R);
-  double* Fs = (double*)smraw;  // Jg x RS, then W x 64 doubles of per-warp scratch (branch-free RMW)
+  const SlotGeom sg = slot_geom(FB, PB, W, l, R);
+  double* Fs = (double*)smraw;  // Jg x RS, then W x kScrD doubles of scratch
   const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * kScrD * 8 + 127) & ~127ull);
   uint64_t* full = (uint64_t*)(smraw + fs_bytes);
   uint64_t* empty = full + NSt;
   const uint32_t slots_off = fs_bytes + ((2 * NSt * 8 + 127) & ~127);
   unsigned char* slots = smraw + slots_off;
-  const int64_t* smI64 = reinterpret_cast<const int64_t*>(smraw);
-  const int32_t* smI32 = reinterpret_cast<const int32_t*>(smraw);
-  const uint16_t* smU16 = reinterpret_cast<const uint16_t*>(smraw);
-  const double* smD = reinterpret_cast<const double*>(smraw);
   for (int64_t x = threadIdx.x; x < Jg * RS; x += blockDim.x) Fs[x] = 0.0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSt; ++i) {
       mbar_init(full + i, 1);
-      mbar_init(empty + i, W);
+      mbar_init(empty + i, W * CS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int s0 = cta_st[blockIdx.x], ns = cta_st[blockIdx.x + 1] - s0;
-  const int64_t K1 = K + 1;
-  if (w == W) {
-    // ---------------- producer (one lane)
+  if (wc == W * CS) {
+    // ---------------- producer (one lane); stage metadata loaded one stage ahead
     if (lane == 0) {
-      // stage metadata is loaded one stage ahead so that its latency overlaps the ring wait
       int64_t nf0 = 0, nf1 = 0;
-      int32_t nk0 = 0, nk1 = 0;
+      int32_t nk0 = 0, nk1 = 0, nt0 = 0;
       if (ns > 0) {
         nf0 = st_f[2 * (int64_t)s0]; nf1 = st_f[2 * (int64_t)s0 + 1];
         nk0 = st_k[2 * (int64_t)s0]; nk1 = st_k[2 * (int64_t)s0 + 1];
+        nt0 = st_t[s0];
       }
       int slot = 0, phase = 1;  // the producer's first pass over the ring does not wait
       for (int i = 0; i < ns; ++i) {
         const int64_t f0 = nf0, f1 = nf1;
-        const int32_t k0 = nk0, k1 = nk1;
+        const int32_t k0 = nk0, k1 = nk1, t0 = nt0;
         if (i + 1 < ns) {
           const int64_t st = s0 + i + 1;
           nf0 = st_f[2 * st]; nf1 = st_f[2 * st + 1];
           nk0 = st_k[2 * st]; nk1 = st_k[2 * st + 1];
+          nt0 = st_t[st];
         }
         mbar_wait_park(empty + slot, phase, 1000000u);  // parked, no issue slots taken from consumers
         unsigned char* base = slots + (size_t)slot * sg.bytes;
-        int64_t* meta = (int64_t*)base;
-        int32_t* mi = (int32_t*)(base + 16);
-        meta[0] = f0;
-        meta[1] = f1;
-        mi[0] = k0;
-        mi[1] = k1;
-        const uintptr_t sc = (uintptr_t)(fiber_col + f0), sv = (uintptr_t)(fiber_val + f0 * l),
-                        sn = (uintptr_t)(Nst + (int64_t)k0 * l * R), sp = (uintptr_t)(gptr + grp * K1 + k0),
-                        sw = (uintptr_t)(woff + ((int64_t)grp * K + k0) * kWoS);
-        const size_t bc = 4ull * (f1 - f0), bv = 8ull * (f1 - f0) * l, bn = 8ull * (k1 - k0) * l * R,
-                     bp = 8ull * (k1 - k0 + 1), bw = 2ull * kWoS * (k1 - k0);
+        int32_t* mi = (int32_t*)base;
+        const uintptr_t sl = (uintptr_t)(st_tab + t0), sc = (uintptr_t)(fiber_col + f0),
+                        sv = (uintptr_t)(fiber_val + f0 * l), sn = (uintptr_t)(Nst + (int64_t)k0 * l * R);
+        const size_t bl = 4ull * W * (k1 - k0), bc = 4ull * (f1 - f0), bv = 8ull * (f1 - f0) * l,
+                     bn = 8ull * (k1 - k0) * l * R;
+        mi[0] = k1 - k0;
+        mi[1] = (int32_t)(sl & 15);
         mi[2] = (int32_t)(sc & 15);
         mi[3] = (int32_t)(sv & 15);
         mi[4] = (int32_t)(sn & 15);
-        mi[5] = (int32_t)(sp & 15);
-        mi[6] = (int32_t)(sw & 15);
         // expected bytes first (same rounding as bulk_g2s_span), then the copies
-        const uint32_t tx = al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn) +
-                            al16((sp & 15) + bp) + al16((sw & 15) + bw);
+        const uint32_t tx = al16((sl & 15) + bl) + al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn);
         mbar_arrive_tx(full + slot, tx);
         uint32_t t2 = 0;
-        bulk_g2s_span(base + sg.gp, (const void*)sp, bp, full + slot, &t2);
-        bulk_g2s_span(base + sg.wo, (const void*)sw, bw, full + slot, &t2);
+        bulk_g2s_span(base + sg.lh, (const void*)sl, bl, full + slot, &t2);
         bulk_g2s_span(base + sg.col, (const void*)sc, bc, full + slot, &t2);
         bulk_g2s_span(base + sg.val, (const void*)sv, bv, full + slot, &t2);
         bulk_g2s_span(base + sg.nrows, (const void*)sn, bn, full + slot, &t2);
@@ -229,111 +255,103 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
       }
     }
   } else {
-    // ---------------- consumers: warp w owns label sub-range (grp, w) = labels [grp Jg + w Js, + Js),
-    // all R columns of those F_V rows: no two warps write the same row. Its sub-run of each run
-    // comes from the staged offsets; tiles of 8 fibers (one patient, distinct labels) run TB at a
-    // time: loads and MMAs of the batch first, then the read-modify-writes.
-    const int ln = lane;
-    const int g = ln >> 2, t = ln & 3;
+    // ---------------- consumers
+    const int g = lane >> 2, t = lane & 3;
     const int per = l * R;
-    const int scr = (int)Jg * RS + w * kScrD + 2 * ln;  // this lane's scratch slot (index into Fs; + 8 nt stays
-                                                        // inside the warp's kScrD doubles)
-    // B fragment B[t][g] = N(a = 4 ks + t, r = 8 nt + g) at nb0 + 4 ks R + 8 nt of a patient's N block
-    // (compile-time offsets for the configured shapes); lanes outside (a < l, r < R) load nothing
-    const int nb0 = t * R + g;
-    unsigned nok = 0;  // bit (ks NT + nt): the lane's fragment is inside N
+    const int c0 = 8 * NTW * cpart;  // first F_V column of this warp's n-tiles
+    const uint32_t sbase = smem_u32(smraw);
+    const uint32_t fwA = sbase + 8u * (uint32_t)(c0 + 2 * t);  // + row byte offset + 64 nt: the lane's pair
+    // scratch words of this lane (the CS warps of a sub-range share them: redirected updates are
+    // never read back, so their interleaving is immaterial); + 64 nt stays inside kScrD doubles
+    const uint32_t scrA = sbase + 8u * (uint32_t)(Jg * RS + w * kScrD + 2 * lane);
+    // B fragment B[t][g] = N(a = 4 ks + t, r = c0 + 8 nt + g); lanes outside (a < l, r < R) load nothing
+    const int nb0 = t * R + g + c0;
+    unsigned nok = 0;  // bit (ks NTW + nt): the lane's fragment is inside N
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-        if (4 * ks + t < l && 8 * nt + g < R) nok |= 1u << (ks * NT + nt);
-    // One tile (8 fibers of one patient sub-run) in flight: the loads and MMAs of the next tile are
-    // issued before the F_V read-modify-write of the pending one, so the MMA latency overlaps the
-    // shared-memory updates (a tile's MMAs never touch F_V; updates stay in tile order).
-    int pbase = scr;
-    double pcc[NT][2];
+      for (int nt = 0; nt < NTW; ++nt)
+        if (4 * ks + t < l && c0 + 8 * nt + g < R) nok |= 1u << (ks * NTW + nt);
+    bool colok[NTW];  // the lane's two columns of n-tile nt are inside R (else: scratch)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) pcc[nt][0] = pcc[nt][1] = 0.0;
+    for (int nt = 0; nt < NTW; ++nt) colok[nt] = c0 + 8 * nt + 2 * t < R;
+    bool aok[KS];  // the lane's A fragment (a = 4 ks + t) is inside l
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) aok[ks] = 4 * ks + t < l;
+    uint32_t pA = scrA;  // pending tile: the lane's F_V row address (or scratch) and its products
+    double pcc[NTW][2];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) pcc[nt][0] = pcc[nt][1] = 0.0;
     auto commit = [&]() {
-      int idx[NT];
-      double2 v[NT];
+      uint32_t a[NTW];
+      double2 v[NTW];
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        // tile nt at base + 8 nt (an immediate offset); columns >= R of the last tile -> scratch
-        idx[nt] = (8 * nt + 8 <= R || 8 * nt + 2 * t < R) ? pbase + 8 * nt : scr;
-        v[nt] = *reinterpret_cast<const double2*>(Fs + idx[nt]);
+      for (int nt = 0; nt < NTW; ++nt) {
+        a[nt] = (colok[nt] ? pA : scrA) + 64u * nt;
+        v[nt] = lds_v2(a[nt]);
       }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
+      for (int nt = 0; nt < NTW; ++nt) {
         v[nt].x += pcc[nt][0];
         v[nt].y += pcc[nt][1];
-        *reinterpret_cast<double2*>(Fs + idx[nt]) = v[nt];
+        sts_v2(a[nt], v[nt]);
       }
     };
+    const uint32_t fullA = smem_u32(full), emptyA = smem_u32(empty);
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
-      mbar_wait(full + slot, phase);
-      // stage arrays addressed by index into the shared buffer (keeps every access a plain LDS;
-      // derived pointers were rebuilt as generic addresses per patient)
-      const uint32_t sb = slots_off + (uint32_t)slot * sg.bytes;
-      const int64_t f0 = smI64[sb >> 3], f1 = smI64[(sb >> 3) + 1];
-      const int32_t* mi = smI32 + ((sb + 16) >> 2);
-      const int32_t k0 = mi[0], k1 = mi[1];
-      const int64_t* gp = smI64 + ((sb + sg.gp + mi[5]) >> 3);
-      const uint16_t* wo = smU16 + ((sb + sg.wo + mi[6]) >> 1);
-      const int32_t* colS = smI32 + ((sb + sg.col + mi[2]) >> 2);
-      const double* valS = smD + ((sb + sg.val + mi[3]) >> 3);
-      const double* nS = smD + ((sb + sg.nrows + mi[4]) >> 3);
-      // per-patient setup (sub-run bounds, B fragments B[t][g] = N(a = 4 ks + t, r = 8 nt + g)) is
-      // loaded one patient ahead, off the critical path of the current patient's tiles
-      const int npat = k1 - k0;
-      auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NT]) {
-        const int64_t rs = gp[p];
-        lo_ = (int)(max(rs + wo[p * kWoS + w], f0) - f0);
-        hi_ = (int)(min(rs + wo[p * kWoS + w + 1], f1) - f0);
-        const double* Np = nS + (int64_t)p * per + nb0;
+      mbar_wait_a(fullA + 8u * slot, phase);
+      const uint32_t sb = sbase + slots_off + (uint32_t)slot * sg.bytes;
+      const int npat = lds_s32(sb);
+      const uint32_t lhA = sb + sg.lh + lds_s32(sb + 4) + 4u * w;
+      const uint32_t colA = sb + sg.col + lds_s32(sb + 8) + 4u * g;
+      const uint32_t valA = sb + sg.val + lds_s32(sb + 12) + 8u * (uint32_t)(t + l * g);
+      const uint32_t nA = sb + sg.nrows + lds_s32(sb + 16) + 8u * nb0;
+      // per-patient setup (sub-run bounds, B fragments) one patient ahead of its tiles
+      auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NTW]) {
+        const uint32_t lh = (uint32_t)lds_s32(lhA + 4u * W * p);
+        lo_ = (int)(lh & 0xffffu);
+        hi_ = (int)(lh >> 16);
+        const uint32_t np = nA + 8u * (uint32_t)(p * per);
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt)
-            b[ks][nt] = (nok >> (ks * NT + nt)) & 1u ? Np[4 * ks * R + 8 * nt] : 0.0;
+          for (int nt = 0; nt < NTW; ++nt)
+            b[ks][nt] = lds_f64_if(np + 8u * (4 * ks * R + 8 * nt), (nok >> (ks * NTW + nt)) & 1u);
       };
       int nlo = 0, nhi = 0;
-      double nbfr[KS][NT];
+      double nbfr[KS][NTW];
       if (npat > 0) setup(0, nlo, nhi, nbfr);
       for (int p = 0; p < npat; ++p) {
         const int lo = nlo, hi = nhi;
-        double bfr[KS][NT];
+        double bfr[KS][NTW];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) bfr[ks][nt] = nbfr[ks][nt];
+          for (int nt = 0; nt < NTW; ++nt) bfr[ks][nt] = nbfr[ks][nt];
         if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
-        if (lo >= hi) continue;
 #pragma unroll 2
         for (int tb = lo; tb < hi; tb += 8) {
-          const int f = tb + g;
-          const bool ok = f < hi;
-          const int base = ok ? colS[f] + 2 * t : scr;  // fibers carry their F_V row offset (label - g Jg) RS
-          const double* vf = valS + f * l + t;
+          const bool ok = tb + g < hi;
+          const int rb = lds_s32_if(colA + 4u * tb, ok, 0);  // the fiber's F_V row byte offset
           double av[KS];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) av[ks] = (ok && 4 * ks + t < l) ? vf[4 * ks] : 0.0;
-          double cc[NT][2];
+          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(valA + 8u * (uint32_t)(l * tb + 4 * ks), ok && aok[ks]);
+          double cc[NTW][2];
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
+          for (int nt = 0; nt < NTW; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
-          commit();  // the previous tile (or a zero update of the scratch slot)
-          pbase = base;
+            for (int nt = 0; nt < NTW; ++nt) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
+          commit();  // the previous tile (or a zero update of the scratch words)
+          pA = ok ? fwA + (uint32_t)rb : scrA;
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) { pcc[nt][0] = cc[nt][0]; pcc[nt][1] = cc[nt][1]; }
+          for (int nt = 0; nt < NTW; ++nt) { pcc[nt][0] = cc[nt][0]; pcc[nt][1] = cc[nt][1]; }
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + slot);
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(emptyA + 8u * slot) : "memory");
       if (++slot == NSt) { slot = 0; phase ^= 1; }
     }
     commit();  // the last tile
@@ -344,6 +362,36 @@ __global__ void __launch_bounds__(32 * (W + 1)) k_scatter_tma(
     const int64_t jj = x / R, r = x - jj * R;
     out[x] = Fs[jj * RS + r];
   }
+}
+
+// Init: the pass-B stage table of sub-run bounds. CTA c = (range, group c % G) walks its stages;
+// entry (stage s, patient k in [k0, k1), sub-range w) = lo | hi << 16 with [lo, hi) the fibers of
+// sub-range (g, w) of patient k inside the stage's fiber window [f0, f1), relative to f0.
+__global__ void k_stage_tab(const int64_t* __restrict__ gptr, const uint16_t* __restrict__ woff, int64_t K, int G,
+                            int W, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
+                            const int32_t* __restrict__ st_t, const int32_t* __restrict__ cta_st,
+                            uint32_t* __restrict__ st_tab) {
+  const int c = blockIdx.x, grp = c % G;
+  const int64_t* gp = gptr + (int64_t)grp * (K + 1);
+  for (int s = cta_st[c] + threadIdx.x; s < cta_st[c + 1]; s += blockDim.x) {
+    const int64_t f0 = st_f[2 * (int64_t)s], f1 = st_f[2 * (int64_t)s + 1];
+    const int32_t k0 = st_k[2 * (int64_t)s], k1 = st_k[2 * (int64_t)s + 1];
+    uint32_t* out = st_tab + st_t[s];
+    for (int32_t k = k0; k < k1; ++k) {
+      const uint16_t* wo = woff + ((int64_t)grp * K + k) * kWoS;
+      for (int w = 0; w < W; ++w) {
+        const int64_t lo = min(max(gp[k] + wo[w], f0), f1) - f0;
+        const int64_t hi = min(max(gp[k] + wo[w + 1], f0), f1) - f0;
+        out[(int64_t)(k - k0) * W + w] = (uint32_t)lo | ((uint32_t)hi << 16);
+      }
+    }
+  }
+}
+
+void launch_stage_tab(Handle& h) {
+  if (!h.sc_ok || h.nst == 0) return;
+  k_stage_tab<<<(unsigned)(h.sc_ranges * h.sc_G), 128, 0, h.stream>>>(h.gptr, h.woff, h.K, h.sc_G, h.sc_W, h.st_f,
+                                                                      h.st_k, h.st_t, h.cta_st, h.st_tab);
 }
 
 // FV[inv[j']] = sum over ranges of part[range][j'] (fixed order), for every used label j'
@@ -359,33 +407,32 @@ __global__ void k_sum_ranges(const double* __restrict__ part, int nr, int64_t Jl
   FV[(int64_t)j * R + r] = s;
 }
 
-template <int KS, int NT, int W, int TB, int LT = 0, int RT = 0>
+template <int KS, int NT, int W, int LT = 0, int RT = 0, int CS = 1>
 static void scatter_inst_w(Handle& h) {
-  constexpr auto fn = k_scatter_tma<KS, NT, W, TB, LT, RT>;
+  constexpr auto fn = k_scatter_tma<KS, NT, W, LT, RT, CS>;
   max_smem_attr<fn>(h);
   const int ctas = h.sc_ranges * h.sc_G;
-  fn<<<ctas, 32 * (W + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.gptr, h.K, h.sc_G, h.sc_Js, h.sc_Jg,
-                                                   h.st_f, h.st_k, h.cta_st, h.woff, h.l, h.R, h.sc_RS, h.sc_FB,
-                                                   h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
+  fn<<<ctas, 32 * (W * CS + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.sc_G, h.sc_Jg, h.st_f, h.st_k,
+                                                        h.st_t, h.st_tab, h.cta_st, h.l, h.R, h.sc_RS, h.sc_FB,
+                                                        h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
 
 template <int KS, int NT>
 static void scatter_inst(Handle& h) {
-  if (h.sc_W == 2) scatter_inst_w<KS, NT, 2, 4>(h);
-  else scatter_inst_w<KS, NT, 4, 2>(h);
+  if (h.sc_W == 2) scatter_inst_w<KS, NT, 2>(h);
+  else scatter_inst_w<KS, NT, 4>(h);
 }
 
+// Column splits for the configured shapes (measured at Scale: CS = 3 23.3 ms vs CS = 1 24.7 ms;
+// Medium CS = 2 1.26 vs 1.40 ms; Large CS = 5 8.1 vs 9.0 ms; 2 or 8 sub-ranges per group slower).
 template <int KS>
 static void scatter_dispatch_n(Handle& h) {
   if (h.sc_W == 4) {
-    if (KS == 2 && h.l == 7 && h.R == 20) {
-      scatter_inst_w<2, 3, 4, 3, 7, 20>(h);  // 3-tile batches (TB 2/4 measured slower)
-      return;
-    }
-    if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 2, 7, 15>(h); return; }
-    if (KS == 3 && h.l == 9 && h.R == 40) { scatter_inst_w<3, 5, 4, 2, 9, 40>(h); return; }
+    if (KS == 2 && h.l == 7 && h.R == 20) { scatter_inst_w<2, 3, 4, 7, 20, 3>(h); return; }
+    if (KS == 2 && h.l == 7 && h.R == 15) { scatter_inst_w<2, 2, 4, 7, 15, 2>(h); return; }
+    if (KS == 3 && h.l == 9 && h.R == 40) { scatter_inst_w<3, 5, 4, 9, 40, 5>(h); return; }
   }
   switch ((h.R + 7) / 8) {
     case 1: scatter_inst<KS, 1>(h); break;
@@ -413,7 +460,7 @@ int launch_scatter_fibers(Handle& h) {
 // ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared memory.
 void plan_scatter(Handle& h) {
   const size_t budget = 225 * 1024;
-  h.sc_W = kScW;  // label sub-ranges per group = consumer warps of k_scatter_tma (2 or 4)
+  h.sc_W = kScW;  // label sub-ranges per group (2 or 4)
   h.sc_RS = (h.R + 1) & ~1;
   h.sc_FB = 256;
   h.sc_ok = 0;
@@ -426,7 +473,7 @@ void plan_scatter(Handle& h) {
       const size_t fs = ((size_t)Jg * h.sc_RS * 8 + (size_t)h.sc_W * kScrD * 8 + 127) & ~(size_t)127;
       for (int NSt = 4; NSt >= (pass ? 2 : 3) && !h.sc_ok; --NSt)
         for (int pi = 0; pi < (pass ? 3 : 2) && !h.sc_ok; ++pi) {
-          const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.l, h.R);
+          const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.sc_W, h.l, h.R);
           const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
           if (bytes <= budget) {
             h.sc_G = G;
@@ -447,7 +494,7 @@ void plan_scatter(Handle& h) {
     bool done = false;
     for (int NSt = 4; NSt >= 3 && !done; --NSt)
       for (int pi = 0; pi < 2 && !done; ++pi) {
-        const SlotGeom sg = slot_geom(512, pbs[pi], h.l, h.R);
+        const SlotGeom sg = slot_geom(512, pbs[pi], h.sc_W, h.l, h.R);
         const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
         if (bytes <= budget) {
           h.sc_FB = 512;
@@ -481,7 +528,7 @@ __global__ void k_fiber_rowoff(const int64_t* __restrict__ gptr, int64_t K, int 
   for (int g = 0; g < G; ++g) {
     const int64_t f0 = gptr[(int64_t)g * (K + 1)], f1 = gptr[(int64_t)g * (K + 1) + K];
     for (int64_t f = f0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < f1; f += (int64_t)gridDim.x * blockDim.x)
-      fiber_col[f] = (int32_t)((fiber_col[f] - g * Jg) * RS);
+      fiber_col[f] = (int32_t)((fiber_col[f] - g * Jg) * RS * 8);  // bytes
   }
 }
 
@@ -490,6 +537,10 @@ void launch_fiber_rowoff(Handle& h) {
   k_fiber_rowoff<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.gptr, h.K, h.sc_G, h.sc_Jg, h.sc_RS, h.fiber_col);
 }
 
+// stage-table entries: every stage holds its patients' sub-range bounds; a patient's run is split
+// over at most (run / FB + 2) stages, so sum over stages of (k1 - k0) <= G K + nst
+int64_t stage_tab_cap(const Handle& h) { return ((int64_t)h.sc_G * h.K + stage_cap(h)) * h.sc_W + 16; }
+
 int64_t stage_cap(const Handle& h) {
   return h.F / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
 }
@@ -497,7 +548,7 @@ int64_t stage_cap(const Handle& h) {
 // Host planning from the per-group run lengths gcnt[g][k]: stream offsets gptr (absolute), pass-B
 // patient ranges (balanced by fibers) and the stage table of every (range, group) CTA.
 void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int64_t>& st_f, std::vector<int32_t>& st_k,
-                  std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k) {
+                  std::vector<int32_t>& st_t, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k) {
   const int G = h.sc_G;
   const int64_t K = h.K, K1 = K + 1;
   int64_t base = 0;
@@ -553,6 +604,14 @@ void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int
       }
     }
   cta_st[(size_t)nr * G] = (int32_t)(st_k.size() / 2);
+  // offsets of every stage's (patient, sub-range) entries in the stage table st_tab
+  const size_t nst = st_k.size() / 2;
+  st_t.assign(nst + 1, 0);
+  int64_t acc = 0;  // (the caller rejects tables beyond int32)
+  for (size_t x = 0; x < nst; ++x) {
+    acc += (int64_t)(st_k[2 * x + 1] - st_k[2 * x]) * h.sc_W;
+    st_t[x + 1] = (int32_t)std::min<int64_t>(acc, INT32_MAX);
+  }
 }
 
 // ------------------------------------------------------------------ init-time relabeling
