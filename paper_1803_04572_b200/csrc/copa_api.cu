@@ -105,6 +105,9 @@ size_t carve(Handle& h, char* base) {
     h.fv_part = c.take<double>((int64_t)h.sc_ranges * h.Jl * R);
     h.fhist = c.take<unsigned long long>(h.J);
     h.woff = c.take<uint16_t>((int64_t)G * h.K * kWoS + 16);
+    h.twoff = c.take<uint16_t>((int64_t)G * h.K * kWoS + 16);
+    h.tptr = c.take<int64_t>((int64_t)G * (h.K + 1) + 2);
+    h.tiles = c.take<unsigned char>(tiles_cap(h) * (int64_t)tile_bytes_host(h.l) + 64);
     h.nst_cap = stage_cap(h);
     h.st_f = c.take<int64_t>(2 * h.nst_cap);
     h.st_k = c.take<int32_t>(2 * h.nst_cap);
@@ -356,16 +359,27 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
                  "gcnt copy");
       CUDA_TRY(cudaStreamSynchronize(s), "gcnt sync");
       tm.mark("count_groups");
+      prefix_runs(h, gcnt.data(), gptr.data());  // g-stream fiber offsets
+      // tiled stream (pass B): tiles per run -> tile offsets and the stage table
+      int32_t* tcnt_dev = gcnt_dev;  // reused: gcnt is on the host now
+      launch_tile_counts(h, tcnt_dev);
+      std::vector<int32_t> tcnt((size_t)G * (size_t)h.K);
+      std::vector<int64_t> tptr((size_t)G * (size_t)(h.K + 1));
+      if (h.K > 0)
+        CUDA_TRY(cudaMemcpyAsync(tcnt.data(), tcnt_dev, sizeof(int32_t) * tcnt.size(), cudaMemcpyDeviceToHost, s),
+                 "tcnt copy");
+      CUDA_TRY(cudaStreamSynchronize(s), "tcnt sync");
       std::vector<int64_t> st_f, block_k;
       std::vector<int32_t> st_k, st_t, cta_st;
-      plan_streams(h, gcnt.data(), gptr.data(), st_f, st_k, st_t, cta_st, block_k);
+      plan_streams(h, tcnt.data(), tptr.data(), st_f, st_k, st_t, cta_st, block_k);
       h.nst = (int64_t)st_k.size() / 2;
-      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F || (int64_t)st_t.back() > stage_tab_cap(h) ||
-          stage_tab_cap(h) > INT32_MAX) {
+      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F || tptr[tptr.size() - 1] > tiles_cap(h) ||
+          (int64_t)st_t.back() > stage_tab_cap(h) || stage_tab_cap(h) > INT32_MAX) {
         delete H;
         return fail(COPA_E_WORKSPACE, "internal: stage table exceeds its bound");
       }
       CUDA_TRY(cudaMemcpyAsync(h.gptr, gptr.data(), sizeof(int64_t) * gptr.size(), cudaMemcpyHostToDevice, s), "gptr");
+      CUDA_TRY(cudaMemcpyAsync(h.tptr, tptr.data(), sizeof(int64_t) * tptr.size(), cudaMemcpyHostToDevice, s), "tptr");
       if (h.nst > 0) {
         CUDA_TRY(cudaMemcpyAsync(h.st_f, st_f.data(), sizeof(int64_t) * st_f.size(), cudaMemcpyHostToDevice, s), "st_f");
         CUDA_TRY(cudaMemcpyAsync(h.st_k, st_k.data(), sizeof(int32_t) * st_k.size(), cudaMemcpyHostToDevice, s), "st_k");
@@ -398,8 +412,8 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
     cudaMemsetAsync(h.Vl, 0, sizeof(double) * (size_t)(h.Jl * h.R + 64), s);
     launch_layoutA(h);
-    launch_fiber_rowoff(h);  // pass B addresses F_V rows by precomputed offsets (k_fibers.cu)
-    launch_stage_tab(h);     // ... and reads its sub-run bounds from the stage table
+    launch_build_tiles(h);  // pass B's tiled stream (k_fibers.cu) ...
+    launch_stage_tab(h);    // ... and its stage table of tile bounds
     tm.mark("layoutA");
   } else {
     launch_row_patient(h);

@@ -87,11 +87,14 @@ struct Handle {
   int32_t* st_k;         // [nst_cap x 2] pass-B stage: patient range [k0, k1)
   int32_t* cta_st;       // [sc_ranges x G + 1] first stage of each pass-B CTA
   int32_t* st_t;         // [nst_cap + 1] pass-B stage: first entry in st_tab
-  uint32_t* st_tab;      // pass-B stage table: sub-run bounds lo | hi << 16 per (stage, patient, sub-range)
+  uint32_t* st_tab;      // pass-B stage table: tile bounds lo | hi << 16 per (stage, patient, sub-range)
+  unsigned char* tiles;  // pass-B tiled stream (k_fibers.cu): per group, patient, sub-range: 8-slot tiles
+  int64_t* tptr;         // [G x (K + 1)] first tile of each (group, patient) run
+  uint16_t* twoff;       // [G x K x kWoS] tile offset of each sub-range inside its run
   int64_t nst = 0, nst_cap = 0;
   int64_t Jl = 0;        // labels = G * Jg >= J
   int sc_G = 1, sc_W = 4, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
-  int sc_FB = 256, sc_PB = 16, sc_NS = 3;
+  int sc_FB = 32, sc_PB = 16, sc_NS = 3;  // pass-B stage: tiles (FB), patients (PB), ring slots (NS)
   int64_t sc_Js = 0, sc_Jg = 0;
   size_t sc_slot = 0, sc_smem = 0;
   void* layout_tmp;
@@ -344,7 +347,11 @@ void launch_U(Handle& h, double* U, int64_t k0, int64_t k1);
 void launch_spmm_fibers(Handle& h);   // pass A (k_passA.cu)
 void launch_relabel_V(Handle& h);
 void launch_layoutA(Handle& h);
-void launch_fiber_rowoff(Handle& h);
+void launch_tile_counts(Handle& h, int32_t* tcnt);
+void launch_build_tiles(Handle& h);
+int64_t tiles_cap(const Handle& h);
+void prefix_runs(const Handle& h, const int32_t* cnt, int64_t* ptr);
+inline uint32_t tile_bytes_host(int l) { return 32u + 64u * (uint32_t)l; }
 void plan_passA(Handle& h);
 void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
 int launch_scatter_fibers(Handle& h);

@@ -110,30 +110,54 @@ void launch_relabel_V(Handle& h) {
   k_relabel_V<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.V, h.inv, h.Jl, h.R, h.Vl);
 }
 
-// ------------------------------------------------------------------ pass B (TMA-staged scatter)
+// ------------------------------------------------------------------ pass B (tiled stream, TMA-staged)
+// Tiled stream (built once at init from the g-streams, k_build_tiles): per label group g, patient
+// after patient, sub-range after sub-range, the sub-run of (patient k, sub-range (g, w)) is cut into
+// ceil(n / 8) tiles of 8 fiber slots, each tile
+//   int32 rowoff[8]   F_V row byte offset (label - g Jg) RS 8 inside the CTA's shared-memory slice
+//   f64   val[l][8]   x'(a, slot), a-major: the MMA A fragment of a k-step (a = 4 ks + t, slot g) is
+//                     256 contiguous bytes (two conflict-free wavefronts)
+// Padding slots hold zeros and address one of the scratch rows behind the slice. The slots of a tile
+// are paired (2i, 2i + 1) so that the two rows one quarter-warp touches in an F_V read-modify-write
+// lie in opposite halves of the 32 banks (row labels differ by D mod M, see pair_rule); pads are
+// wildcards that take the partner class. tptr[g][k]: first tile of (g, k); twoff[g][k][w]: tile
+// offset of sub-range w inside it.
+__host__ __device__ inline uint32_t tile_bytes(int l) { return 32u + 64u * (uint32_t)l; }
+constexpr int kScrRows = 8;  // scratch rows behind the F_V slice (pads; any label class mod M <= 8)
+
+// Rows j0, j1 with byte offsets 8 RS j: their 64-byte segments (same columns) are bank-disjoint iff
+// 8 RS (j0 - j1) = 64 mod 128, i.e. RS (j0 - j1) = 8 mod 16. With RS = 2^a b (b odd, 1 <= a <= 3):
+// j0 - j1 = D mod M with M = 2^(4 - a), D = M / 2. RS is chosen with a <= 3 (plan_scatter).
+__host__ __device__ inline void pair_rule(int RS, int* M, int* D) {
+  int a = 0;
+  while (((RS >> a) & 1) == 0 && a < 4) ++a;
+  *M = 1 << (4 - a);
+  *D = *M / 2;
+}
+
 // Stage slot layout (bytes, each part 16-byte aligned):
-//   meta  : int32 npat, shift_lh, shift_col, shift_val, shift_n (32)
-//   lh    : uint32 [PB][W] + 16  sub-run bounds lo | hi << 16 of every (patient, sub-range), relative
-//           to the stage's first fiber (st_tab, built at init; bulk copy, shifted)
-//   col   : int32 [FB] + 16  F_V row byte offsets (bulk copy, shifted)
-//   val   : f64 [FB l] + 16   fiber values     (bulk copy, shifted)
-//   nrows : f64 [PB l R] + 16 N_k rows         (bulk copy, shifted)
+//   meta  : int32 npat, shift_lh, shift_tiles, shift_n (32)
+//   lh    : uint32 [PB][W] + 16   tile bounds lo | hi << 16 of every (patient, sub-range) relative to
+//           the stage's first tile (st_tab, built at init; bulk copy, shifted)
+//   tiles : [FT] x tile_bytes + 16  (bulk copy, shifted)
+//   nrows : f64 [PB l R] + 16      N_k rows (bulk copy, shifted)
 struct SlotGeom {
-  uint32_t lh, col, val, nrows, bytes;
+  uint32_t lh, tiles, nrows, bytes;
 };
 __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15) & ~(uint64_t)15); }
-__host__ __device__ inline SlotGeom slot_geom(int FB, int PB, int W, int l, int R) {
+__host__ __device__ inline SlotGeom slot_geom(int FT, int PB, int W, int l, int R) {
   SlotGeom s;
   s.lh = 32;
-  s.col = s.lh + al16(4ull * W * PB + 16);
-  s.val = s.col + al16(4ull * FB + 16);
-  s.nrows = s.val + al16(8ull * FB * l + 16);
+  s.tiles = s.lh + al16(4ull * W * PB + 16);
+  s.nrows = s.tiles + al16((uint64_t)tile_bytes(l) * FT + 16);
   s.bytes = (s.nrows + al16(8ull * PB * l * R + 16) + 127) & ~127u;
   return s;
 }
+__host__ __device__ inline uint32_t slice_bytes(int64_t Jg, int RS) {
+  return (uint32_t)(((uint64_t)(Jg + kScrRows) * RS * 8 + 127) & ~127ull);
+}
 
-constexpr int kScW = 4;          // pass-B consumer warps per CTA (label sub-ranges per group)
-constexpr int kScrD = 128;       // per-sub-range scratch doubles behind the F_V slice (redirected row updates)
+constexpr int kScW = 4;  // pass-B label sub-ranges per group
 
 // Shared-memory accesses by 32-bit shared addresses: the consumers hold their base addresses in
 // registers (with generic pointers the compiler re-derived the shared window, S2UR + ULEA, per tile).
@@ -143,23 +167,22 @@ __device__ __forceinline__ int lds_s32(uint32_t a) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ int lds_s32_if(uint32_t a, bool p, int dflt) {
-  int v = dflt;
-  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.b32 %0, [%1];\n}" : "+r"(v) : "r"(a), "r"((int)p));
-  return v;
-}
 __device__ __forceinline__ double lds_f64_if(uint32_t a, bool p) {
   double v = 0.0;
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}" : "+d"(v) : "r"(a), "r"((int)p));
   return v;
 }
-__device__ __forceinline__ double2 lds_v2(uint32_t a) {
-  double2 v;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+__device__ __forceinline__ double2 lds_v2_if(uint32_t a, bool p) {
+  double2 v = make_double2(0.0, 0.0);
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.shared.v2.f64 {%0, %1}, [%2];\n}"
+               : "+d"(v.x), "+d"(v.y)
+               : "r"(a), "r"((int)p));
   return v;
 }
-__device__ __forceinline__ void sts_v2(uint32_t a, double2 v) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
+__device__ __forceinline__ void sts_v2_if(uint32_t a, double2 v, bool p) {
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a),
+               "d"(v.x), "d"(v.y), "r"((int)p)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
   asm volatile(
@@ -170,21 +193,23 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
       : "memory");
 }
 
-// W label sub-ranges per group, CS consumer warps per sub-range: warp (w, c) owns the F_V rows of
-// sub-range w, columns [8 NT/CS c, 8 NT/CS (c + 1)) — disjoint words, no atomics. Per stage it reads
-// its sub-run bounds of every patient from the staged lh table, then runs 8-fiber MMA tiles
-// (M = fibers, N = r, K = a) with one tile in flight: the next tile's loads and MMAs are issued
-// before the F_V read-modify-write of the pending one (updates stay in tile order). Lanes outside
-// the sub-run or past column R are redirected to scratch words (branch-free updates).
+// CTA = (patient range, label group g) owns the F_V rows of group g in shared memory. One producer
+// warp streams the range's stages (<= FT tiles, <= PB patients) of the group's tiled stream into an
+// NS-deep ring with 1-D TMA bulk copies. W x CS consumer warps: warp (w, c) owns the rows of
+// sub-range (g, w), columns [8 NT/CS c, 8 NT/CS (c + 1)) — disjoint words, no atomics. Per stage
+// it reads its tile bounds of every patient from the staged lh table and runs one MMA per tile and
+// k-step (M = 8 slots, N = r, K = a) with one tile in flight: the next tile's loads and MMAs are
+// issued before the F_V read-modify-write of the pending one (updates stay in tile order). Lanes
+// whose columns are past R are predicated off.
 template <int KS, int NT, int W, int LT, int RT, int CS>
 __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
-    const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val, int G, int64_t Jg,
-    const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k, const int32_t* __restrict__ st_t,
-    const uint32_t* __restrict__ st_tab, const int32_t* __restrict__ cta_st, int l_, int R_, int RS_, int FB, int PB,
-    int NSt, const double* __restrict__ Nst, double* __restrict__ FVpart) {
+    const unsigned char* __restrict__ tiles, int G, int64_t Jg, const int64_t* __restrict__ st_f,
+    const int32_t* __restrict__ st_k, const int32_t* __restrict__ st_t, const uint32_t* __restrict__ st_tab,
+    const int32_t* __restrict__ cta_st, int l_, int R_, int RS_, int FT, int PB, int NSt,
+    const double* __restrict__ Nst, double* __restrict__ FVpart) {
   const int R = RT ? RT : R_;  // compile-time for the configured (R, l) shapes
   const int l = LT ? LT : l_;
-  const int RS = RT ? ((RT + 1) & ~1) : RS_;
+  const int RS = RS_;
   static_assert(NT % CS == 0, "column splits divide the n-tiles");
   constexpr int NTW = NT / CS;  // n-tiles per consumer warp
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -194,14 +219,15 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
   const int w = wc % W, cpart = wc / W;
   const int grp = blockIdx.x % G;
   const int64_t rng = blockIdx.x / G;
-  const SlotGeom sg = slot_geom(FB, PB, W, l, R);
-  double* Fs = (double*)smraw;  // Jg x RS, then W x kScrD doubles of scratch
-  const uint32_t fs_bytes = (uint32_t)(((uint64_t)Jg * RS * 8 + (uint64_t)W * kScrD * 8 + 127) & ~127ull);
+  const SlotGeom sg = slot_geom(FT, PB, W, l, R);
+  const uint32_t TB = tile_bytes(l);
+  double* Fs = (double*)smraw;  // (Jg + kScrRows) x RS
+  const uint32_t fs_bytes = slice_bytes(Jg, RS);
   uint64_t* full = (uint64_t*)(smraw + fs_bytes);
   uint64_t* empty = full + NSt;
   const uint32_t slots_off = fs_bytes + ((2 * NSt * 8 + 127) & ~127);
   unsigned char* slots = smraw + slots_off;
-  for (int64_t x = threadIdx.x; x < Jg * RS; x += blockDim.x) Fs[x] = 0.0;
+  for (int64_t x = threadIdx.x; x < (Jg + kScrRows) * RS; x += blockDim.x) Fs[x] = 0.0;
   if (threadIdx.x == 0) {
     for (int i = 0; i < NSt; ++i) {
       mbar_init(full + i, 1);
@@ -234,22 +260,19 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
         mbar_wait_park(empty + slot, phase, 1000000u);  // parked, no issue slots taken from consumers
         unsigned char* base = slots + (size_t)slot * sg.bytes;
         int32_t* mi = (int32_t*)base;
-        const uintptr_t sl = (uintptr_t)(st_tab + t0), sc = (uintptr_t)(fiber_col + f0),
-                        sv = (uintptr_t)(fiber_val + f0 * l), sn = (uintptr_t)(Nst + (int64_t)k0 * l * R);
-        const size_t bl = 4ull * W * (k1 - k0), bc = 4ull * (f1 - f0), bv = 8ull * (f1 - f0) * l,
-                     bn = 8ull * (k1 - k0) * l * R;
+        const uintptr_t sl = (uintptr_t)(st_tab + t0), sc = (uintptr_t)(tiles + (size_t)f0 * TB),
+                        sn = (uintptr_t)(Nst + (int64_t)k0 * l * R);
+        const size_t bl = 4ull * W * (k1 - k0), bc = (size_t)TB * (f1 - f0), bn = 8ull * (k1 - k0) * l * R;
         mi[0] = k1 - k0;
         mi[1] = (int32_t)(sl & 15);
         mi[2] = (int32_t)(sc & 15);
-        mi[3] = (int32_t)(sv & 15);
-        mi[4] = (int32_t)(sn & 15);
+        mi[3] = (int32_t)(sn & 15);
         // expected bytes first (same rounding as bulk_g2s_span), then the copies
-        const uint32_t tx = al16((sl & 15) + bl) + al16((sc & 15) + bc) + al16((sv & 15) + bv) + al16((sn & 15) + bn);
+        const uint32_t tx = al16((sl & 15) + bl) + al16((sc & 15) + bc) + al16((sn & 15) + bn);
         mbar_arrive_tx(full + slot, tx);
         uint32_t t2 = 0;
         bulk_g2s_span(base + sg.lh, (const void*)sl, bl, full + slot, &t2);
-        bulk_g2s_span(base + sg.col, (const void*)sc, bc, full + slot, &t2);
-        bulk_g2s_span(base + sg.val, (const void*)sv, bv, full + slot, &t2);
+        bulk_g2s_span(base + sg.tiles, (const void*)sc, bc, full + slot, &t2);
         bulk_g2s_span(base + sg.nrows, (const void*)sn, bn, full + slot, &t2);
         if (++slot == NSt) { slot = 0; phase ^= 1; }
       }
@@ -261,9 +284,6 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
     const int c0 = 8 * NTW * cpart;  // first F_V column of this warp's n-tiles
     const uint32_t sbase = smem_u32(smraw);
     const uint32_t fwA = sbase + 8u * (uint32_t)(c0 + 2 * t);  // + row byte offset + 64 nt: the lane's pair
-    // scratch words of this lane (the CS warps of a sub-range share them: redirected updates are
-    // never read back, so their interleaving is immaterial); + 64 nt stays inside kScrD doubles
-    const uint32_t scrA = sbase + 8u * (uint32_t)(Jg * RS + w * kScrD + 2 * lane);
     // B fragment B[t][g] = N(a = 4 ks + t, r = c0 + 8 nt + g); lanes outside (a < l, r < R) load nothing
     const int nb0 = t * R + g + c0;
     unsigned nok = 0;  // bit (ks NTW + nt): the lane's fragment is inside N
@@ -272,42 +292,40 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
 #pragma unroll
       for (int nt = 0; nt < NTW; ++nt)
         if (4 * ks + t < l && c0 + 8 * nt + g < R) nok |= 1u << (ks * NTW + nt);
-    bool colok[NTW];  // the lane's two columns of n-tile nt are inside R (else: scratch)
+    bool colok[NTW];  // the lane's two columns of n-tile nt are inside R (else: no access)
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) colok[nt] = c0 + 8 * nt + 2 * t < R;
     bool aok[KS];  // the lane's A fragment (a = 4 ks + t) is inside l
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) aok[ks] = 4 * ks + t < l;
-    uint32_t pA = scrA;  // pending tile: the lane's F_V row address (or scratch) and its products
+    // pending tile: the lane's F_V row address and its products (initially a zero update of a
+    // scratch row)
+    uint32_t pA = fwA + 8u * (uint32_t)(Jg * RS);
     double pcc[NTW][2];
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) pcc[nt][0] = pcc[nt][1] = 0.0;
     auto commit = [&]() {
-      uint32_t a[NTW];
       double2 v[NTW];
 #pragma unroll
-      for (int nt = 0; nt < NTW; ++nt) {
-        a[nt] = (colok[nt] ? pA : scrA) + 64u * nt;
-        v[nt] = lds_v2(a[nt]);
-      }
+      for (int nt = 0; nt < NTW; ++nt) v[nt] = lds_v2_if(pA + 64u * nt, colok[nt]);
 #pragma unroll
       for (int nt = 0; nt < NTW; ++nt) {
         v[nt].x += pcc[nt][0];
         v[nt].y += pcc[nt][1];
-        sts_v2(a[nt], v[nt]);
+        sts_v2_if(pA + 64u * nt, v[nt], colok[nt]);
       }
     };
     const uint32_t fullA = smem_u32(full), emptyA = smem_u32(empty);
+    const uint32_t aoff = 32u + 8u * (uint32_t)(8 * t + g);  // A fragment of k-step 0 inside a tile
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
       mbar_wait_a(fullA + 8u * slot, phase);
       const uint32_t sb = sbase + slots_off + (uint32_t)slot * sg.bytes;
       const int npat = lds_s32(sb);
       const uint32_t lhA = sb + sg.lh + lds_s32(sb + 4) + 4u * w;
-      const uint32_t colA = sb + sg.col + lds_s32(sb + 8) + 4u * g;
-      const uint32_t valA = sb + sg.val + lds_s32(sb + 12) + 8u * (uint32_t)(t + l * g);
-      const uint32_t nA = sb + sg.nrows + lds_s32(sb + 16) + 8u * nb0;
-      // per-patient setup (sub-run bounds, B fragments) one patient ahead of its tiles
+      const uint32_t tA = sb + sg.tiles + lds_s32(sb + 8);
+      const uint32_t nA = sb + sg.nrows + lds_s32(sb + 12) + 8u * nb0;
+      // per-patient setup (tile bounds, B fragments) one patient ahead of its tiles
       auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NTW]) {
         const uint32_t lh = (uint32_t)lds_s32(lhA + 4u * W * p);
         lo_ = (int)(lh & 0xffffu);
@@ -331,12 +349,12 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
           for (int nt = 0; nt < NTW; ++nt) bfr[ks][nt] = nbfr[ks][nt];
         if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
 #pragma unroll 2
-        for (int tb = lo; tb < hi; tb += 8) {
-          const bool ok = tb + g < hi;
-          const int rb = lds_s32_if(colA + 4u * tb, ok, 0);  // the fiber's F_V row byte offset
+        for (int tt = lo; tt < hi; ++tt) {
+          const uint32_t ta = tA + TB * (uint32_t)tt;
+          const int rb = lds_s32(ta + 4u * g);  // the slot's F_V row byte offset
           double av[KS];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(valA + 8u * (uint32_t)(l * tb + 4 * ks), ok && aok[ks]);
+          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(ta + aoff + 256u * ks, aok[ks]);
           double cc[NTW][2];
 #pragma unroll
           for (int nt = 0; nt < NTW; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
@@ -344,8 +362,8 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
           for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
             for (int nt = 0; nt < NTW; ++nt) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
-          commit();  // the previous tile (or a zero update of the scratch words)
-          pA = ok ? fwA + (uint32_t)rb : scrA;
+          commit();  // the previous tile
+          pA = fwA + (uint32_t)rb;
 #pragma unroll
           for (int nt = 0; nt < NTW; ++nt) { pcc[nt][0] = cc[nt][0]; pcc[nt][1] = cc[nt][1]; }
         }
@@ -364,24 +382,134 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
   }
 }
 
-// Init: the pass-B stage table of sub-run bounds. CTA c = (range, group c % G) walks its stages;
-// entry (stage s, patient k in [k0, k1), sub-range w) = lo | hi << 16 with [lo, hi) the fibers of
-// sub-range (g, w) of patient k inside the stage's fiber window [f0, f1), relative to f0.
-__global__ void k_stage_tab(const int64_t* __restrict__ gptr, const uint16_t* __restrict__ woff, int64_t K, int G,
+// ------------------------------------------------------------------ init: the tiled stream
+// Tiles per (group, patient) run and the tile offset of every sub-range inside it.
+__global__ void k_tile_counts(const uint16_t* __restrict__ woff, int64_t K, int G, int W, int32_t* __restrict__ tcnt,
+                              uint16_t* __restrict__ twoff) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= (int64_t)G * K) return;
+  const uint16_t* wo = woff + x * kWoS;
+  uint16_t* tw = twoff + x * kWoS;
+  int acc = 0;
+  for (int w = 0; w < W; ++w) {
+    tw[w] = (uint16_t)acc;
+    acc += (wo[w + 1] - wo[w] + 7) >> 3;
+  }
+  tw[W] = (uint16_t)acc;
+  tcnt[x] = acc;
+}
+
+// Thread per (group, patient, sub-range): the sub-run's n fibers (g-stream, sorted by label) go to
+// 8 ceil(n / 8) slots paired as described above. Pairs, in order: (class c rank i, class c + D rank
+// i) for every c < D; each class's surplus with a pad; the remaining surplus fibers with each other
+// (consecutive, possibly a same-half pair); pads with pads. Slot = 2 pair + side.
+__global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* __restrict__ woff,
+                              const int64_t* __restrict__ tptr, const uint16_t* __restrict__ twoff, int64_t K, int G,
+                              int W, int64_t Jg, int RS, int l, const int32_t* __restrict__ fiber_col,
+                              const double* __restrict__ fiber_val, unsigned char* __restrict__ tiles) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= (int64_t)G * K * W) return;
+  const int w = (int)(x % W);
+  const int64_t gk = x / W;
+  const int g = (int)(gk / K);
+  const int64_t k = gk - (int64_t)g * K;
+  const uint16_t* wo = woff + gk * kWoS;
+  const int64_t f0 = gptr[(int64_t)g * (K + 1) + k] + wo[w];
+  const int n = wo[w + 1] - wo[w];
+  if (n == 0) return;
+  const int T = (n + 7) >> 3, P = 8 * T - n;
+  const uint32_t TB = tile_bytes(l);
+  unsigned char* tb = tiles + (size_t)TB * (size_t)(tptr[(int64_t)g * (K + 1) + k] + twoff[gk * kWoS + w]);
+  int M, D;
+  pair_rule(RS, &M, &D);
+  const int64_t lab0 = (int64_t)g * Jg;
+  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) ++cnt[(int)((fiber_col[f0 + i] - lab0) & (M - 1))];
+  // pair bookkeeping per class pair c < D
+  int m[4], q[4], rem[4], base1[4], base2[4], off3[4], X[4];
+  int pair = 0, padsLeft = P;
+  for (int c = 0; c < D; ++c) {
+    m[c] = min(cnt[c], cnt[c + D]);
+    base1[c] = pair;
+    pair += m[c];
+    X[c] = cnt[c] >= cnt[c + D] ? c : c + D;
+  }
+  for (int c = 0; c < D; ++c) {
+    const int sur = abs(cnt[c] - cnt[c + D]);
+    q[c] = min(sur, padsLeft);
+    padsLeft -= q[c];
+    base2[c] = pair;
+    pair += q[c];
+    rem[c] = sur - q[c];
+  }
+  int tot3 = 0;
+  for (int c = 0; c < D; ++c) { off3[c] = tot3; tot3 += rem[c]; }
+  const int base3 = pair;  // phase-3 pairs: base3 .. base3 + ceil(tot3 / 2)
+  auto put = [&](int slot, int64_t rowlab, const double* v) {
+    unsigned char* tp = tb + (size_t)TB * (slot >> 3);
+    const int pos = slot & 7;
+    reinterpret_cast<int32_t*>(tp)[pos] = (int32_t)(rowlab * RS * 8);
+    double* vv = reinterpret_cast<double*>(tp + 32);
+    for (int a = 0; a < l; ++a) vv[a * 8 + pos] = v ? v[a] : 0.0;
+  };
+  int seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < n; ++i) {
+    const int64_t lab = fiber_col[f0 + i] - lab0;
+    const int c = (int)(lab & (M - 1)), cp = c % D;
+    const int r = seen[c]++;
+    int slot;
+    if (r < m[cp]) {
+      slot = 2 * (base1[cp] + r) + (c >= D ? 1 : 0);
+    } else {
+      const int j = r - m[cp];  // surplus rank (c == X[cp])
+      if (j < q[cp]) slot = 2 * (base2[cp] + j);
+      else {
+        const int s = off3[cp] + (j - q[cp]);
+        slot = 2 * base3 + s;  // consecutive slots: pairs (s even, s odd)
+      }
+    }
+    put(slot, lab, fiber_val + (f0 + i) * l);
+  }
+  // pads: partners of the phase-2 surplus, the odd phase-3 tail, then pad pairs
+  auto scr = [&](int cls) -> int64_t { return Jg + (((int64_t)cls - Jg) & (M - 1)); };
+  for (int c = 0; c < D; ++c)
+    for (int j = 0; j < q[c]; ++j) put(2 * (base2[c] + j) + 1, scr((X[c] + D) & (M - 1)), nullptr);
+  int s = 2 * base3 + tot3;
+  for (; s < 8 * T; ++s) put(s, scr((s & 1) ? D : 0), nullptr);
+}
+
+void launch_tile_counts(Handle& h, int32_t* tcnt) {
+  const int64_t n = (int64_t)h.sc_G * h.K;
+  if (n == 0) return;
+  k_tile_counts<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.woff, h.K, h.sc_G, h.sc_W, tcnt, h.twoff);
+}
+
+void launch_build_tiles(Handle& h) {
+  if (!h.sc_ok || h.K == 0) return;
+  const int64_t n = (int64_t)h.sc_G * h.K * h.sc_W;
+  k_build_tiles<<<(unsigned)((n + 127) / 128), 128, 0, h.stream>>>(h.gptr, h.woff, h.tptr, h.twoff, h.K, h.sc_G,
+                                                                   h.sc_W, h.sc_Jg, h.sc_RS, h.l, h.fiber_col,
+                                                                   h.fiber_val, h.tiles);
+}
+
+// Init: the pass-B stage table of tile bounds. CTA c = (range, group c % G) walks its stages;
+// entry (stage s, patient k in [k0, k1), sub-range w) = lo | hi << 16 with [lo, hi) the tiles of
+// sub-range (g, w) of patient k inside the stage's tile window [t0, t1), relative to t0.
+__global__ void k_stage_tab(const int64_t* __restrict__ tptr, const uint16_t* __restrict__ twoff, int64_t K, int G,
                             int W, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
                             const int32_t* __restrict__ st_t, const int32_t* __restrict__ cta_st,
                             uint32_t* __restrict__ st_tab) {
   const int c = blockIdx.x, grp = c % G;
-  const int64_t* gp = gptr + (int64_t)grp * (K + 1);
+  const int64_t* tp = tptr + (int64_t)grp * (K + 1);
   for (int s = cta_st[c] + threadIdx.x; s < cta_st[c + 1]; s += blockDim.x) {
-    const int64_t f0 = st_f[2 * (int64_t)s], f1 = st_f[2 * (int64_t)s + 1];
+    const int64_t t0 = st_f[2 * (int64_t)s], t1 = st_f[2 * (int64_t)s + 1];
     const int32_t k0 = st_k[2 * (int64_t)s], k1 = st_k[2 * (int64_t)s + 1];
     uint32_t* out = st_tab + st_t[s];
     for (int32_t k = k0; k < k1; ++k) {
-      const uint16_t* wo = woff + ((int64_t)grp * K + k) * kWoS;
+      const uint16_t* tw = twoff + ((int64_t)grp * K + k) * kWoS;
       for (int w = 0; w < W; ++w) {
-        const int64_t lo = min(max(gp[k] + wo[w], f0), f1) - f0;
-        const int64_t hi = min(max(gp[k] + wo[w + 1], f0), f1) - f0;
+        const int64_t lo = min(max(tp[k] + tw[w], t0), t1) - t0;
+        const int64_t hi = min(max(tp[k] + tw[w + 1], t0), t1) - t0;
         out[(int64_t)(k - k0) * W + w] = (uint32_t)lo | ((uint32_t)hi << 16);
       }
     }
@@ -390,7 +518,7 @@ __global__ void k_stage_tab(const int64_t* __restrict__ gptr, const uint16_t* __
 
 void launch_stage_tab(Handle& h) {
   if (!h.sc_ok || h.nst == 0) return;
-  k_stage_tab<<<(unsigned)(h.sc_ranges * h.sc_G), 128, 0, h.stream>>>(h.gptr, h.woff, h.K, h.sc_G, h.sc_W, h.st_f,
+  k_stage_tab<<<(unsigned)(h.sc_ranges * h.sc_G), 128, 0, h.stream>>>(h.tptr, h.twoff, h.K, h.sc_G, h.sc_W, h.st_f,
                                                                       h.st_k, h.st_t, h.cta_st, h.st_tab);
 }
 
@@ -412,9 +540,9 @@ static void scatter_inst_w(Handle& h) {
   constexpr auto fn = k_scatter_tma<KS, NT, W, LT, RT, CS>;
   max_smem_attr<fn>(h);
   const int ctas = h.sc_ranges * h.sc_G;
-  fn<<<ctas, 32 * (W * CS + 1), h.sc_smem, h.stream>>>(h.fiber_col, h.fiber_val, h.sc_G, h.sc_Jg, h.st_f, h.st_k,
-                                                        h.st_t, h.st_tab, h.cta_st, h.l, h.R, h.sc_RS, h.sc_FB,
-                                                        h.sc_PB, h.sc_NS, h.Nst, h.fv_part);
+  fn<<<ctas, 32 * (W * CS + 1), h.sc_smem, h.stream>>>(h.tiles, h.sc_G, h.sc_Jg, h.st_f, h.st_k, h.st_t, h.st_tab,
+                                                        h.cta_st, h.l, h.R, h.sc_RS, h.sc_FB, h.sc_PB, h.sc_NS, h.Nst,
+                                                        h.fv_part);
   int64_t n = h.Jl * h.R;
   k_sum_ranges<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.fv_part, h.sc_ranges, h.Jl, h.R, h.inv, h.FV);
 }
@@ -456,21 +584,22 @@ int launch_scatter_fibers(Handle& h) {
   return 2;
 }
 
-// Chooses the label groups G (F_V slice of a CTA), stage geometry and the number of pass-B patient
-// ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared memory.
+// Chooses the label groups G (F_V slice of a CTA), stage geometry (sc_FB = tiles per stage) and the
+// number of pass-B patient ranges so that one CTA's F_V slice plus its NS-stage ring fits in shared
+// memory. RS (F_V row stride) = R rounded up to even, with 2-adic order <= 3 (pair_rule).
 void plan_scatter(Handle& h) {
   const size_t budget = 225 * 1024;
-  h.sc_W = kScW;  // label sub-ranges per group (2 or 4)
+  h.sc_W = kScW;
   h.sc_RS = (h.R + 1) & ~1;
-  h.sc_FB = 256;
+  if (h.sc_RS % 16 == 0) h.sc_RS += 2;
+  h.sc_FB = 32;
   h.sc_ok = 0;
   const int pbs[3] = {16, 8, 4};
-  const int gmin = 1;
   for (int pass = 0; pass < 2 && !h.sc_ok; ++pass)  // pass 0: >= 3 stages of >= 8 patients
-    for (int G = gmin; G <= kMaxGroups && !h.sc_ok; ++G) {
+    for (int G = 1; G <= kMaxGroups && !h.sc_ok; ++G) {
       const int64_t Js = (h.J + (int64_t)G * h.sc_W - 1) / ((int64_t)G * h.sc_W);
       const int64_t Jg = Js * h.sc_W;
-      const size_t fs = ((size_t)Jg * h.sc_RS * 8 + (size_t)h.sc_W * kScrD * 8 + 127) & ~(size_t)127;
+      const size_t fs = slice_bytes(Jg, h.sc_RS);
       for (int NSt = 4; NSt >= (pass ? 2 : 3) && !h.sc_ok; --NSt)
         for (int pi = 0; pi < (pass ? 3 : 2) && !h.sc_ok; ++pi) {
           const SlotGeom sg = slot_geom(h.sc_FB, pbs[pi], h.sc_W, h.l, h.R);
@@ -487,17 +616,17 @@ void plan_scatter(Handle& h) {
           }
         }
     }
-  // Larger stages (FB = 512: fewer per-stage overheads; measured 43 -> 40 ms at Scale, 2.26 -> 2.10 ms
-  // at Medium) when they still fit at the same G with >= 3 slots of >= 8 patients.
+  // Larger stages (64 tiles: fewer per-stage overheads) when they still fit at the same G with >= 3
+  // slots of >= 8 patients.
   if (h.sc_ok) {
-    const size_t fs = ((size_t)h.sc_Jg * h.sc_RS * 8 + (size_t)h.sc_W * kScrD * 8 + 127) & ~(size_t)127;
+    const size_t fs = slice_bytes(h.sc_Jg, h.sc_RS);
     bool done = false;
     for (int NSt = 4; NSt >= 3 && !done; --NSt)
       for (int pi = 0; pi < 2 && !done; ++pi) {
-        const SlotGeom sg = slot_geom(512, pbs[pi], h.sc_W, h.l, h.R);
+        const SlotGeom sg = slot_geom(64, pbs[pi], h.sc_W, h.l, h.R);
         const size_t bytes = fs + ((2 * NSt * 8 + 127) & ~127) + (size_t)NSt * sg.bytes;
         if (bytes <= budget) {
-          h.sc_FB = 512;
+          h.sc_FB = 64;
           h.sc_PB = pbs[pi];
           h.sc_NS = NSt;
           h.sc_slot = sg.bytes;
@@ -521,50 +650,47 @@ void plan_scatter(Handle& h) {
 
 bool scatter_smem_ok(const Handle& h) { return h.sc_ok != 0; }
 
-// Init (after layoutA has copied the labels): the g-stream labels become F_V slice offsets
-// (label - g Jg) RS, so pass B addresses a fiber's F_V row without index arithmetic.
-__global__ void k_fiber_rowoff(const int64_t* __restrict__ gptr, int64_t K, int G, int64_t Jg, int RS,
-                               int32_t* __restrict__ fiber_col) {
-  for (int g = 0; g < G; ++g) {
-    const int64_t f0 = gptr[(int64_t)g * (K + 1)], f1 = gptr[(int64_t)g * (K + 1) + K];
-    for (int64_t f = f0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < f1; f += (int64_t)gridDim.x * blockDim.x)
-      fiber_col[f] = (int32_t)((fiber_col[f] - g * Jg) * RS * 8);  // bytes
-  }
-}
-
-void launch_fiber_rowoff(Handle& h) {
-  if (!h.sc_ok || h.K == 0) return;
-  k_fiber_rowoff<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.gptr, h.K, h.sc_G, h.sc_Jg, h.sc_RS, h.fiber_col);
+// Tiles of the tiled stream: sum over sub-runs of ceil(n / 8) <= F / 8 + (non-empty sub-runs).
+int64_t tiles_cap(const Handle& h) {
+  const int64_t runs = std::min<int64_t>(h.F, (int64_t)h.sc_G * h.K * h.sc_W);
+  return h.F / 8 + runs + 8;
 }
 
 // stage-table entries: every stage holds its patients' sub-range bounds; a patient's run is split
-// over at most (run / FB + 2) stages, so sum over stages of (k1 - k0) <= G K + nst
+// over at most (run / FT + 2) stages, so sum over stages of (k1 - k0) <= G K + nst
 int64_t stage_tab_cap(const Handle& h) { return ((int64_t)h.sc_G * h.K + stage_cap(h)) * h.sc_W + 16; }
 
 int64_t stage_cap(const Handle& h) {
-  return h.F / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
+  return tiles_cap(h) / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
 }
 
-// Host planning from the per-group run lengths gcnt[g][k]: stream offsets gptr (absolute), pass-B
-// patient ranges (balanced by fibers) and the stage table of every (range, group) CTA.
-void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int64_t>& st_f, std::vector<int32_t>& st_k,
+// Run offsets from per-(group, patient) run lengths cnt[g][k]: ptr[g][k] (absolute, groups one after
+// the other).
+void prefix_runs(const Handle& h, const int32_t* cnt, int64_t* ptr) {
+  const int64_t K = h.K, K1 = K + 1;
+  int64_t base = 0;
+  for (int g = 0; g < h.sc_G; ++g) {
+    int64_t* gp = ptr + g * K1;
+    gp[0] = base;
+    for (int64_t k = 0; k < K; ++k) gp[k + 1] = gp[k] + cnt[g * K + k];
+    base = gp[K];
+  }
+}
+
+// Host planning from the per-group tile counts tcnt[g][k]: tile offsets tptr, pass-B patient ranges
+// (balanced by tiles) and the stage table of every (range, group) CTA.
+void plan_streams(Handle& h, const int32_t* tcnt, int64_t* tptr, std::vector<int64_t>& st_f, std::vector<int32_t>& st_k,
                   std::vector<int32_t>& st_t, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k) {
   const int G = h.sc_G;
   const int64_t K = h.K, K1 = K + 1;
-  int64_t base = 0;
-  for (int g = 0; g < G; ++g) {
-    int64_t* gp = gptr + g * K1;
-    gp[0] = base;
-    for (int64_t k = 0; k < K; ++k) gp[k + 1] = gp[k] + gcnt[g * K + k];
-    base = gp[K];
-  }
-  // balanced patient ranges by total fibers
+  prefix_runs(h, tcnt, tptr);
+  // balanced patient ranges by total tiles
   const int nr = h.sc_ranges;
   block_k.assign((size_t)nr + 1, 0);
   std::vector<int64_t> tot((size_t)K1, 0);
   for (int64_t k = 0; k < K; ++k) {
     int64_t c = 0;
-    for (int g = 0; g < G; ++g) c += gcnt[g * K + k];
+    for (int g = 0; g < G; ++g) c += tcnt[g * K + k];
     tot[(size_t)k + 1] = tot[(size_t)k] + c;
   }
   for (int b = 0; b <= nr; ++b) {
@@ -576,11 +702,11 @@ void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int
   st_f.clear();
   st_k.clear();
   cta_st.assign((size_t)nr * G + 1, 0);
-  const int64_t FB = h.sc_FB, PB = h.sc_PB;
+  const int64_t FT = h.sc_FB, PB = h.sc_PB;
   for (int r = 0; r < nr; ++r)
     for (int g = 0; g < G; ++g) {
       cta_st[(size_t)r * G + g] = (int32_t)(st_k.size() / 2);
-      const int64_t* gp = gptr + g * K1;
+      const int64_t* gp = tptr + g * K1;
       const int64_t kr0 = block_k[(size_t)r], kr1 = block_k[(size_t)r + 1];
       if (kr0 >= kr1) continue;
       int64_t f = gp[kr0];
@@ -588,7 +714,7 @@ void plan_streams(Handle& h, const int32_t* gcnt, int64_t* gptr, std::vector<int
       int64_t k = kr0;
       while (f < fend) {
         while (gp[k + 1] <= f) ++k;  // first patient whose run ends after f
-        int64_t f1 = std::min(f + FB, fend);
+        int64_t f1 = std::min(f + FT, fend);
         int64_t kk = k + 1;
         while (kk < kr1 && gp[kk] < f1) ++kk;
         if (kk - k > PB) {
