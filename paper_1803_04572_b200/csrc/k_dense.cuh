@@ -661,13 +661,24 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
   const int hoff = ((R * R + 31) / 32) * 32;
   double* Hs = sm;                 // R x R
   double* Gs = sm + hoff;          // R x R  (G_W + rho I)^-1
+  constexpr int KA = 2 * NT;       // k-steps of the batched W-row solves (K = columns, permuted, see below)
+  double* gfr = sm + 2 * hoff;     // (G_W + rho I)^-1 as MMA B fragments [KA][NT][lane]
   const int wib = threadIdx.x >> 5;
-  double* wv = sm + 2 * hoff + wib * (3 * RP * 32 + MT * 8 * RP);  // per warp: fw, w̄, d as [r][lane] + N scratch
+  double* wv = sm + 2 * hoff + KA * NT * 32 + wib * (3 * RP * 32 + MT * 8 * RP);  // per warp: fw, w̄, d as [r][lane] + N scratch
   double* fwv = wv;
   double* wbv = wv + RP * 32;
   double* dv = wv + 2 * RP * 32;
   double* ns = wv + 3 * RP * 32;   // N_p (MT 8 x RP)
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Gs[x] = GWi[x]; }
+  // Batched W-row solve z_p = Ginv rhs_p of a warp round as MMAs (M = 8 patients, N = r, K = q) whose
+  // A operand is the rhs in accumulator (C) layout: k-step ks, lane t covers column
+  // q = 8 (ks / 2) + 2 t + ks % 2 — exactly the C-fragment element (n-tile ks / 2, ks % 2) a lane
+  // holds, so the ADMM steps need no shuffles. B[t][g] = Ginv^T(q, r = 8 nt + g) = Ginv(r, q).
+  for (int x = threadIdx.x; x < KA * NT * 32; x += blockDim.x) {
+    const int ln = x & 31, nt = (x >> 5) % NT, ks = (x >> 5) / NT;
+    const int q = 8 * (ks >> 1) + 2 * (ln & 3) + (ks & 1), r = 8 * nt + (ln >> 2);
+    gfr[x] = (q < R && r < R) ? GWi[r * R + q] : 0.0;
+  }
   __syncthreads();
   const double rho = scal[S_RHO_W];
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
@@ -776,41 +787,70 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
       }
     }
     __syncwarp();
-    // ---- W-row ADMM (thread = patient)
+    // ---- W-row ADMM: z = Ginv (f + rho (w̄ + d)), w̄ = prox(z - d), d += w̄ - z, n_inner steps
     const int64_t kme = base + lane;
     int nsteps = 0;
     if (kme < K) {
       for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
-      if (tol > 0.0) {
-        // per-row inner stop (reading R-inner-tol); out of line, so that the fixed-step loop below keeps
-        // its register allocation
-        nsteps = w_row_admm_tol(Gs, R, fwv + lane, wbv + lane, dv + lane, rho, n_inner, kind, param, tol);
-      } else {
+    } else {
+      for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = 0.0; dv[r * 32 + lane] = 0.0; }
+    }
+    if (tol > 0.0) {
+      // per-row inner stop (reading R-inner-tol): thread per patient, out of line
+      if (kme < K) nsteps = w_row_admm_tol(Gs, R, fwv + lane, wbv + lane, dv + lane, rho, n_inner, kind, param, tol);
+    } else {
+      // fixed steps: the warp's 32 rows at once, 8 patients (one M tile) at a time; the rows of
+      // patients past K stay zero (f = w̄ = d = 0 and prox(0) = 0)
+      __syncwarp();
+#pragma unroll 1
+      for (int mt = 0; mt < 4; ++mt) {
+        const int p = 8 * mt + g;
+        double f[NT][2], wb[NT][2], dd[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int r = 8 * nt + 2 * t + c;
+            f[nt][c] = (r < R && p < np) ? fwv[r * 32 + p] : 0.0;  // (rows p >= np hold stale sums)
+            wb[nt][c] = r < R ? wbv[r * 32 + p] : 0.0;
+            dd[nt][c] = r < R ? dv[r * 32 + p] : 0.0;
+          }
+#pragma unroll 1
         for (int it = 0; it < n_inner; ++it) {
-          double rhs[RP];
+          double a[KA], z[NT][2];
 #pragma unroll
-          for (int r = 0; r < RP; ++r)
-            rhs[r] = r < R ? fwv[r * 32 + lane] + rho * (wbv[r * 32 + lane] + dv[r * 32 + lane]) : 0.0;
+          for (int ks = 0; ks < KA; ++ks) a[ks] = f[ks >> 1][ks & 1] + rho * (wb[ks >> 1][ks & 1] + dd[ks >> 1][ks & 1]);
 #pragma unroll
-          for (int r = 0; r < RP; ++r) {
+          for (int nt = 0; nt < NT; ++nt) {
+            z[nt][0] = z[nt][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < KA; ++ks) dmma2(z[nt][0], z[nt][1], a[ks], gfr[(ks * NT + nt) * 32 + lane]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const double nb = prox(kind, param, rho, z[nt][c] - dd[nt][c]);
+              dd[nt][c] = dd[nt][c] + nb - z[nt][c];
+              wb[nt][c] = nb;
+            }
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const int r = 8 * nt + 2 * t + c;
             if (r < R) {
-              double z = 0.0;
-#pragma unroll
-              for (int q = 0; q < RP; ++q)
-                if (q < R) z = fma(Gs[r * R + q], rhs[q], z);
-              const double d0 = dv[r * 32 + lane];
-              const double nb = prox(kind, param, rho, z - d0);
-              dv[r * 32 + lane] = d0 + nb - z;
-              wbv[r * 32 + lane] = nb;
+              wbv[r * 32 + p] = wb[nt][c];
+              dv[r * 32 + p] = dd[nt][c];
             }
           }
-        }
-        nsteps = n_inner;
       }
-      for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
-    } else {
-      for (int r = 0; r < R; ++r) wbv[r * 32 + lane] = 0.0;
+      __syncwarp();
+      nsteps = kme < K ? n_inner : 0;
     }
+    if (kme < K)
+      for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
     steps_warp(steps + 1, nsteps);
     __syncwarp();
     // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T  (MMA with K = patients)
@@ -908,7 +948,8 @@ static void passB_wide_inst(Handle& h) {
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
   size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32 + MT * 8 * RP);
   size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
-  size_t smem = sizeof(double) * 2 * hoff + (per_warp * (kDenseThreads / 32) > red ? per_warp * (kDenseThreads / 32) : red);
+  const size_t gfr = sizeof(double) * (size_t)(2 * NT * NT * 32);
+  size_t smem = sizeof(double) * 2 * hoff + (gfr + per_warp * (kDenseThreads / 32) > red ? gfr + per_warp * (kDenseThreads / 32) : red);
   max_smem_attr<fn>(h);
   int64_t rounds = (h.K + 31) / 32;
   int64_t blocks = (rounds + 3) / 4;
