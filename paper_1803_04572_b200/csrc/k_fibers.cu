@@ -115,14 +115,21 @@ void launch_relabel_V(Handle& h) {
 // after patient, sub-range after sub-range, the sub-run of (patient k, sub-range (g, w)) is cut into
 // ceil(n / 8) tiles of 8 fiber slots, each tile
 //   int32 rowoff[8]   F_V row byte offset (label - g Jg) RS 8 inside the CTA's shared-memory slice
-//   f64   val[l][8]   x'(a, slot), a-major: the MMA A fragment of a k-step (a = 4 ks + t, slot g) is
-//                     256 contiguous bytes (two conflict-free wavefronts)
+//   f64   val         x'(a, slot) in blocks of nb = min(4, l - 4 b) a's (b = a / 4): byte 256 b +
+//                     32 nb (slot / 4) + 32 (a % 4) + 8 (slot % 4), so the MMA A fragment of a
+//                     k-step (a = 4 ks + t, slot g) is one block whose two half-warps each read 32 nb
+//                     contiguous bytes (two conflict-free wavefronts; a-major rows of 64 bytes
+//                     measured 4, a zero-padded last block made the tiles larger and pass B slower)
 // Padding slots hold zeros and address one of the scratch rows behind the slice. The slots of a tile
 // are paired (2i, 2i + 1) so that the two rows one quarter-warp touches in an F_V read-modify-write
 // lie in opposite halves of the 32 banks (row labels differ by D mod M, see pair_rule); pads are
 // wildcards that take the partner class. tptr[g][k]: first tile of (g, k); twoff[g][k][w]: tile
 // offset of sub-range w inside it.
 __host__ __device__ inline uint32_t tile_bytes(int l) { return 32u + 64u * (uint32_t)l; }
+__host__ __device__ inline uint32_t tile_val_off(int l, int a, int slot) {  // byte offset of x'(a, slot)
+  const int b = a >> 2, nb = min(4, l - 4 * b);
+  return 32u + 256u * b + 32u * nb * (slot >> 2) + 32u * (a & 3) + 8u * (slot & 3);
+}
 constexpr int kScrRows = 8;  // scratch rows behind the F_V slice (pads; any label class mod M <= 8)
 
 // Rows j0, j1 with byte offsets 8 RS j: their 64-byte segments (same columns) are bank-disjoint iff
@@ -295,9 +302,13 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
     bool colok[NTW];  // the lane's two columns of n-tile nt are inside R (else: no access)
 #pragma unroll
     for (int nt = 0; nt < NTW; ++nt) colok[nt] = c0 + 8 * nt + 2 * t < R;
-    bool aok[KS];  // the lane's A fragment (a = 4 ks + t) is inside l
+    bool aok[KS];      // the lane's A fragment (a = 4 ks + t) is inside l
+    uint32_t aoff[KS];  // ... and its byte offset inside a tile
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) aok[ks] = 4 * ks + t < l;
+    for (int ks = 0; ks < KS; ++ks) {
+      aok[ks] = 4 * ks + t < l;
+      aoff[ks] = aok[ks] ? tile_val_off(l, 4 * ks + t, g) : 0u;
+    }
     // pending tile: the lane's F_V row address and its products (initially a zero update of a
     // scratch row)
     uint32_t pA = fwA + 8u * (uint32_t)(Jg * RS);
@@ -316,7 +327,6 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
       }
     };
     const uint32_t fullA = smem_u32(full), emptyA = smem_u32(empty);
-    const uint32_t aoff = 32u + 8u * (uint32_t)(8 * t + g);  // A fragment of k-step 0 inside a tile
     int slot = 0, phase = 0;
     for (int i = 0; i < ns; ++i) {
       mbar_wait_a(fullA + 8u * slot, phase);
@@ -354,7 +364,7 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
           const int rb = lds_s32(ta + 4u * g);  // the slot's F_V row byte offset
           double av[KS];
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(ta + aoff + 256u * ks, aok[ks]);
+          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(ta + aoff[ks], aok[ks]);
           double cc[NTW][2];
 #pragma unroll
           for (int nt = 0; nt < NTW; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
@@ -449,8 +459,7 @@ __global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* 
     unsigned char* tp = tb + (size_t)TB * (slot >> 3);
     const int pos = slot & 7;
     reinterpret_cast<int32_t*>(tp)[pos] = (int32_t)(rowlab * RS * 8);
-    double* vv = reinterpret_cast<double*>(tp + 32);
-    for (int a = 0; a < l; ++a) vv[a * 8 + pos] = v ? v[a] : 0.0;
+    for (int a = 0; a < l; ++a) *reinterpret_cast<double*>(tp + tile_val_off(l, a, pos)) = v ? v[a] : 0.0;
   };
   int seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int i = 0; i < n; ++i) {
