@@ -113,7 +113,7 @@ size_t carve(Handle& h, char* base) {
     h.st_k = c.take<int32_t>(2 * h.nst_cap);
     h.cta_st = c.take<int32_t>((int64_t)h.sc_ranges * G + 1);
     h.st_t = c.take<int32_t>(h.nst_cap + 1);
-    h.st_tab = c.take<uint32_t>(stage_tab_cap(h));
+    h.st_list = c.take<uint32_t>(stage_tab_cap(h));
     h.layout_tmp_bytes = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;  // per-group run lengths
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
@@ -373,6 +373,12 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       std::vector<int32_t> st_k, st_t, cta_st;
       plan_streams(h, tcnt.data(), tptr.data(), st_f, st_k, st_t, cta_st, block_k);
       h.nst = (int64_t)st_k.size() / 2;
+      if (tm.on)
+        fprintf(stderr,
+                "[copa init] pass B: G=%d Jg=%lld W=%d RS=%d tiles/stage=%d patients/stage=%d slots=%d smem=%zu "
+                "ranges=%d stages=%lld tiles=%lld (cap %lld) fibers=%lld workspace=%zu\n",
+                h.sc_G, (long long)h.sc_Jg, h.sc_W, h.sc_RS, h.sc_FB, h.sc_PB, h.sc_NS, h.sc_smem, h.sc_ranges,
+                (long long)h.nst, (long long)tptr.back(), (long long)tiles_cap(h), (long long)h.F, bytes);
       if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F || tptr[tptr.size() - 1] > tiles_cap(h) ||
           (int64_t)st_t.back() > stage_tab_cap(h) || stage_tab_cap(h) > INT32_MAX) {
         delete H;

@@ -86,8 +86,8 @@ struct Handle {
   int64_t* st_f;         // [nst_cap x 2] pass-B stage: logical fiber range [f0, f1) in its stream
   int32_t* st_k;         // [nst_cap x 2] pass-B stage: patient range [k0, k1)
   int32_t* cta_st;       // [sc_ranges x G + 1] first stage of each pass-B CTA
-  int32_t* st_t;         // [nst_cap + 1] pass-B stage: first entry in st_tab
-  uint32_t* st_tab;      // pass-B stage table: tile bounds lo | hi << 16 per (stage, patient, sub-range)
+  int32_t* st_t;         // [nst_cap + 1] pass-B stage: first entry in st_list
+  uint32_t* st_list;     // pass-B stage lists: per stage 8 sub-range offsets + (tile | patient << 16) per tile
   unsigned char* tiles;  // pass-B tiled stream (k_fibers.cu): per group, patient, sub-range: 8-slot tiles
   int64_t* tptr;         // [G x (K + 1)] first tile of each (group, patient) run
   uint16_t* twoff;       // [G x K x kWoS] tile offset of each sub-range inside its run

@@ -143,9 +143,10 @@ __host__ __device__ inline void pair_rule(int RS, int* M, int* D) {
 }
 
 // Stage slot layout (bytes, each part 16-byte aligned):
-//   meta  : int32 npat, shift_lh, shift_tiles, shift_n (32)
-//   lh    : uint32 [PB][W] + 16   tile bounds lo | hi << 16 of every (patient, sub-range) relative to
-//           the stage's first tile (st_tab, built at init; bulk copy, shifted)
+//   meta  : int32 npat, shift_list, shift_tiles, shift_n (32)
+//   list  : uint32 [8 + FT] + 16   the stage's tile list (st_list, built at init; bulk copy, shifted):
+//           8 offsets e[w] (w = 0..W), then the tiles grouped by sub-range, entry = tile | patient << 16
+//           (relative to the stage), sub-range w's tiles at [e[w], e[w + 1])
 //   tiles : [FT] x tile_bytes + 16  (bulk copy, shifted)
 //   nrows : f64 [PB l R] + 16      N_k rows (bulk copy, shifted)
 struct SlotGeom {
@@ -155,7 +156,7 @@ __host__ __device__ inline uint32_t al16(uint64_t x) { return (uint32_t)((x + 15
 __host__ __device__ inline SlotGeom slot_geom(int FT, int PB, int W, int l, int R) {
   SlotGeom s;
   s.lh = 32;
-  s.tiles = s.lh + al16(4ull * W * PB + 16);
+  s.tiles = s.lh + al16(4ull * (8 + FT) + 16);
   s.nrows = s.tiles + al16((uint64_t)tile_bytes(l) * FT + 16);
   s.bytes = (s.nrows + al16(8ull * PB * l * R + 16) + 127) & ~127u;
   return s;
@@ -186,6 +187,9 @@ __device__ __forceinline__ double2 lds_v2_if(uint32_t a, bool p) {
                : "r"(a), "r"((int)p));
   return v;
 }
+__device__ __forceinline__ void lds_f64_keep(double& v, uint32_t a, bool p) {  // v unchanged when !p
+  asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}" : "+d"(v) : "r"(a), "r"((int)p));
+}
 __device__ __forceinline__ void sts_v2_if(uint32_t a, double2 v, bool p) {
   asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q st.shared.v2.f64 [%0], {%1, %2};\n}" ::"r"(a),
                "d"(v.x), "d"(v.y), "r"((int)p)
@@ -211,7 +215,7 @@ __device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
 template <int KS, int NT, int W, int LT, int RT, int CS>
 __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
     const unsigned char* __restrict__ tiles, int G, int64_t Jg, const int64_t* __restrict__ st_f,
-    const int32_t* __restrict__ st_k, const int32_t* __restrict__ st_t, const uint32_t* __restrict__ st_tab,
+    const int32_t* __restrict__ st_k, const int32_t* __restrict__ st_t, const uint32_t* __restrict__ st_list,
     const int32_t* __restrict__ cta_st, int l_, int R_, int RS_, int FT, int PB, int NSt,
     const double* __restrict__ Nst, double* __restrict__ FVpart) {
   const int R = RT ? RT : R_;  // compile-time for the configured (R, l) shapes
@@ -267,9 +271,9 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
         mbar_wait_park(empty + slot, phase, 1000000u);  // parked, no issue slots taken from consumers
         unsigned char* base = slots + (size_t)slot * sg.bytes;
         int32_t* mi = (int32_t*)base;
-        const uintptr_t sl = (uintptr_t)(st_tab + t0), sc = (uintptr_t)(tiles + (size_t)f0 * TB),
+        const uintptr_t sl = (uintptr_t)(st_list + t0), sc = (uintptr_t)(tiles + (size_t)f0 * TB),
                         sn = (uintptr_t)(Nst + (int64_t)k0 * l * R);
-        const size_t bl = 4ull * W * (k1 - k0), bc = (size_t)TB * (f1 - f0), bn = 8ull * (k1 - k0) * l * R;
+        const size_t bl = 4ull * (8 + (f1 - f0)), bc = (size_t)TB * (f1 - f0), bn = 8ull * (k1 - k0) * l * R;
         mi[0] = k1 - k0;
         mi[1] = (int32_t)(sl & 15);
         mi[2] = (int32_t)(sc & 15);
@@ -331,51 +335,84 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
     for (int i = 0; i < ns; ++i) {
       mbar_wait_a(fullA + 8u * slot, phase);
       const uint32_t sb = sbase + slots_off + (uint32_t)slot * sg.bytes;
-      const int npat = lds_s32(sb);
-      const uint32_t lhA = sb + sg.lh + lds_s32(sb + 4) + 4u * w;
+      const uint32_t lA = sb + sg.lh + lds_s32(sb + 4);
       const uint32_t tA = sb + sg.tiles + lds_s32(sb + 8);
       const uint32_t nA = sb + sg.nrows + lds_s32(sb + 12) + 8u * nb0;
-      // per-patient setup (tile bounds, B fragments) one patient ahead of its tiles
-      auto setup = [&](int p, int& lo_, int& hi_, double (&b)[KS][NTW]) {
-        const uint32_t lh = (uint32_t)lds_s32(lhA + 4u * W * p);
-        lo_ = (int)(lh & 0xffffu);
-        hi_ = (int)(lh >> 16);
-        const uint32_t np = nA + 8u * (uint32_t)(p * per);
+      const int e0 = lds_s32(lA + 4u * w), e1 = lds_s32(lA + 4u * (w + 1));
+      // Software pipeline over this warp's tiles of the stage (flat list): iteration e issues the
+      // F_V load of the pending tile e - 1, the loads of tile e + 1 (entry of e + 2), the MMAs of
+      // tile e, then the F_V update of e - 1. B fragments are reloaded only when the patient changes.
+      if (e0 < e1) {
+        const uint32_t eA = lA + 32u;
+        uint32_t ent = (uint32_t)lds_s32(eA + 4u * e0);
+        uint32_t ent2 = (uint32_t)lds_s32(eA + 4u * min(e0 + 1, e1 - 1));
+        int pc = (int)(ent >> 16);
+        double bc[KS][NTW], ac[KS];
+        int rc;
+        {
+          const uint32_t ta = tA + TB * (ent & 0xffffu);
+          rc = lds_s32(ta + 4u * g);
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
+          for (int ks = 0; ks < KS; ++ks) ac[ks] = lds_f64_if(ta + aoff[ks], aok[ks]);
+          const uint32_t np = nA + 8u * (uint32_t)(pc * per);
 #pragma unroll
-          for (int nt = 0; nt < NTW; ++nt)
-            b[ks][nt] = lds_f64_if(np + 8u * (4 * ks * R + 8 * nt), (nok >> (ks * NTW + nt)) & 1u);
-      };
-      int nlo = 0, nhi = 0;
-      double nbfr[KS][NTW];
-      if (npat > 0) setup(0, nlo, nhi, nbfr);
-      for (int p = 0; p < npat; ++p) {
-        const int lo = nlo, hi = nhi;
-        double bfr[KS][NTW];
+          for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks)
+            for (int nt = 0; nt < NTW; ++nt)
+              bc[ks][nt] = lds_f64_if(np + 8u * (4 * ks * R + 8 * nt), (nok >> (ks * NTW + nt)) & 1u);
+        }
+        for (int e = e0; e < e1; ++e) {
+          // F_V rows of the pending tile
+          double2 v[NTW];
 #pragma unroll
-          for (int nt = 0; nt < NTW; ++nt) bfr[ks][nt] = nbfr[ks][nt];
-        if (p + 1 < npat) setup(p + 1, nlo, nhi, nbfr);
-#pragma unroll 2
-        for (int tt = lo; tt < hi; ++tt) {
-          const uint32_t ta = tA + TB * (uint32_t)tt;
-          const int rb = lds_s32(ta + 4u * g);  // the slot's F_V row byte offset
-          double av[KS];
+          for (int nt = 0; nt < NTW; ++nt) v[nt] = lds_v2_if(pA + 64u * nt, colok[nt]);
+          // next tile's operands (entry e + 1 = ent2) and the entry after it
+          double an[KS], bn[KS][NTW];
+          int rn = 0, pn = pc;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) av[ks] = lds_f64_if(ta + aoff[ks], aok[ks]);
+          for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+            for (int nt = 0; nt < NTW; ++nt) bn[ks][nt] = bc[ks][nt];
+          const bool more = e + 1 < e1;
+          {
+            const uint32_t ta = tA + TB * (ent2 & 0xffffu);
+            pn = more ? (int)(ent2 >> 16) : pc;
+            rn = lds_s32(ta + 4u * g);
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks) an[ks] = lds_f64_if(ta + aoff[ks], aok[ks] && more);
+            const uint32_t np = nA + 8u * (uint32_t)(pn * per);
+            const bool newp = pn != pc;
+#pragma unroll
+            for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+              for (int nt = 0; nt < NTW; ++nt)
+                lds_f64_keep(bn[ks][nt], np + 8u * (4 * ks * R + 8 * nt), newp && ((nok >> (ks * NTW + nt)) & 1u));
+            ent2 = (uint32_t)lds_s32(eA + 4u * min(e + 2, e1 - 1));
+          }
           double cc[NTW][2];
 #pragma unroll
           for (int nt = 0; nt < NTW; ++nt) cc[nt][0] = cc[nt][1] = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
-            for (int nt = 0; nt < NTW; ++nt) dmma(cc[nt][0], cc[nt][1], av[ks], bfr[ks][nt]);
-          commit();  // the previous tile
-          pA = fwA + (uint32_t)rb;
+            for (int nt = 0; nt < NTW; ++nt) dmma(cc[nt][0], cc[nt][1], ac[ks], bc[ks][nt]);
+#pragma unroll
+          for (int nt = 0; nt < NTW; ++nt) {
+            v[nt].x += pcc[nt][0];
+            v[nt].y += pcc[nt][1];
+            sts_v2_if(pA + 64u * nt, v[nt], colok[nt]);
+          }
+          pA = fwA + (uint32_t)rc;
 #pragma unroll
           for (int nt = 0; nt < NTW; ++nt) { pcc[nt][0] = cc[nt][0]; pcc[nt][1] = cc[nt][1]; }
+          rc = rn;
+          pc = pn;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            ac[ks] = an[ks];
+#pragma unroll
+            for (int nt = 0; nt < NTW; ++nt) bc[ks][nt] = bn[ks][nt];
+          }
         }
       }
       __syncwarp();
@@ -501,34 +538,37 @@ void launch_build_tiles(Handle& h) {
                                                                    h.fiber_val, h.tiles);
 }
 
-// Init: the pass-B stage table of tile bounds. CTA c = (range, group c % G) walks its stages;
-// entry (stage s, patient k in [k0, k1), sub-range w) = lo | hi << 16 with [lo, hi) the tiles of
-// sub-range (g, w) of patient k inside the stage's tile window [t0, t1), relative to t0.
+// Init: the pass-B stage lists. CTA c = (range, group c % G) walks its stages; stage s (tile window
+// [t0, t1), patients [k0, k1)) gets at st_list + st_t[s]: 8 offsets, then for w = 0..W-1 the tiles
+// of sub-range (g, w) of every patient inside the window, entry = (tile - t0) | (k - k0) << 16.
 __global__ void k_stage_tab(const int64_t* __restrict__ tptr, const uint16_t* __restrict__ twoff, int64_t K, int G,
                             int W, const int64_t* __restrict__ st_f, const int32_t* __restrict__ st_k,
                             const int32_t* __restrict__ st_t, const int32_t* __restrict__ cta_st,
-                            uint32_t* __restrict__ st_tab) {
+                            uint32_t* __restrict__ st_list) {
   const int c = blockIdx.x, grp = c % G;
   const int64_t* tp = tptr + (int64_t)grp * (K + 1);
   for (int s = cta_st[c] + threadIdx.x; s < cta_st[c + 1]; s += blockDim.x) {
     const int64_t t0 = st_f[2 * (int64_t)s], t1 = st_f[2 * (int64_t)s + 1];
     const int32_t k0 = st_k[2 * (int64_t)s], k1 = st_k[2 * (int64_t)s + 1];
-    uint32_t* out = st_tab + st_t[s];
-    for (int32_t k = k0; k < k1; ++k) {
-      const uint16_t* tw = twoff + ((int64_t)grp * K + k) * kWoS;
-      for (int w = 0; w < W; ++w) {
-        const int64_t lo = min(max(tp[k] + tw[w], t0), t1) - t0;
-        const int64_t hi = min(max(tp[k] + tw[w + 1], t0), t1) - t0;
-        out[(int64_t)(k - k0) * W + w] = (uint32_t)lo | ((uint32_t)hi << 16);
+    uint32_t* hdr = st_list + st_t[s];
+    uint32_t* ent = hdr + 8;
+    uint32_t n = 0;
+    for (int w = 0; w < W; ++w) {
+      hdr[w] = n;
+      for (int32_t k = k0; k < k1; ++k) {
+        const uint16_t* tw = twoff + ((int64_t)grp * K + k) * kWoS;
+        const int64_t lo = min(max(tp[k] + tw[w], t0), t1), hi = min(max(tp[k] + tw[w + 1], t0), t1);
+        for (int64_t x = lo; x < hi; ++x) ent[n++] = (uint32_t)(x - t0) | ((uint32_t)(k - k0) << 16);
       }
     }
+    for (int w = W; w < 8; ++w) hdr[w] = n;
   }
 }
 
 void launch_stage_tab(Handle& h) {
   if (!h.sc_ok || h.nst == 0) return;
   k_stage_tab<<<(unsigned)(h.sc_ranges * h.sc_G), 128, 0, h.stream>>>(h.tptr, h.twoff, h.K, h.sc_G, h.sc_W, h.st_f,
-                                                                      h.st_k, h.st_t, h.cta_st, h.st_tab);
+                                                                      h.st_k, h.st_t, h.cta_st, h.st_list);
 }
 
 // FV[inv[j']] = sum over ranges of part[range][j'] (fixed order), for every used label j'
@@ -549,7 +589,7 @@ static void scatter_inst_w(Handle& h) {
   constexpr auto fn = k_scatter_tma<KS, NT, W, LT, RT, CS>;
   max_smem_attr<fn>(h);
   const int ctas = h.sc_ranges * h.sc_G;
-  fn<<<ctas, 32 * (W * CS + 1), h.sc_smem, h.stream>>>(h.tiles, h.sc_G, h.sc_Jg, h.st_f, h.st_k, h.st_t, h.st_tab,
+  fn<<<ctas, 32 * (W * CS + 1), h.sc_smem, h.stream>>>(h.tiles, h.sc_G, h.sc_Jg, h.st_f, h.st_k, h.st_t, h.st_list,
                                                         h.cta_st, h.l, h.R, h.sc_RS, h.sc_FB, h.sc_PB, h.sc_NS, h.Nst,
                                                         h.fv_part);
   int64_t n = h.Jl * h.R;
@@ -665,9 +705,8 @@ int64_t tiles_cap(const Handle& h) {
   return h.F / 8 + runs + 8;
 }
 
-// stage-table entries: every stage holds its patients' sub-range bounds; a patient's run is split
-// over at most (run / FT + 2) stages, so sum over stages of (k1 - k0) <= G K + nst
-int64_t stage_tab_cap(const Handle& h) { return ((int64_t)h.sc_G * h.K + stage_cap(h)) * h.sc_W + 16; }
+// stage-list words: 8 per stage plus one per tile
+int64_t stage_tab_cap(const Handle& h) { return 8 * stage_cap(h) + tiles_cap(h) + 16; }
 
 int64_t stage_cap(const Handle& h) {
   return tiles_cap(h) / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
@@ -739,12 +778,12 @@ void plan_streams(Handle& h, const int32_t* tcnt, int64_t* tptr, std::vector<int
       }
     }
   cta_st[(size_t)nr * G] = (int32_t)(st_k.size() / 2);
-  // offsets of every stage's (patient, sub-range) entries in the stage table st_tab
+  // offsets of every stage's list in st_list (8 header words + one per tile)
   const size_t nst = st_k.size() / 2;
   st_t.assign(nst + 1, 0);
-  int64_t acc = 0;  // (the caller rejects tables beyond int32)
+  int64_t acc = 0;  // (the caller rejects lists beyond int32)
   for (size_t x = 0; x < nst; ++x) {
-    acc += (int64_t)(st_k[2 * x + 1] - st_k[2 * x]) * h.sc_W;
+    acc += 8 + (st_f[2 * x + 1] - st_f[2 * x]);
     st_t[x + 1] = (int32_t)std::min<int64_t>(acc, INT32_MAX);
   }
 }
