@@ -446,82 +446,117 @@ __global__ void k_tile_counts(const uint16_t* __restrict__ woff, int64_t K, int 
   tcnt[x] = acc;
 }
 
-// Thread per (group, patient, sub-range): the sub-run's n fibers (g-stream, sorted by label) go to
-// 8 ceil(n / 8) slots paired as described above. Pairs, in order: (class c rank i, class c + D rank
-// i) for every c < D; each class's surplus with a pad; the remaining surplus fibers with each other
-// (consecutive, possibly a same-half pair); pads with pads. Slot = 2 pair + side.
+// Warp per (group, patient) run, its W sub-runs one after the other: a sub-run's n fibers (g-stream,
+// sorted by label) go to 8 ceil(n / 8) slots paired as described above. Pairs, in order: (class c
+// rank i, class c + D rank i) for every c < D; each class's surplus with a pad; the remaining surplus
+// fibers with each other (consecutive, possibly a same-half pair); pads with pads. Slot = 2 pair +
+// side. Class ranks come from per-class warp ballots, 32 fibers at a time; the lanes then write
+// their fibers (and the pads) in parallel.
 __global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* __restrict__ woff,
                               const int64_t* __restrict__ tptr, const uint16_t* __restrict__ twoff, int64_t K, int G,
                               int W, int64_t Jg, int RS, int l, const int32_t* __restrict__ fiber_col,
                               const double* __restrict__ fiber_val, unsigned char* __restrict__ tiles) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= (int64_t)G * K * W) return;
-  const int w = (int)(x % W);
-  const int64_t gk = x / W;
+  const int lane = threadIdx.x & 31;
+  const int64_t gk = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (gk >= (int64_t)G * K) return;
   const int g = (int)(gk / K);
   const int64_t k = gk - (int64_t)g * K;
   const uint16_t* wo = woff + gk * kWoS;
-  const int64_t f0 = gptr[(int64_t)g * (K + 1) + k] + wo[w];
-  const int n = wo[w + 1] - wo[w];
-  if (n == 0) return;
-  const int T = (n + 7) >> 3, P = 8 * T - n;
   const uint32_t TB = tile_bytes(l);
-  unsigned char* tb = tiles + (size_t)TB * (size_t)(tptr[(int64_t)g * (K + 1) + k] + twoff[gk * kWoS + w]);
   int M, D;
   pair_rule(RS, &M, &D);
   const int64_t lab0 = (int64_t)g * Jg;
-  int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) ++cnt[(int)((fiber_col[f0 + i] - lab0) & (M - 1))];
-  // pair bookkeeping per class pair c < D
-  int m[4], q[4], rem[4], base1[4], base2[4], off3[4], X[4];
-  int pair = 0, padsLeft = P;
-  for (int c = 0; c < D; ++c) {
-    m[c] = min(cnt[c], cnt[c + D]);
-    base1[c] = pair;
-    pair += m[c];
-    X[c] = cnt[c] >= cnt[c + D] ? c : c + D;
-  }
-  for (int c = 0; c < D; ++c) {
-    const int sur = abs(cnt[c] - cnt[c + D]);
-    q[c] = min(sur, padsLeft);
-    padsLeft -= q[c];
-    base2[c] = pair;
-    pair += q[c];
-    rem[c] = sur - q[c];
-  }
-  int tot3 = 0;
-  for (int c = 0; c < D; ++c) { off3[c] = tot3; tot3 += rem[c]; }
-  const int base3 = pair;  // phase-3 pairs: base3 .. base3 + ceil(tot3 / 2)
-  auto put = [&](int slot, int64_t rowlab, const double* v) {
-    unsigned char* tp = tb + (size_t)TB * (slot >> 3);
-    const int pos = slot & 7;
-    reinterpret_cast<int32_t*>(tp)[pos] = (int32_t)(rowlab * RS * 8);
-    for (int a = 0; a < l; ++a) *reinterpret_cast<double*>(tp + tile_val_off(l, a, pos)) = v ? v[a] : 0.0;
-  };
-  int seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int i = 0; i < n; ++i) {
-    const int64_t lab = fiber_col[f0 + i] - lab0;
-    const int c = (int)(lab & (M - 1)), cp = c % D;
-    const int r = seen[c]++;
-    int slot;
-    if (r < m[cp]) {
-      slot = 2 * (base1[cp] + r) + (c >= D ? 1 : 0);
-    } else {
-      const int j = r - m[cp];  // surplus rank (c == X[cp])
-      if (j < q[cp]) slot = 2 * (base2[cp] + j);
-      else {
-        const int s = off3[cp] + (j - q[cp]);
-        slot = 2 * base3 + s;  // consecutive slots: pairs (s even, s odd)
+  const unsigned lt = (1u << lane) - 1u;
+  auto scr = [&](int cls) -> int64_t { return Jg + (((int64_t)cls - Jg) & (M - 1)); };
+  for (int w = 0; w < W; ++w) {
+    const int64_t f0 = gptr[(int64_t)g * (K + 1) + k] + wo[w];
+    const int n = wo[w + 1] - wo[w];
+    if (n == 0) continue;
+    const int T = (n + 7) >> 3, P = 8 * T - n;
+    unsigned char* tb = tiles + (size_t)TB * (size_t)(tptr[(int64_t)g * (K + 1) + k] + twoff[gk * kWoS + w]);
+    auto put = [&](int slot, int64_t rowlab, const double* v) {
+      unsigned char* tp = tb + (size_t)TB * (slot >> 3);
+      const int pos = slot & 7;
+      reinterpret_cast<int32_t*>(tp)[pos] = (int32_t)(rowlab * RS * 8);
+      for (int a = 0; a < l; ++a) *reinterpret_cast<double*>(tp + tile_val_off(l, a, pos)) = v ? v[a] : 0.0;
+    };
+    int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const bool ok = i0 + lane < n;
+      const int c = ok ? (int)((fiber_col[f0 + i0 + lane] - lab0) & (M - 1)) : -1;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) cnt[cc] += __popc(__ballot_sync(0xffffffffu, c == cc));
+    }
+    // pair bookkeeping per class pair c < D (warp-uniform)
+    int m[4], q[4], base1[4], base2[4], off3[4], X[4];
+    int pair = 0, padsLeft = P, tot3 = 0, nq = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < D) {
+        m[c] = min(cnt[c], cnt[c + D]);
+        base1[c] = pair;
+        pair += m[c];
+        X[c] = cnt[c] >= cnt[c + D] ? c : c + D;
+      }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (c < D) {
+        const int sur = abs(cnt[c] - cnt[c + D]);
+        q[c] = min(sur, padsLeft);
+        padsLeft -= q[c];
+        base2[c] = pair;
+        pair += q[c];
+        off3[c] = tot3;
+        tot3 += sur - q[c];
+        nq += q[c];
+      }
+    const int base3 = pair;  // phase-3 pairs: base3 .. base3 + ceil(tot3 / 2)
+    int seen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i0 = 0; i0 < n; i0 += 32) {
+      const bool ok = i0 + lane < n;
+      const int64_t lab = ok ? fiber_col[f0 + i0 + lane] - lab0 : 0;
+      const int c = ok ? (int)(lab & (M - 1)) : -1;
+      int r = 0;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const unsigned b = __ballot_sync(0xffffffffu, c == cc);
+        if (c == cc) r = seen[cc] + __popc(b & lt);
+        seen[cc] += __popc(b);
+      }
+      if (ok) {
+        const int cp = c % D;
+        int mm = 0, qq = 0, b1 = 0, b2 = 0, o3 = 0;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          if (x == cp) { mm = m[x]; qq = q[x]; b1 = base1[x]; b2 = base2[x]; o3 = off3[x]; }
+        int slot;
+        if (r < mm) {
+          slot = 2 * (b1 + r) + (c >= D ? 1 : 0);
+        } else {
+          const int j = r - mm;  // surplus rank (c == X[cp])
+          slot = j < qq ? 2 * (b2 + j) : 2 * base3 + o3 + (j - qq);  // phase 3: consecutive slots
+        }
+        put(slot, lab, fiber_val + (f0 + i0 + lane) * l);
       }
     }
-    put(slot, lab, fiber_val + (f0 + i) * l);
+    // pads: partners of the phase-2 surplus (nq), then the odd phase-3 tail and pad pairs
+    const int npads = nq + (8 * T - 2 * base3 - tot3);
+    for (int j = lane; j < npads; j += 32) {
+      if (j < nq) {
+        int jj = j, slot = 0, cls = 0;
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          if (x < D) {
+            if (jj >= 0 && jj < q[x]) { slot = 2 * (base2[x] + jj) + 1; cls = (X[x] + D) & (M - 1); }
+            jj -= q[x];
+          }
+        put(slot, scr(cls), nullptr);
+      } else {
+        const int s = 2 * base3 + tot3 + (j - nq);
+        put(s, scr((s & 1) ? D : 0), nullptr);
+      }
+    }
   }
-  // pads: partners of the phase-2 surplus, the odd phase-3 tail, then pad pairs
-  auto scr = [&](int cls) -> int64_t { return Jg + (((int64_t)cls - Jg) & (M - 1)); };
-  for (int c = 0; c < D; ++c)
-    for (int j = 0; j < q[c]; ++j) put(2 * (base2[c] + j) + 1, scr((X[c] + D) & (M - 1)), nullptr);
-  int s = 2 * base3 + tot3;
-  for (; s < 8 * T; ++s) put(s, scr((s & 1) ? D : 0), nullptr);
 }
 
 void launch_tile_counts(Handle& h, int32_t* tcnt) {
@@ -532,8 +567,8 @@ void launch_tile_counts(Handle& h, int32_t* tcnt) {
 
 void launch_build_tiles(Handle& h) {
   if (!h.sc_ok || h.K == 0) return;
-  const int64_t n = (int64_t)h.sc_G * h.K * h.sc_W;
-  k_build_tiles<<<(unsigned)((n + 127) / 128), 128, 0, h.stream>>>(h.gptr, h.woff, h.tptr, h.twoff, h.K, h.sc_G,
+  const int64_t n = (int64_t)h.sc_G * h.K;  // warps
+  k_build_tiles<<<(unsigned)((n + 7) / 8), 256, 0, h.stream>>>(h.gptr, h.woff, h.tptr, h.twoff, h.K, h.sc_G,
                                                                    h.sc_W, h.sc_Jg, h.sc_RS, h.l, h.fiber_col,
                                                                    h.fiber_val, h.tiles);
 }
