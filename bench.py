@@ -147,6 +147,12 @@ def phase_model(st: dict, cfg, R: int, K: int, J: int, rows: int, nnz: int, m: n
         "fit": {"bytes": 3 * JR8, "layout_bytes": 3 * JR8, "flops": 0.0, "bound": "hbm"},
         "admm_H": {"bytes": 0.0, "layout_bytes": 0.0, "flops": 0.0, "bound": "hbm"},
     }
+    # DMMA instructions the fiber passes issue (m8n8k4: 512 flops each, padding included): pass A one
+    # k-step per 4 fibers per (M tile, N tile); pass B KS k-steps per 8-slot tile per N tile
+    if l > 0:
+        nt, mt, ks = (R + 7) // 8, (l + 7) // 8, (l + 3) // 4
+        model["spmm"]["dmma"] = float(F) / 4.0 * mt * nt
+        model["scatter"]["dmma"] = float(st.get("tiles", 0)) * ks * nt
     b_iter = 2 * BX + 4 * U + 2 * C + 5 * KR8
     return model, b_iter
 
@@ -336,6 +342,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                 roof["fp64_tensor"] = {"achieved": tf, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                                        "frac": tf / DMMA_PEAK_TFLOPS,
                                        "flops": "SURVEY 8(d): 2 nnz R + 2 R sum I_k l'_k per pass"}
+                if mdl.get("dmma"):  # what the tensor pipe actually issues (padded tiles), vs its peak
+                    ex = mdl["dmma"] * 512.0 / (ms_launch / 1e3) / 1e12
+                    roof["fp64_tensor"].update({"executed_dmma": mdl["dmma"], "executed": ex,
+                                                "executed_frac": ex / DMMA_PEAK_TFLOPS})
     phase_report = {k: {"ms_per_launch": per_launch[k][0], "share": per_launch[k][0] / ms_per_step,
                         "alg_GBps": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9) if k in model else None,
                         "alg_frac": (model[k]["bytes"] / (per_launch[k][0] / 1e3) / 1e9 / hbm_peak) if k in model

@@ -128,6 +128,7 @@ typedef struct {
   double polar_min_kept, polar_max_dropped;
   int64_t basis_near;
   double basis_min_kept, basis_max_dropped;
+  int64_t tiles;        /* 8-slot tiles of pass B's tiled stream (smooth path, shard; 0 otherwise) */
 } copa_stats;
 
 /* Kernel limits of this build: R <= max_R, q = min(m_k, R) <= max_q (warp polar), smooth_l <= max_smooth_l. */

@@ -55,7 +55,7 @@ class _Stats(ctypes.Structure):
                 ("inner_steps", ctypes.c_int64 * 3), ("polar_near", ctypes.c_int64),
                 ("polar_min_kept", ctypes.c_double), ("polar_max_dropped", ctypes.c_double),
                 ("basis_near", ctypes.c_int64), ("basis_min_kept", ctypes.c_double),
-                ("basis_max_dropped", ctypes.c_double)]
+                ("basis_max_dropped", ctypes.c_double), ("tiles", ctypes.c_int64)]
 
 
 class _State(ctypes.Structure):
@@ -318,7 +318,7 @@ class Copa:
     def stats(self) -> dict:
         s = _Stats()
         _check(lib().copa_get_stats(self.h, ctypes.byref(s)))
-        return {"fit": s.fit, "rho": list(s.rho), "normX": s.normX, "iterations": s.iterations, "fibers": s.fibers,
+        return {"fit": s.fit, "rho": list(s.rho), "normX": s.normX, "iterations": s.iterations, "fibers": s.fibers, "tiles": s.tiles,
                 "state_rows": s.state_rows, "rank_deficient": s.rank_deficient, "sparsity_V": s.sparsity_V,
                 "inner_steps": list(s.inner_steps), "polar_near": s.polar_near, "polar_min_kept": s.polar_min_kept,
                 "polar_max_dropped": s.polar_max_dropped, "basis_near": s.basis_near,

@@ -386,6 +386,7 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       }
       CUDA_TRY(cudaMemcpyAsync(h.gptr, gptr.data(), sizeof(int64_t) * gptr.size(), cudaMemcpyHostToDevice, s), "gptr");
       CUDA_TRY(cudaMemcpyAsync(h.tptr, tptr.data(), sizeof(int64_t) * tptr.size(), cudaMemcpyHostToDevice, s), "tptr");
+      h.ntiles = tptr.back();
       if (h.nst > 0) {
         CUDA_TRY(cudaMemcpyAsync(h.st_f, st_f.data(), sizeof(int64_t) * st_f.size(), cudaMemcpyHostToDevice, s), "st_f");
         CUDA_TRY(cudaMemcpyAsync(h.st_k, st_k.data(), sizeof(int32_t) * st_k.size(), cudaMemcpyHostToDevice, s), "st_k");
@@ -741,6 +742,7 @@ copa_status copa_get_stats(copa_handle* H, copa_stats* out) {
   out->normX = sc[S_NORMX];
   out->iterations = h.iterations;
   out->fibers = h.F;
+  out->tiles = h.ntiles;
   out->state_rows = h.S;
   out->rank_deficient = (int64_t)rd;
   unsigned long long dg[kDiagSlots], stp[4];

@@ -91,7 +91,7 @@ struct Handle {
   unsigned char* tiles;  // pass-B tiled stream (k_fibers.cu): per group, patient, sub-range: 8-slot tiles
   int64_t* tptr;         // [G x (K + 1)] first tile of each (group, patient) run
   uint16_t* twoff;       // [G x K x kWoS] tile offset of each sub-range inside its run
-  int64_t nst = 0, nst_cap = 0;
+  int64_t nst = 0, nst_cap = 0, ntiles = 0;
   int64_t Jl = 0;        // labels = G * Jg >= J
   int sc_G = 1, sc_W = 4, sc_RS = 0, sc_ok = 0, sc_ranges = 1;
   int sc_FB = 32, sc_PB = 16, sc_NS = 3;  // pass-B stage: tiles (FB), patients (PB), ring slots (NS)
