@@ -193,7 +193,10 @@ copa_status copa_get_stats(copa_handle* h, copa_stats* out);
 
 /* init + iterate(n_outer) + get_factors + destroy with HOST inputs (the end-to-end call):
  * problem pointers are HOST pointers here; the library copies them into the workspace
- * (so workspace must be >= copa_fit_workspace_size). Outputs are HOST pointers (or NULL). */
+ * (so workspace must be >= copa_fit_workspace_size). Outputs are HOST pointers (or NULL).
+ * copa_fit_workspace_size reads the host patient_row_ptr, row_ptr and col arrays (it counts the
+ * distinct (patient, feature) pairs the smooth path stores, with host threads); val, visit_time and
+ * the option arrays are not read. */
 copa_status copa_fit_workspace_size(const copa_problem* host_problem, const copa_options* host_options,
                                     size_t* bytes);
 copa_status copa_fit(const copa_problem* host_problem, const copa_options* host_options, void* workspace,

@@ -408,8 +408,10 @@ def fit_workspace_bytes(prob, options: Options, R: Optional[int] = None) -> int:
     R = int(R or prob.R)
     prp = np.ascontiguousarray(prob.patient_row_ptr, np.int64)
     rp = np.ascontiguousarray(prob.row_ptr, np.int64)
+    col = np.ascontiguousarray(prob.col, np.int32)  # read: the fibers are counted from the host CSR
     p = _Problem(K_local=len(prp) - 1, K_global=len(prp) - 1, J=int(prob.J), R=R, rows=len(rp) - 1,
-                 nnz=len(prob.col), patient_row_ptr=prp.ctypes.data, row_ptr=rp.ctypes.data, col=1, val=1,
+                 nnz=len(prob.col), patient_row_ptr=prp.ctypes.data, row_ptr=rp.ctypes.data, col=col.ctypes.data,
+                 val=1,
                  visit_time=1 if options.smooth_l > 0 else None)
     o = options.c_struct(1, 1, 1, ALLREDUCE_FN(), None)
     nbytes = ctypes.c_size_t(0)

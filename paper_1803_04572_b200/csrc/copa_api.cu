@@ -10,6 +10,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "copa_internal.cuh"
@@ -92,8 +93,15 @@ size_t carve(Handle& h, char* base) {
     h.Bk = c.take<double>(h.K * h.l * h.l);
     h.fiber_ptr = c.take<int64_t>(h.K + 1);
     h.gptr = c.take<int64_t>((int64_t)G * (h.K + 1) + 2);  // +2: bulk copies round up to 16 bytes
-    h.fiber_col = c.take<int32_t>(h.Fcap);
-    h.fiber_val = c.take<double>(h.Fcap * h.l);
+    {  // the tiled stream's buffer first holds the g-streams (init only: layout A is built from
+       // them, the tiles from layout A; without a shared-memory F_V slice the g-streams stay)
+      const size_t gcol = align_up(sizeof(int32_t) * (size_t)h.Fcap);
+      const size_t gsz = gcol + sizeof(double) * (size_t)(h.Fcap * h.l);
+      const size_t tsz = (size_t)tiles_cap(h) * tile_bytes_host(h.l) + 64;
+      h.tiles = c.take<unsigned char>((int64_t)(gsz > tsz ? gsz : tsz));
+      h.fiber_col = reinterpret_cast<int32_t*>(h.tiles);
+      h.fiber_val = h.tiles ? reinterpret_cast<double*>(h.tiles + gcol) : nullptr;
+    }
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
     h.perm = c.take<int32_t>(h.J);
     h.inv = c.take<int32_t>(h.Jl);
@@ -107,7 +115,6 @@ size_t carve(Handle& h, char* base) {
     h.woff = c.take<uint16_t>((int64_t)G * h.K * kWoS + 16);
     h.twoff = c.take<uint16_t>((int64_t)G * h.K * kWoS + 16);
     h.tptr = c.take<int64_t>((int64_t)G * (h.K + 1) + 2);
-    h.tiles = c.take<unsigned char>(tiles_cap(h) * (int64_t)tile_bytes_host(h.l) + 64);
     h.nst_cap = stage_cap(h);
     h.st_f = c.take<int64_t>(2 * h.nst_cap);
     h.st_k = c.take<int32_t>(2 * h.nst_cap);
@@ -831,13 +838,39 @@ copa_status copa_fit_workspace_size(const copa_problem* p, const copa_options* o
   if (!bytes) return fail(COPA_E_ARG, "null bytes");
   Handle h{};
   fill_sizes(h, p, o);
-  // upper bound on fibers from the host CSR: sum_k min(J, nnz_k)
+  // fibers = distinct (patient, feature) pairs, counted from the host CSR (the workspace grows
+  // ~150 bytes per fiber, so the sum_k min(J, nnz_k) bound overshoots a B200 at Scale); host threads
+  // over patient chunks, a feature bitmap each. Out-of-range columns are left to init's validation
+  // and counted as distinct.
   int64_t F = 0;
   if (h.fib) {
-    for (int64_t k = 0; k < p->K_local; ++k) {
-      int64_t nk = p->row_ptr[p->patient_row_ptr[k + 1]] - p->row_ptr[p->patient_row_ptr[k]];
-      F += nk < p->J ? nk : p->J;
-    }
+    const int64_t K = p->K_local;
+    const unsigned nth = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<int64_t> part(nth, 0);
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nth; ++t)
+      pool.emplace_back([&, t]() {
+        std::vector<uint64_t> bits((size_t)((p->J + 63) / 64), 0);
+        int64_t cnt = 0;
+        for (int64_t k = K * t / nth; k < K * (t + 1) / nth; ++k) {
+          const int64_t a = p->row_ptr[p->patient_row_ptr[k]], b = p->row_ptr[p->patient_row_ptr[k + 1]];
+          for (int64_t x = a; x < b; ++x) {
+            const int32_t j = p->col[x];
+            if (j < 0 || j >= p->J) { ++cnt; continue; }
+            uint64_t& wd = bits[(size_t)j >> 6];
+            const uint64_t m = 1ull << (j & 63);
+            cnt += (wd & m) ? 0 : 1;
+            wd |= m;
+          }
+          for (int64_t x = a; x < b; ++x) {
+            const int32_t j = p->col[x];
+            if (j >= 0 && j < p->J) bits[(size_t)j >> 6] = 0;
+          }
+        }
+        part[t] = cnt;
+      });
+    for (auto& th : pool) th.join();
+    for (auto v : part) F += v;
     cub::DeviceScan::InclusiveSum(nullptr, h.cub_temp_bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)(h.K + 1));
   }
   h.F = F;

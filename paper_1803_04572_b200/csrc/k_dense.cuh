@@ -319,7 +319,7 @@ __device__ __forceinline__ void a_slab(int nt, int64_t base, int64_t K, int l, i
 }
 
 template <int L, int MT, int NT, int RT, int LT>
-__global__ void __launch_bounds__(128, 3) k_polar_wide(const int32_t* __restrict__ m, int64_t K, int R_, int l_,
+__global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32_t* __restrict__ m, int64_t K, int R_, int l_,
                                                        const double* __restrict__ Pp, const double* __restrict__ W,
                                                        const double* __restrict__ Hg, double tau,
                                                        double* __restrict__ Qt, int32_t* __restrict__ rank,

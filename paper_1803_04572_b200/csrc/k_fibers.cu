@@ -454,8 +454,9 @@ __global__ void k_tile_counts(const uint16_t* __restrict__ woff, int64_t K, int 
 // their fibers (and the pads) in parallel.
 __global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* __restrict__ woff,
                               const int64_t* __restrict__ tptr, const uint16_t* __restrict__ twoff, int64_t K, int G,
-                              int W, int64_t Jg, int RS, int l, const int32_t* __restrict__ fiber_col,
-                              const double* __restrict__ fiber_val, unsigned char* __restrict__ tiles) {
+                              int W, int64_t Jg, int RS, int l, const int64_t* __restrict__ fp,
+                              const int32_t* __restrict__ fiber_col, const double* __restrict__ fiber_val,
+                              unsigned char* __restrict__ tiles) {
   const int lane = threadIdx.x & 31;
   const int64_t gk = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (gk >= (int64_t)G * K) return;
@@ -468,8 +469,12 @@ __global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* 
   const int64_t lab0 = (int64_t)g * Jg;
   const unsigned lt = (1u << lane) - 1u;
   auto scr = [&](int cls) -> int64_t { return Jg + (((int64_t)cls - Jg) & (M - 1)); };
+  // the run (g, k) inside layout A (patient k's G runs concatenated at fp[k]); the tiles overwrite
+  // the g-streams, so they are read from layout A
+  int64_t run0 = fp[k];
+  for (int gg = 0; gg < g; ++gg) run0 += gptr[(int64_t)gg * (K + 1) + k + 1] - gptr[(int64_t)gg * (K + 1) + k];
   for (int w = 0; w < W; ++w) {
-    const int64_t f0 = gptr[(int64_t)g * (K + 1) + k] + wo[w];
+    const int64_t f0 = run0 + wo[w];
     const int n = wo[w + 1] - wo[w];
     if (n == 0) continue;
     const int T = (n + 7) >> 3, P = 8 * T - n;
@@ -569,8 +574,8 @@ void launch_build_tiles(Handle& h) {
   if (!h.sc_ok || h.K == 0) return;
   const int64_t n = (int64_t)h.sc_G * h.K;  // warps
   k_build_tiles<<<(unsigned)((n + 7) / 8), 256, 0, h.stream>>>(h.gptr, h.woff, h.tptr, h.twoff, h.K, h.sc_G,
-                                                                   h.sc_W, h.sc_Jg, h.sc_RS, h.l, h.fiber_col,
-                                                                   h.fiber_val, h.tiles);
+                                                                   h.sc_W, h.sc_Jg, h.sc_RS, h.l, h.fiber_ptr,
+                                                                   h.fa_col, h.fa_val, h.tiles);
 }
 
 // Init: the pass-B stage lists. CTA c = (range, group c % G) walks its stages; stage s (tile window
