@@ -379,10 +379,11 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
     for (int i = 0; i < L; ++i)
 #pragma unroll
       for (int j = 0; j < L; ++j) Rf[i][j] = 0.0;
+#pragma unroll 1
     for (int nt = 0; nt < NT; ++nt) {
       a_slab<MT, KS, BULK, SR, FAST>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
-#pragma unroll
+#pragma unroll 1
       for (int cc = 0; cc < 8; ++cc) {
         if (8 * nt + cc < R) {
           double col[L];
@@ -423,12 +424,13 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
     if (kme < K) rank[kme] = mme > 0 ? rk : 0;
     ratio_diag_warp(diag, D_POLAR_NEAR, dg);
     // ---- Q~ = K A, slab by slab (A recomputed on the tensor cores)
+#pragma unroll 1
     for (int nt = 0; nt < NT; ++nt) {
       a_slab<MT, KS, BULK, SR, FAST>(nt, base, K, l, R, Pp, W, Hs, slab, ringbuf, bars, q0);
       __syncwarp();
       if (kme < K && mme > 0) {
         double* Q = Qt + kme * pstride;
-#pragma unroll
+#pragma unroll 1
         for (int cc = 0; cc < 8; ++cc) {
           const int s = 8 * nt + cc;
           if (s < R) {
