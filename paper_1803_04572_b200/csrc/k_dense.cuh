@@ -145,6 +145,8 @@ __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %
 
 constexpr int kRing = 4;  // patients staged ahead (per warp) by the cp.async rings of the wide kernels
 constexpr int kRingA = 3; // ... by the polar A-slab ring (smaller, for 3 polar CTAs per SM)
+// F_H ring depth of the wide polar: 3 for l > 8, so that the ring fits in the A slab it reuses
+__host__ __device__ constexpr int polar_fh_ring(int L) { return L > 8 ? 3 : kRing; }
 constexpr bool kSplitK = false;  // even/odd k-step accumulators in the A slabs (changes rounding order)
 
 __device__ __forceinline__ uint32_t su32d(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -338,17 +340,18 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
   const int wib = threadIdx.x >> 5;
   constexpr bool BULK = RT > 0 && (RT % 2) == 0;     // 16-byte aligned records: TMA bulk copies
   constexpr int SR = LT ? LT : MT * 8;                 // A rows kept per patient in the slab
+  constexpr int NRF = polar_fh_ring(L);  // F_H ring depth
   // per warp: a-slab ring + 2 barrier sets, kept a multiple of 2 doubles (16-byte bulk-copy alignment)
-  const int ringd = kRingA * (l * R + R) + ((kRingA + kRing + 1) & ~1);
-  // per warp: slab of 32 patients x SR x 8, reused as the F_H ring (kRing x (2 l R + R))
-  const int slabd = 32 * SR * 8 > kRing * (2 * l * R + R) ? 32 * SR * 8 : kRing * (2 * l * R + R);
+  const int ringd = kRingA * (l * R + R) + ((kRingA + NRF + 1) & ~1);
+  // per warp: slab of 32 patients x SR x 8, reused as the F_H ring (NRF x (2 l R + R))
+  const int slabd = 32 * SR * 8 > NRF * (2 * l * R + R) ? 32 * SR * 8 : NRF * (2 * l * R + R);
   double* slab = sm + hoff + wib * (slabd + ringd);
   double* ringbuf = slab + slabd;
   uint64_t* bars = (uint64_t*)(ringbuf + kRingA * (l * R + R));  // kRingA (a-slab ring)
-  uint64_t* barsf = bars + kRingA;                                 // kRing (F_H ring)
+  uint64_t* barsf = bars + kRingA;                                 // NRF (F_H ring)
   if (BULK) {
     ring_bars_init(bars, kRingA);
-    ring_bars_init(barsf, kRing);
+    ring_bars_init(barsf, NRF);
   }
   int q0 = 0, qf = 0;  // records pulled through each ring (mbarrier phase continuity)
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) Hs[x] = Hg[x];
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
         for (int b = 0; b < NT; ++b) fh[a][b][0] = fh[a][b][1] = 0.0;
       const int np = (int)(K - base < 32 ? K - base : 32);
       const int lR = l * R;
-      WarpRing<3, BULK> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R), staged in the (free) slab
+      WarpRing<3, BULK, NRF> ring;  // record: Q~_p (l R), P'_p (l R), w̄_p (R), staged in the (free) slab
       ring.buf = slab;
       ring.bar = barsf;
       ring.q0 = qf;
@@ -495,7 +498,7 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
       ring.stride[2] = R;
       ring.len[2] = R;
 #pragma unroll
-      for (int p = 0; p < kRing; ++p) ring.issue(p, np);
+      for (int p = 0; p < NRF; ++p) ring.issue(p, np);
       for (int p = 0; p < np; ++p) {
         ring.wait(p);
         const double* rec = ring.slot(p);
@@ -517,7 +520,7 @@ __global__ void __launch_bounds__(128, (L > 8 ? 1 : 3)) k_polar_wide(const int32
 #pragma unroll
             for (int j = 0; j < NT; ++j) dmma2(fh[i][j][0], fh[i][j][1], af[ks][i], bf[ks][j]);
         __syncwarp();
-        ring.issue(p + kRing, np);
+        ring.issue(p + NRF, np);
       }
       ring.drain();
       qf += np;
@@ -574,17 +577,24 @@ static void polar_wide_inst(Handle& h) {
   constexpr auto fn = k_polar_wide<L, MT, NT, RT, LT>;
   const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
   constexpr int SR = LT ? LT : MT * 8;
-  const size_t slabd = (size_t)std::max(32 * SR * 8, kRing * (2 * h.l * h.R + h.R));
-  const size_t per_warp = slabd + (size_t)(kRingA * (h.l * h.R + h.R) + ((kRingA + kRing + 1) & ~1));
-  int wpb = kDenseThreads / 32;  // warps per block: fewer when the per-warp slab + ring is large
-  while (wpb > 1 && sizeof(double) * (hoff + wpb * per_warp) > 227 * 1024) wpb /= 2;
+  constexpr int NRF = polar_fh_ring(L);
+  const size_t slabd = (size_t)std::max(32 * SR * 8, NRF * (2 * h.l * h.R + h.R));
+  const size_t per_warp = slabd + (size_t)(kRingA * (h.l * h.R + h.R) + ((kRingA + NRF + 1) & ~1));
+  max_smem_attr<fn>(h);
+  // warps per block (4, 2 or 1): the one with the most resident warps per SM (the R x R H̄ copy is
+  // per block, so large per-warp slabs can favour smaller blocks)
+  int wpb = 1, per_sm = 1, best = -1;
+  for (int cand = kDenseThreads / 32; cand >= 1; cand /= 2) {
+    const size_t sm_c = sizeof(double) * (hoff + cand * per_warp);
+    if (sm_c > 227 * 1024) continue;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * cand, sm_c);
+    if (occ * cand > best) { best = occ * cand; wpb = cand; per_sm = occ; }
+  }
   const int threads = 32 * wpb;
   size_t smem = sizeof(double) * (hoff + wpb * per_warp);
-  max_smem_attr<fn>(h);
   int64_t rounds = (h.K + 31) / 32;
   int64_t blocks = (rounds + wpb - 1) / wpb;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   int64_t cap = h.sms * (int64_t)(per_sm > 0 ? per_sm : 1);
   if (cap > kPartBlocks * 4 / wpb) cap = kPartBlocks * 4 / wpb;  // fh_warp holds kPartBlocks x 4 warps
   if (blocks > cap) blocks = cap;
