@@ -671,17 +671,27 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
   const int l = LT ? LT : l_;
   extern __shared__ double sm[];
   const int hoff = ((R * R + 31) / 32) * 32;
-  double* Hs = sm;                 // R x R
-  double* Gs = sm + hoff;          // R x R  (G_W + rho I)^-1
   constexpr int KA = 2 * NT;       // k-steps of the batched W-row solves (K = columns, permuted, see below)
-  double* gfr = sm + 2 * hoff;     // (G_W + rho I)^-1 as MMA B fragments [KA][NT][lane]
+  // Shared memory (passB_wide_smem): H̄ [R x R] | (G_W + rho I)^-1 as MMA B fragments [KA][NT][lane] |
+  // with the per-row stop only: (G_W + rho I)^-1 [R x R] | per warp: F_W and w̄ as [r][lane] (+ d as
+  // [r][lane] and a separate N scratch with the per-row stop; otherwise the N scratch reuses the F_W
+  // rows, dead after the solves, and d stays in registers).
+  const bool tolpath = tol > 0.0;
+  double* Hs = sm;
+  double* gfr = sm + hoff;
+  double* Gs = tolpath ? gfr + KA * NT * 32 : nullptr;
+  const int fwd = RP * 32 > MT * 8 * RP ? RP * 32 : MT * 8 * RP;
+  const int per_warp = tolpath ? 3 * RP * 32 + MT * 8 * RP : fwd + RP * 32;
   const int wib = threadIdx.x >> 5;
-  double* wv = sm + 2 * hoff + KA * NT * 32 + wib * (3 * RP * 32 + MT * 8 * RP);  // per warp: fw, w̄, d as [r][lane] + N scratch
+  double* wv = sm + hoff + KA * NT * 32 + (tolpath ? hoff : 0) + wib * per_warp;
   double* fwv = wv;
-  double* wbv = wv + RP * 32;
-  double* dv = wv + 2 * RP * 32;
-  double* ns = wv + 3 * RP * 32;   // N_p (MT 8 x RP)
-  for (int x = threadIdx.x; x < R * R; x += blockDim.x) { Hs[x] = Hg[x]; Gs[x] = GWi[x]; }
+  double* wbv = tolpath ? wv + RP * 32 : wv + fwd;
+  double* dv = tolpath ? wv + 2 * RP * 32 : nullptr;
+  double* ns = tolpath ? wv + 3 * RP * 32 : wv;  // N_p (MT 8 x RP)
+  for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
+    Hs[x] = Hg[x];
+    if (tolpath) Gs[x] = GWi[x];
+  }
   // Batched W-row solve z_p = Ginv rhs_p of a warp round as MMAs (M = 8 patients, N = r, K = q) whose
   // A operand is the rhs in accumulator (C) layout: k-step ks, lane t covers column
   // q = 8 (ks / 2) + 2 t + ks % 2 — exactly the C-fragment element (n-tile ks / 2, ks % 2) a lane
@@ -802,14 +812,15 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
     // ---- W-row ADMM: z = Ginv (f + rho (w̄ + d)), w̄ = prox(z - d), d += w̄ - z, n_inner steps
     const int64_t kme = base + lane;
     int nsteps = 0;
-    if (kme < K) {
-      for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
-    } else {
-      for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = 0.0; dv[r * 32 + lane] = 0.0; }
-    }
-    if (tol > 0.0) {
+    if (tolpath) {
       // per-row inner stop (reading R-inner-tol): thread per patient, out of line
-      if (kme < K) nsteps = w_row_admm_tol(Gs, R, fwv + lane, wbv + lane, dv + lane, rho, n_inner, kind, param, tol);
+      if (kme < K) {
+        for (int r = 0; r < R; ++r) { wbv[r * 32 + lane] = W[kme * R + r]; dv[r * 32 + lane] = DW[kme * R + r]; }
+        nsteps = w_row_admm_tol(Gs, R, fwv + lane, wbv + lane, dv + lane, rho, n_inner, kind, param, tol);
+        for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
+      } else {
+        for (int r = 0; r < R; ++r) wbv[r * 32 + lane] = 0.0;
+      }
     } else {
       // fixed steps: the warp's 32 rows at once, 8 patients (one M tile) at a time; the rows of
       // patients past K stay zero (f = w̄ = d = 0 and prox(0) = 0)
@@ -818,14 +829,16 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
       for (int mt = 0; mt < 4; ++mt) {
         const int p = 8 * mt + g;
         double f[NT][2], wb[NT][2], dd[NT][2];
+        const int64_t rowo = (base + p) * R;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int r = 8 * nt + 2 * t + c;
-            f[nt][c] = (r < R && p < np) ? fwv[r * 32 + p] : 0.0;  // (rows p >= np hold stale sums)
-            wb[nt][c] = r < R ? wbv[r * 32 + p] : 0.0;
-            dd[nt][c] = r < R ? dv[r * 32 + p] : 0.0;
+            const bool in = r < R && p < np;  // (F_W rows p >= np hold stale sums)
+            f[nt][c] = in ? fwv[r * 32 + p] : 0.0;
+            wb[nt][c] = in ? W[rowo + r] : 0.0;
+            dd[nt][c] = in ? DW[rowo + r] : 0.0;
           }
 #pragma unroll 1
         for (int it = 0; it < n_inner; ++it) {
@@ -852,17 +865,16 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int r = 8 * nt + 2 * t + c;
-            if (r < R) {
-              wbv[r * 32 + p] = wb[nt][c];
-              dv[r * 32 + p] = dd[nt][c];
+            if (r < R) wbv[r * 32 + p] = wb[nt][c];  // zero for rows p >= np
+            if (r < R && p < np) {
+              W[rowo + r] = wb[nt][c];
+              DW[rowo + r] = dd[nt][c];
             }
           }
       }
       __syncwarp();
       nsteps = kme < K ? n_inner : 0;
     }
-    if (kme < K)
-      for (int r = 0; r < R; ++r) { W[kme * R + r] = wbv[r * 32 + lane]; DW[kme * R + r] = dv[r * 32 + lane]; }
     steps_warp(steps + 1, nsteps);
     __syncwarp();
     // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T  (MMA with K = patients)
@@ -922,26 +934,36 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
       }
     }
   }
-  __syncthreads();
-  double* red = sm + 2 * hoff;  // reuse: warps x 2 x RP^2
+  // block partials of M and W̄^T W̄, one after the other through warps x RP^2 doubles at offset 0
+  double* red = sm;
   const int nw = blockDim.x >> 5;
+#pragma unroll 1
+  for (int which = 0; which < 2; ++which) {
+    __syncthreads();
 #pragma unroll
-  for (int i = 0; i < NT; ++i)
+    for (int i = 0; i < NT; ++i)
 #pragma unroll
-    for (int j = 0; j < NT; ++j)
+      for (int j = 0; j < NT; ++j)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        red[(wib * 2 + 0) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = macc[i][j][c];
-        red[(wib * 2 + 1) * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = wacc[i][j][c];
-      }
-  __syncthreads();
-  for (int x = threadIdx.x; x < 2 * R * R; x += blockDim.x) {
-    const int which = x / (R * R), y = x - which * R * R;
-    const int r = y / R, s2 = y - r * R;
-    double v = 0.0;
-    for (int ww = 0; ww < nw; ++ww) v += red[(ww * 2 + which) * RP * RP + r * RP + s2];
-    part[((int64_t)blockIdx.x * 2 + which) * R * R + y] = v;
+        for (int c = 0; c < 2; ++c)
+          red[wib * RP * RP + (8 * i + g) * RP + 8 * j + 2 * t + c] = which == 0 ? macc[i][j][c] : wacc[i][j][c];
+    __syncthreads();
+    for (int y = threadIdx.x; y < R * R; y += blockDim.x) {
+      const int r = y / R, s2 = y - r * R;
+      double v = 0.0;
+      for (int ww = 0; ww < nw; ++ww) v += red[ww * RP * RP + r * RP + s2];
+      part[((int64_t)blockIdx.x * 2 + which) * R * R + y] = v;
+    }
   }
+}
+
+// dynamic shared memory of k_passB_wide (layout in the kernel)
+inline size_t passB_wide_smem(int R, int NT, int MT, bool tolpath, int warps) {
+  const size_t RP = 8 * (size_t)NT, hoff = (size_t)((R * R + 31) / 32) * 32;
+  const size_t fwd = std::max(RP * 32, (size_t)MT * 8 * RP);
+  const size_t per_warp = tolpath ? 3 * RP * 32 + (size_t)MT * 8 * RP : fwd + RP * 32;
+  const size_t main = hoff + 2 * NT * (size_t)NT * 32 + (tolpath ? hoff : 0) + warps * per_warp;
+  return sizeof(double) * std::max(main, (size_t)warps * RP * RP);
 }
 
 static __global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, double* WtW) {
@@ -955,13 +977,8 @@ static __global__ void k_sum_rr2(const double* part, int nb, int RR, double* M, 
 
 template <int MT, int NT, int RT = 0, int LT = 0>
 static void passB_wide_inst(Handle& h) {
-  constexpr int RP = 8 * NT;
   constexpr auto fn = k_passB_wide<MT, NT, RT, LT>;
-  const size_t hoff = (size_t)((h.R * h.R + 31) / 32) * 32;
-  size_t per_warp = sizeof(double) * (size_t)(3 * RP * 32 + MT * 8 * RP);
-  size_t red = sizeof(double) * (size_t)((kDenseThreads / 32) * 2 * RP * RP);
-  const size_t gfr = sizeof(double) * (size_t)(2 * NT * NT * 32);
-  size_t smem = sizeof(double) * 2 * hoff + (gfr + per_warp * (kDenseThreads / 32) > red ? gfr + per_warp * (kDenseThreads / 32) : red);
+  const size_t smem = passB_wide_smem(h.R, NT, MT, h.o.admm_tol > 0.0, kDenseThreads / 32);
   max_smem_attr<fn>(h);
   int64_t rounds = (h.K + 31) / 32;
   int64_t blocks = (rounds + 3) / 4;
