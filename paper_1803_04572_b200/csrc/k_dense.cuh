@@ -677,17 +677,24 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
   // [r][lane] and a separate N scratch with the per-row stop; otherwise the N scratch reuses the F_W
   // rows, dead after the solves, and d stays in registers).
   const bool tolpath = tol > 0.0;
+  // TBUF (fixed steps, small tiles): the round runs as four sub-rounds of 8 patients and keeps each
+  // patient's T = Q~ H̄ fragments in shared memory between the F_W and N steps (no recompute, no
+  // second read of Q~); per warp: F_W [RP][8], w̄ [RP][8], N scratch, T [8][MT][NT][2][lane]
+  constexpr bool TBUF_OK = MT * NT <= 4;
+  const bool tbuf = TBUF_OK && !tolpath;
   double* Hs = sm;
   double* gfr = sm + hoff;
   double* Gs = tolpath ? gfr + KA * NT * 32 : nullptr;
   const int fwd = RP * 32 > MT * 8 * RP ? RP * 32 : MT * 8 * RP;
-  const int per_warp = tolpath ? 3 * RP * 32 + MT * 8 * RP : fwd + RP * 32;
+  const int per_warp = tolpath ? 3 * RP * 32 + MT * 8 * RP
+                       : tbuf ? 2 * RP * 8 + MT * 8 * RP + 8 * 32 * MT * NT * 2 : fwd + RP * 32;
   const int wib = threadIdx.x >> 5;
   double* wv = sm + hoff + KA * NT * 32 + (tolpath ? hoff : 0) + wib * per_warp;
   double* fwv = wv;
-  double* wbv = tolpath ? wv + RP * 32 : wv + fwd;
+  double* wbv = tolpath ? wv + RP * 32 : tbuf ? wv + RP * 8 : wv + fwd;
   double* dv = tolpath ? wv + 2 * RP * 32 : nullptr;
-  double* ns = tolpath ? wv + 3 * RP * 32 : wv;  // N_p (MT 8 x RP)
+  double* ns = tolpath ? wv + 3 * RP * 32 : tbuf ? wv + 2 * RP * 8 : wv;  // N_p (MT 8 x RP)
+  double* tb = tbuf ? ns + MT * 8 * RP : nullptr;
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) {
     Hs[x] = Hg[x];
     if (tolpath) Gs[x] = GWi[x];
@@ -774,6 +781,148 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
         warp_prefetch(Pp + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
         warp_prefetch(Qt + nb * pstride, sizeof(double) * (size_t)(nn * pstride), false);
       }
+    }
+    if (TBUF_OK && tbuf) {
+      const double* Q = Qt + base * pstride;
+      const double* P = Pp + base * pstride;
+      double* Nrow = Nst + base * pstride;
+      double fq[KS][MT];
+      load_q(Q, fq);
+#pragma unroll 1
+      for (int sr = 0; sr < 4; ++sr) {
+        const int p0 = 8 * sr;
+        const int n8 = np - p0 < 8 ? (np - p0 > 0 ? np - p0 : 0) : 8;
+        // ---- F_W rows of the sub-round, T_p fragments kept
+        for (int pp = 0; pp < n8; ++pp) {
+          double pv[MT][NT][2];
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) pv[mt][nt][c] = offp[mt][nt][c] >= 0 ? P[offp[mt][nt][c]] : 0.0;
+          double c[MT][NT][2];
+          t_mma(fq, c);
+          Q += pstride;
+          P += pstride;
+          if (p0 + pp + 1 < np) load_q(Q, fq);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int i = 0; i < 2; ++i) tb[(((pp * MT + mt) * NT + nt) * 2 + i) * 32 + lane] = c[mt][nt][i];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              double sv = 0.0;
+#pragma unroll
+              for (int mt = 0; mt < MT; ++mt) sv = fma(c[mt][nt][i], pv[mt][nt][i], sv);
+              sv += __shfl_xor_sync(0xffffffffu, sv, 4);
+              sv += __shfl_xor_sync(0xffffffffu, sv, 8);
+              sv += __shfl_xor_sync(0xffffffffu, sv, 16);
+              if (g == 0) fwv[(8 * nt + 2 * t + i) * 8 + pp] = sv;
+            }
+        }
+        __syncwarp();
+        // ---- W-row ADMM of the sub-round's 8 rows (rows past np stay zero)
+        {
+          const int p = p0 + g;
+          double f[NT][2], wb[NT][2], dd[NT][2];
+          const int64_t rowo = (base + p) * R;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int r = 8 * nt + 2 * t + c;
+              const bool in = r < R && p < np;
+              f[nt][c] = in ? fwv[r * 8 + g] : 0.0;
+              wb[nt][c] = in ? W[rowo + r] : 0.0;
+              dd[nt][c] = in ? DW[rowo + r] : 0.0;
+            }
+#pragma unroll 1
+          for (int it = 0; it < n_inner; ++it) {
+            double a[KA], z[NT][2];
+#pragma unroll
+            for (int ks = 0; ks < KA; ++ks)
+              a[ks] = f[ks >> 1][ks & 1] + rho * (wb[ks >> 1][ks & 1] + dd[ks >> 1][ks & 1]);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              z[nt][0] = z[nt][1] = 0.0;
+#pragma unroll
+              for (int ks = 0; ks < KA; ++ks) dmma2(z[nt][0], z[nt][1], a[ks], gfr[(ks * NT + nt) * 32 + lane]);
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const double nb = prox(kind, param, rho, z[nt][c] - dd[nt][c]);
+                dd[nt][c] = dd[nt][c] + nb - z[nt][c];
+                wb[nt][c] = nb;
+              }
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int r = 8 * nt + 2 * t + c;
+              if (r < R) wbv[r * 8 + g] = wb[nt][c];
+              if (r < R && p < np) {
+                W[rowo + r] = wb[nt][c];
+                DW[rowo + r] = dd[nt][c];
+              }
+            }
+        }
+        __syncwarp();
+        // ---- W̄^T W̄ += sum_p w̄_p w̄_p^T over the sub-round (K = patients)
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const int pp = 4 * ks + t;
+          double af[NT];
+#pragma unroll
+          for (int i = 0; i < NT; ++i) {
+            const int r = 8 * i + g;
+            af[i] = r < R ? wbv[r * 8 + pp] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < NT; ++i)
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma2(wacc[i][j][0], wacc[i][j][1], af[i], af[j]);
+        }
+        // ---- N_p = T_p S_p (new w̄_p) -> HBM; M += N_p^T N_p
+        for (int pp = 0; pp < n8; ++pp) {
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              double v[2];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int r = 8 * nt + 2 * t + i;
+                v[i] = r < R ? tb[(((pp * MT + mt) * NT + nt) * 2 + i) * 32 + lane] * wbv[r * 8 + pp] : 0.0;
+                if (offp[mt][nt][i] >= 0) Nrow[offp[mt][nt][i]] = v[i];
+              }
+              *reinterpret_cast<double2*>(ns + (8 * mt + g) * RP + 8 * nt + 2 * t) = make_double2(v[0], v[1]);
+            }
+          __syncwarp();
+#pragma unroll
+          for (int ks = 0; ks < 2 * MT; ++ks) {
+            const int a = 4 * ks + t;
+            double af[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) af[i] = a < l ? ns[a * RP + 8 * i + g] : 0.0;
+#pragma unroll
+            for (int i = 0; i < NT; ++i)
+#pragma unroll
+              for (int j = 0; j < NT; ++j) dmma2(macc[i][j][0], macc[i][j][1], af[i], af[j]);
+          }
+          __syncwarp();
+          Nrow += pstride;
+        }
+      }
+      steps_warp(steps + 1, base + lane < K ? n_inner : 0);
+      continue;
     }
     // ---- F_W rows: F_W(p, r) = sum_a T_p(a, r) P'_p(a, r)
     {
@@ -961,7 +1110,9 @@ __global__ void __launch_bounds__(128) k_passB_wide(int64_t K, int R_, int l_, c
 inline size_t passB_wide_smem(int R, int NT, int MT, bool tolpath, int warps) {
   const size_t RP = 8 * (size_t)NT, hoff = (size_t)((R * R + 31) / 32) * 32;
   const size_t fwd = std::max(RP * 32, (size_t)MT * 8 * RP);
-  const size_t per_warp = tolpath ? 3 * RP * 32 + (size_t)MT * 8 * RP : fwd + RP * 32;
+  const bool tbuf = MT * NT <= 4 && !tolpath;
+  const size_t per_warp = tolpath ? 3 * RP * 32 + (size_t)MT * 8 * RP
+                          : tbuf ? 2 * RP * 8 + (size_t)MT * 8 * RP + 8 * 32 * (size_t)MT * NT * 2 : fwd + RP * 32;
   const size_t main = hoff + 2 * NT * (size_t)NT * 32 + (tolpath ? hoff : 0) + warps * per_warp;
   return sizeof(double) * std::max(main, (size_t)warps * RP * RP);
 }
