@@ -102,6 +102,7 @@ size_t carve(Handle& h, char* base) {
       h.fiber_col = reinterpret_cast<int32_t*>(h.tiles);
       h.fiber_val = h.tiles ? reinterpret_cast<double*>(h.tiles + gcol) : nullptr;
     }
+    h.cub_temp_bytes = std::max(h.cub_temp_bytes, plan_cub_bytes(h));
     h.cub_temp = c.take<char>((int64_t)h.cub_temp_bytes);
     h.perm = c.take<int32_t>(h.J);
     h.inv = c.take<int32_t>(h.Jl);
@@ -121,7 +122,8 @@ size_t carve(Handle& h, char* base) {
     h.cta_st = c.take<int32_t>((int64_t)h.sc_ranges * G + 1);
     h.st_t = c.take<int32_t>(h.nst_cap + 1);
     h.st_list = c.take<uint32_t>(stage_tab_cap(h));
-    h.layout_tmp_bytes = sizeof(int32_t) * (size_t)G * (size_t)h.K + 256;  // per-group run lengths
+    // per-run fiber and tile counts (each followed by a zero), then the planning scans' scratch
+    h.layout_tmp_bytes = 2 * sizeof(int32_t) * ((size_t)G * (size_t)h.K + 4) + sizeof(int64_t) * plan_tmp_words(h);
     h.layout_tmp = c.take<char>((int64_t)h.layout_tmp_bytes);
   } else {
     if (h.rowproj) {
@@ -357,65 +359,28 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     tm.mark("relabel");
     {  // g-stream layout: per-group run lengths (device) -> offsets and pass-B stage table (host)
       const int G = h.sc_G;
+      // per-run fiber and tile counts (device), then the planning on the device
+      const int64_t GK = (int64_t)G * h.K;
       int32_t* gcnt_dev = (int32_t*)h.layout_tmp;
-      launch_count_groups(h, gcnt_dev);
-      std::vector<int32_t> gcnt((size_t)G * (size_t)h.K);
-      std::vector<int64_t> gptr((size_t)G * (size_t)(h.K + 1));
-      if (h.K > 0)
-        CUDA_TRY(cudaMemcpyAsync(gcnt.data(), gcnt_dev, sizeof(int32_t) * gcnt.size(), cudaMemcpyDeviceToHost, s),
-                 "gcnt copy");
-      CUDA_TRY(cudaStreamSynchronize(s), "gcnt sync");
+      int32_t* tcnt_dev = gcnt_dev + GK + 4;
+      int64_t* plan_tmp = reinterpret_cast<int64_t*>(h.layout_tmp + 2 * sizeof(int32_t) * (GK + 4));
+      CUDA_TRY(cudaMemsetAsync(gcnt_dev + GK, 0, 4 * sizeof(int32_t), s), "counts pad");
+      CUDA_TRY(cudaMemsetAsync(tcnt_dev + GK, 0, 4 * sizeof(int32_t), s), "counts pad");
+      launch_count_groups(h, gcnt_dev, tcnt_dev);
       tm.mark("count_groups");
-      prefix_runs(h, gcnt.data(), gptr.data());  // g-stream fiber offsets
-      // tiled stream (pass B): tiles per run -> tile offsets and the stage table
-      int32_t* tcnt_dev = gcnt_dev;  // reused: gcnt is on the host now
-      launch_tile_counts(h, tcnt_dev);
-      std::vector<int32_t> tcnt((size_t)G * (size_t)h.K);
-      std::vector<int64_t> tptr((size_t)G * (size_t)(h.K + 1));
-      if (h.K > 0)
-        CUDA_TRY(cudaMemcpyAsync(tcnt.data(), tcnt_dev, sizeof(int32_t) * tcnt.size(), cudaMemcpyDeviceToHost, s),
-                 "tcnt copy");
-      CUDA_TRY(cudaStreamSynchronize(s), "tcnt sync");
-      std::vector<int64_t> st_f, block_k;
-      std::vector<int32_t> st_k, st_t, cta_st;
-      plan_streams(h, tcnt.data(), tptr.data(), st_f, st_k, st_t, cta_st, block_k);
-      h.nst = (int64_t)st_k.size() / 2;
+      int64_t gtotal = 0;
+      if (!plan_streams_device(h, gcnt_dev, tcnt_dev, plan_tmp, &gtotal)) {
+        delete H;
+        return fail(COPA_E_WORKSPACE, "internal: stage table exceeds its bound");
+      }
       if (tm.on)
         fprintf(stderr,
                 "[copa init] pass B: G=%d Jg=%lld W=%d RS=%d tiles/stage=%d patients/stage=%d slots=%d smem=%zu "
                 "ranges=%d stages=%lld tiles=%lld (cap %lld) fibers=%lld workspace=%zu\n",
                 h.sc_G, (long long)h.sc_Jg, h.sc_W, h.sc_RS, h.sc_FB, h.sc_PB, h.sc_NS, h.sc_smem, h.sc_ranges,
-                (long long)h.nst, (long long)tptr.back(), (long long)tiles_cap(h), (long long)h.F, bytes);
-      if (h.nst > h.nst_cap || gptr[gptr.size() - 1] > h.F || tptr[tptr.size() - 1] > tiles_cap(h) ||
-          (int64_t)st_t.back() > stage_tab_cap(h) || stage_tab_cap(h) > INT32_MAX) {
-        delete H;
-        return fail(COPA_E_WORKSPACE, "internal: stage table exceeds its bound");
-      }
-      CUDA_TRY(cudaMemcpyAsync(h.gptr, gptr.data(), sizeof(int64_t) * gptr.size(), cudaMemcpyHostToDevice, s), "gptr");
-      CUDA_TRY(cudaMemcpyAsync(h.tptr, tptr.data(), sizeof(int64_t) * tptr.size(), cudaMemcpyHostToDevice, s), "tptr");
-      h.ntiles = tptr.back();
-      if (h.nst > 0) {
-        CUDA_TRY(cudaMemcpyAsync(h.st_f, st_f.data(), sizeof(int64_t) * st_f.size(), cudaMemcpyHostToDevice, s), "st_f");
-        CUDA_TRY(cudaMemcpyAsync(h.st_k, st_k.data(), sizeof(int32_t) * st_k.size(), cudaMemcpyHostToDevice, s), "st_k");
-        CUDA_TRY(cudaMemcpyAsync(h.st_t, st_t.data(), sizeof(int32_t) * st_t.size(), cudaMemcpyHostToDevice, s), "st_t");
-      }
-      CUDA_TRY(cudaMemcpyAsync(h.cta_st, cta_st.data(), sizeof(int32_t) * cta_st.size(), cudaMemcpyHostToDevice, s),
-               "cta_st");
-      CUDA_TRY(cudaMemcpyAsync(h.block_k, block_k.data(), sizeof(int64_t) * block_k.size(), cudaMemcpyHostToDevice, s),
-               "block_k");
+                (long long)h.nst, (long long)h.ntiles, (long long)tiles_cap(h), (long long)h.F, bytes);
       tm.mark("plan_streams+h2d");
-      {  // pass-A warp ranges (fiber-balanced) from the per-patient fiber counts
-        std::vector<int64_t> fp((size_t)h.K + 1, 0), wk;
-        for (int64_t k = 0; k < h.K; ++k) {
-          int64_t c = 0;
-          for (int g = 0; g < G; ++g) c += gcnt[(size_t)g * h.K + k];
-          fp[(size_t)k + 1] = fp[(size_t)k] + c;
-        }
-        plan_passA_ranges(h, fp, wk);
-        CUDA_TRY(cudaMemcpyAsync(h.pa_wk, wk.data(), sizeof(int64_t) * wk.size(), cudaMemcpyHostToDevice, s), "pa_wk");
-        CUDA_TRY(cudaStreamSynchronize(s), "pa_wk sync");
-      }
-      CUDA_TRY(cudaStreamSynchronize(s), "layout sync");  // host vectors go out of scope
+      launch_passA_ranges(h);  // pass-A warp ranges (fiber-balanced) from fiber_ptr
     }
     tm.mark("passA ranges");
     launch_basis(h);

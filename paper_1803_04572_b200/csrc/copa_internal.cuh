@@ -328,7 +328,7 @@ void launch_validate(Handle& h);
 void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/, unsigned long long* hist);
 void launch_basis(Handle& h);
 void launch_build_fibers(Handle& h);
-void launch_count_groups(Handle& h, int32_t* gcnt /*[G][K]*/);
+void launch_count_groups(Handle& h, int32_t* gcnt /*[G][K]*/, int32_t* tcnt /*[G][K]*/);
 void launch_row_patient(Handle& h);
 void launch_sumsq(Handle& h, double* out);
 // iteration
@@ -347,13 +347,14 @@ void launch_U(Handle& h, double* U, int64_t k0, int64_t k1);
 void launch_spmm_fibers(Handle& h);   // pass A (k_passA.cu)
 void launch_relabel_V(Handle& h);
 void launch_layoutA(Handle& h);
-void launch_tile_counts(Handle& h, int32_t* tcnt);
 void launch_build_tiles(Handle& h);
 int64_t tiles_cap(const Handle& h);
-void prefix_runs(const Handle& h, const int32_t* cnt, int64_t* ptr);
+size_t plan_cub_bytes(const Handle& h);
+int64_t plan_tmp_words(const Handle& h);
+bool plan_streams_device(Handle& h, const int32_t* gcnt, const int32_t* tcnt, int64_t* tmp, int64_t* gtotal);
 inline uint32_t tile_bytes_host(int l) { return 32u + 64u * (uint32_t)l; }
 void plan_passA(Handle& h);
-void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk);
+void launch_passA_ranges(Handle& h);
 int launch_scatter_fibers(Handle& h);
 bool scatter_smem_ok(const Handle& h);
 void plan_scatter(Handle& h);
@@ -362,9 +363,7 @@ int64_t stage_cap(const Handle& h);                                // pass-B sta
 int64_t stage_tab_cap(const Handle& h);                            // pass-B sub-run table bound
 void launch_stage_tab(Handle& h);
 // host: gptr (G x (K+1), absolute) from per-group counts; stage table; pass-B patient ranges
-void plan_streams(Handle& h, const int32_t* gcnt_host, int64_t* gptr_host, std::vector<int64_t>& st_f,
-                  std::vector<int32_t>& st_k, std::vector<int32_t>& st_t, std::vector<int32_t>& cta_st,
-                  std::vector<int64_t>& block_k);
+
 // wide per-patient dense kernels (k_dense.cu)
 bool polar_wide_ok(const Handle& h);
 // general path (k_plain.cu)

@@ -28,7 +28,9 @@
 #include <climits>
 #include <cstdlib>
 #include <numeric>
+#include <thread>
 #include <type_traits>
+#include <vector>
 
 #include "copa_internal.cuh"
 
@@ -430,22 +432,6 @@ __global__ void __launch_bounds__(32 * (W * CS + 1)) k_scatter_tma(
 }
 
 // ------------------------------------------------------------------ init: the tiled stream
-// Tiles per (group, patient) run and the tile offset of every sub-range inside it.
-__global__ void k_tile_counts(const uint16_t* __restrict__ woff, int64_t K, int G, int W, int32_t* __restrict__ tcnt,
-                              uint16_t* __restrict__ twoff) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= (int64_t)G * K) return;
-  const uint16_t* wo = woff + x * kWoS;
-  uint16_t* tw = twoff + x * kWoS;
-  int acc = 0;
-  for (int w = 0; w < W; ++w) {
-    tw[w] = (uint16_t)acc;
-    acc += (wo[w + 1] - wo[w] + 7) >> 3;
-  }
-  tw[W] = (uint16_t)acc;
-  tcnt[x] = acc;
-}
-
 // Warp per (group, patient) run, its W sub-runs one after the other: a sub-run's n fibers (g-stream,
 // sorted by label) go to 8 ceil(n / 8) slots paired as described above. Pairs, in order: (class c
 // rank i, class c + D rank i) for every c < D; each class's surplus with a pad; the remaining surplus
@@ -562,12 +548,6 @@ __global__ void k_build_tiles(const int64_t* __restrict__ gptr, const uint16_t* 
       }
     }
   }
-}
-
-void launch_tile_counts(Handle& h, int32_t* tcnt) {
-  const int64_t n = (int64_t)h.sc_G * h.K;
-  if (n == 0) return;
-  k_tile_counts<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.woff, h.K, h.sc_G, h.sc_W, tcnt, h.twoff);
 }
 
 void launch_build_tiles(Handle& h) {
@@ -752,80 +732,154 @@ int64_t stage_cap(const Handle& h) {
   return tiles_cap(h) / h.sc_FB + (int64_t)h.sc_G * (h.K / h.sc_PB + 1) + (int64_t)h.sc_ranges * h.sc_G + 16;
 }
 
-// Run offsets from per-(group, patient) run lengths cnt[g][k]: ptr[g][k] (absolute, groups one after
-// the other).
-void prefix_runs(const Handle& h, const int32_t* cnt, int64_t* ptr) {
-  const int64_t K = h.K, K1 = K + 1;
-  int64_t base = 0;
-  for (int g = 0; g < h.sc_G; ++g) {
-    int64_t* gp = ptr + g * K1;
-    gp[0] = base;
-    for (int64_t k = 0; k < K; ++k) gp[k + 1] = gp[k] + cnt[g * K + k];
-    base = gp[K];
+// ------------------------------------------------------------------ init: pass-B planning on the device
+// (the host only reads back three totals: host arrays of K-proportional size cost more in page faults
+// than the planning itself; measured 180 ms of host planning at Scale)
+namespace {
+struct ToI64 {
+  __host__ __device__ int64_t operator()(int32_t x) const { return (int64_t)x; }
+};
+
+// tmp = exclusive scan of the flat [G][K] counts (GK + 1 entries) -> ptr[g][k], k = 0..K (the groups
+// back to back: ptr[g][K] = ptr[g + 1][0])
+__global__ void k_runs_layout(const int64_t* __restrict__ tmp, int64_t K, int G, int64_t* __restrict__ ptr) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= (int64_t)G * (K + 1)) return;
+  const int64_t g = x / (K + 1), k = x - g * (K + 1);
+  ptr[x] = tmp[g * K + k];
+}
+
+__device__ __forceinline__ int64_t tiles_before(const int64_t* tptr, int G, int64_t K, int64_t k) {
+  int64_t c = 0;
+  for (int g = 0; g < G; ++g) c += tptr[g * (K + 1) + k] - tptr[g * (K + 1)];
+  return c;
+}
+
+// pass-B patient ranges balanced by tiles: block_k[b] = first k with tiles_before(k) >= total b / nr
+__global__ void k_block_ranges(const int64_t* __restrict__ tptr, int G, int64_t K, int nr, int64_t* __restrict__ block_k) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nr) return;
+  if (b == nr) { block_k[b] = K; return; }
+  const int64_t target = tiles_before(tptr, G, K, K) * b / nr;
+  int64_t lo = 0, hi = K + 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (tiles_before(tptr, G, K, mid) < target) lo = mid + 1; else hi = mid;
+  }
+  block_k[b] = lo < K ? lo : K;
+}
+
+// Stages of CTA c = (range c / G, group c % G): from the range's first tile, a stage ends at FT tiles
+// or at the PB-th patient boundary, whichever comes first (greedy walk). Counting pass (st_f null):
+// cnt[c] = stages; writing pass: stages at cta_st[c].
+__global__ void k_stage_walk(const int64_t* __restrict__ tptr, const int64_t* __restrict__ block_k, int G, int64_t K,
+                             int nc, int64_t FT, int64_t PB, int32_t* __restrict__ cnt,
+                             const int32_t* __restrict__ cta_st, int64_t* __restrict__ st_f, int32_t* __restrict__ st_k) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int r = c / G, g = c % G;
+  const int64_t* gp = tptr + (int64_t)g * (K + 1);
+  const int64_t kr0 = block_k[r], kr1 = block_k[r + 1];
+  int64_t n = 0;
+  const int64_t o = st_f ? cta_st[c] : 0;
+  if (kr0 < kr1) {
+    int64_t f = gp[kr0];
+    const int64_t fend = gp[kr1];
+    int64_t k = kr0;
+    while (f < fend) {
+      while (gp[k + 1] <= f) ++k;  // first patient whose run ends after f
+      int64_t f1 = f + FT < fend ? f + FT : fend;
+      int64_t kk = k + 1;
+      while (kk < kr1 && gp[kk] < f1) ++kk;
+      if (kk - k > PB) {
+        kk = k + PB;
+        f1 = gp[kk];
+      }
+      if (st_f) {
+        st_f[2 * (o + n)] = f;
+        st_f[2 * (o + n) + 1] = f1;
+        st_k[2 * (o + n)] = (int32_t)k;
+        st_k[2 * (o + n) + 1] = (int32_t)kk;
+      }
+      ++n;
+      f = f1;
+      k = kk - 1;
+    }
+  }
+  if (!st_f) cnt[c] = (int32_t)n;
+}
+
+__global__ void k_cta_scan(const int32_t* __restrict__ cnt, int nc, int32_t* __restrict__ cta_st) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int64_t a = 0;
+    for (int c = 0; c < nc; ++c) {
+      cta_st[c] = (int32_t)(a < INT32_MAX ? a : INT32_MAX);
+      a += cnt[c];
+    }
+    cta_st[nc] = (int32_t)(a < INT32_MAX ? a : INT32_MAX);
   }
 }
 
-// Host planning from the per-group tile counts tcnt[g][k]: tile offsets tptr, pass-B patient ranges
-// (balanced by tiles) and the stage table of every (range, group) CTA.
-void plan_streams(Handle& h, const int32_t* tcnt, int64_t* tptr, std::vector<int64_t>& st_f, std::vector<int32_t>& st_k,
-                  std::vector<int32_t>& st_t, std::vector<int32_t>& cta_st, std::vector<int64_t>& block_k) {
+// words of every stage's list: 8 header words + one per tile (last entry 0: the exclusive scan's total)
+__global__ void k_stage_len(const int64_t* __restrict__ st_f, int64_t nst, int32_t* __restrict__ len) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s > nst) return;
+  len[s] = s < nst ? (int32_t)(8 + st_f[2 * s + 1] - st_f[2 * s]) : 0;
+}
+}  // namespace
+
+// cub temporary bytes of the planning scans (carve): flat run counts (G K + 1) and stage lists
+size_t plan_cub_bytes(const Handle& h) {
+  size_t a = 0, b = 0;
+  const int64_t gk = (int64_t)h.sc_G * h.K;
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(nullptr, ToI64());
+  cub::DeviceScan::ExclusiveSum(nullptr, a, it, (int64_t*)nullptr, (int)(gk + 1));
+  cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int)(stage_cap(h) + 1));
+  return std::max(a, b);
+}
+int64_t plan_tmp_words(const Handle& h) {  // int64 words of the planning scratch (after the counts)
+  return std::max<int64_t>((int64_t)h.sc_G * h.K + 1, stage_cap(h) + 1) + 8;
+}
+
+// gcnt / tcnt: [G][K] fiber and tile counts per run (device, k_count_groups). Writes gptr, tptr,
+// block_k, cta_st, st_f, st_k, st_t and h.nst, h.ntiles; returns false if a table exceeds its bound.
+bool plan_streams_device(Handle& h, const int32_t* gcnt, const int32_t* tcnt, int64_t* tmp, int64_t* gtotal) {
+  cudaStream_t s = h.stream;
   const int G = h.sc_G;
-  const int64_t K = h.K, K1 = K + 1;
-  prefix_runs(h, tcnt, tptr);
-  // balanced patient ranges by total tiles
-  const int nr = h.sc_ranges;
-  block_k.assign((size_t)nr + 1, 0);
-  std::vector<int64_t> tot((size_t)K1, 0);
-  for (int64_t k = 0; k < K; ++k) {
-    int64_t c = 0;
-    for (int g = 0; g < G; ++g) c += tcnt[g * K + k];
-    tot[(size_t)k + 1] = tot[(size_t)k] + c;
-  }
-  for (int b = 0; b <= nr; ++b) {
-    if (b == nr) { block_k[(size_t)b] = K; break; }
-    const int64_t target = (tot[(size_t)K] * b) / nr;
-    block_k[(size_t)b] = std::lower_bound(tot.begin(), tot.end(), target) - tot.begin();
-    if (block_k[(size_t)b] > K) block_k[(size_t)b] = K;
-  }
-  st_f.clear();
-  st_k.clear();
-  cta_st.assign((size_t)nr * G + 1, 0);
-  const int64_t FT = h.sc_FB, PB = h.sc_PB;
-  for (int r = 0; r < nr; ++r)
-    for (int g = 0; g < G; ++g) {
-      cta_st[(size_t)r * G + g] = (int32_t)(st_k.size() / 2);
-      const int64_t* gp = tptr + g * K1;
-      const int64_t kr0 = block_k[(size_t)r], kr1 = block_k[(size_t)r + 1];
-      if (kr0 >= kr1) continue;
-      int64_t f = gp[kr0];
-      const int64_t fend = gp[kr1];
-      int64_t k = kr0;
-      while (f < fend) {
-        while (gp[k + 1] <= f) ++k;  // first patient whose run ends after f
-        int64_t f1 = std::min(f + FT, fend);
-        int64_t kk = k + 1;
-        while (kk < kr1 && gp[kk] < f1) ++kk;
-        if (kk - k > PB) {
-          kk = k + PB;
-          f1 = gp[kk];
-        }
-        st_f.push_back(f);
-        st_f.push_back(f1);
-        st_k.push_back((int32_t)k);
-        st_k.push_back((int32_t)kk);
-        f = f1;
-        k = kk - 1;
-      }
-    }
-  cta_st[(size_t)nr * G] = (int32_t)(st_k.size() / 2);
-  // offsets of every stage's list in st_list (8 header words + one per tile)
-  const size_t nst = st_k.size() / 2;
-  st_t.assign(nst + 1, 0);
-  int64_t acc = 0;  // (the caller rejects lists beyond int32)
-  for (size_t x = 0; x < nst; ++x) {
-    acc += 8 + (st_f[2 * x + 1] - st_f[2 * x]);
-    st_t[x + 1] = (int32_t)std::min<int64_t>(acc, INT32_MAX);
-  }
+  const int64_t K = h.K, GK = (int64_t)G * K, n1 = (int64_t)G * (K + 1);
+  size_t tb = h.cub_temp_bytes;
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> ig(gcnt, ToI64()), it(tcnt, ToI64());
+  // GK + 1 items: the last reads the zero the caller keeps one past each count array
+  cub::DeviceScan::ExclusiveSum(h.cub_temp, tb, ig, tmp, (int)(GK + 1), s);
+  k_runs_layout<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(tmp, K, G, h.gptr);
+  tb = h.cub_temp_bytes;
+  cub::DeviceScan::ExclusiveSum(h.cub_temp, tb, it, tmp, (int)(GK + 1), s);
+  k_runs_layout<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(tmp, K, G, h.tptr);
+  const int nr = h.sc_ranges, nc = nr * G;
+  k_block_ranges<<<(unsigned)((nr + 1 + 127) / 128), 128, 0, s>>>(h.tptr, G, K, nr, h.block_k);
+  int32_t* cnt = reinterpret_cast<int32_t*>(tmp);
+  k_stage_walk<<<(unsigned)((nc + 63) / 64), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, cnt, nullptr,
+                                                         nullptr, nullptr);
+  k_cta_scan<<<1, 32, 0, s>>>(cnt, nc, h.cta_st);
+  int64_t tot[3] = {0, 0, 0};  // stages, tiles, fibers
+  int32_t nst32 = 0;
+  cudaMemcpyAsync(&nst32, h.cta_st + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&tot[1], h.tptr + n1 - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&tot[2], h.gptr + n1 - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return false;
+  h.nst = nst32;
+  h.ntiles = tot[1];
+  *gtotal = tot[2];
+  if (h.nst >= INT32_MAX || h.nst > h.nst_cap || h.ntiles > tiles_cap(h) || tot[2] > h.F ||
+      8 * h.nst + h.ntiles > stage_tab_cap(h) || stage_tab_cap(h) > INT32_MAX)
+    return false;
+  k_stage_walk<<<(unsigned)((nc + 63) / 64), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, nullptr,
+                                                         h.cta_st, h.st_f, h.st_k);
+  int32_t* len = reinterpret_cast<int32_t*>(tmp);
+  k_stage_len<<<(unsigned)((h.nst + 1 + 255) / 256), 256, 0, s>>>(h.st_f, h.nst, len);
+  tb = h.cub_temp_bytes;
+  cub::DeviceScan::ExclusiveSum(h.cub_temp, tb, len, h.st_t, (int)(h.nst + 1), s);
+  return true;
 }
 
 // ------------------------------------------------------------------ init-time relabeling

@@ -303,9 +303,11 @@ __device__ __forceinline__ int label_rank(const unsigned* bits, const int* pref,
 
 // Also writes, per (group, patient), the offsets of the W label sub-runs inside the run:
 // woff[(g K + k) kWoS + w] = rank(g Jg + w Js) - rank(g Jg), w = 0..W (W < kWoS).
+// Then the tiled stream's counts (k_fibers.cu): tcnt[g][k] = sum_w ceil(n_w / 8) tiles of the run and
+// twoff[(g K + k) kWoS + w] = the tile offset of sub-range w inside it.
 __global__ void k_count_groups(const int64_t* prp, const int64_t* rp, const int32_t* col, const int32_t* perm,
                                int64_t K, int words, int G, int64_t Jg, int W, int64_t Js, int32_t* gcnt /*[G][K]*/,
-                               uint16_t* woff /*[G][K][8]*/) {
+                               uint16_t* woff /*[G][K][8]*/, int32_t* tcnt /*[G][K]*/, uint16_t* twoff) {
   extern __shared__ unsigned smem_g[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, nw = blockDim.x >> 5;
   unsigned* bits = smem_g + wib * words;
@@ -325,10 +327,22 @@ __global__ void k_count_groups(const int64_t* prp, const int64_t* rp, const int3
       woff[((int64_t)g * K + k) * kWoS + w] = (uint16_t)v;
     }
     __syncwarp();
+    if (lane < G) {
+      const uint16_t* wo = woff + ((int64_t)lane * K + k) * kWoS;
+      uint16_t* tw = twoff + ((int64_t)lane * K + k) * kWoS;
+      int acc = 0;
+      for (int w = 0; w < W; ++w) {
+        tw[w] = (uint16_t)acc;
+        acc += (wo[w + 1] - wo[w] + 7) >> 3;
+      }
+      tw[W] = (uint16_t)acc;
+      tcnt[(int64_t)lane * K + k] = acc;
+    }
+    __syncwarp();
   }
 }
 
-void launch_count_groups(Handle& h, int32_t* gcnt) {
+void launch_count_groups(Handle& h, int32_t* gcnt, int32_t* tcnt) {
   if (h.K == 0) return;
   const int words = (int)((h.Jl + 31) / 32);
   const int warps = 8;
@@ -338,7 +352,7 @@ void launch_count_groups(Handle& h, int32_t* gcnt) {
   if (blocks > h.sms * 16) blocks = h.sms * 16;
   k_count_groups<<<(unsigned)blocks, warps * 32, smem, h.stream>>>(h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.perm,
                                                                     h.K, words, h.sc_G, h.sc_Jg, h.sc_W, h.sc_Js, gcnt,
-                                                                    h.woff);
+                                                                    h.woff, tcnt, h.twoff);
 }
 
 // ------------------------------------------------------------------ fibers: build X'_k = C_k^T X_k

@@ -280,18 +280,23 @@ void plan_passA(Handle& h) {
   h.pa_nw = (int64_t)h.pa_ctas * kAWarps;
 }
 
-// Warp ranges of pass A: contiguous patient ranges with balanced fibers (host, from the prefix).
-void plan_passA_ranges(const Handle& h, const std::vector<int64_t>& fp_host, std::vector<int64_t>& wk) {
-  const int64_t nw = h.pa_nw, K = h.K;
-  wk.assign((size_t)nw + 1, K);
-  const int64_t F = fp_host[(size_t)K];
-  int64_t k = 0;
-  for (int64_t w = 0; w <= nw; ++w) {
-    const int64_t target = (w == nw) ? F + 1 : (F * w) / nw;
-    while (k < K && fp_host[(size_t)k] < target) ++k;
-    wk[(size_t)w] = w == nw ? K : k;
+// Warp ranges of pass A: contiguous patient ranges with balanced fibers, from the fiber prefix fp:
+// wk[w] = first patient k with fp[k] >= F w / nw (K if none), wk[0] = 0, wk[nw] = K.
+__global__ void k_passA_ranges(const int64_t* __restrict__ fp, int64_t K, int64_t nw, int64_t* __restrict__ wk) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w > nw) return;
+  if (w == 0 || w == nw) { wk[w] = w == 0 ? 0 : K; return; }
+  const int64_t target = (fp[K] * w) / nw;
+  int64_t lo = 0, hi = K;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (fp[mid] < target) lo = mid + 1; else hi = mid;
   }
-  wk[0] = 0;
+  wk[w] = lo;
+}
+
+void launch_passA_ranges(Handle& h) {
+  k_passA_ranges<<<(unsigned)((h.pa_nw + 1 + 255) / 256), 256, 0, h.stream>>>(h.fiber_ptr, h.K, h.pa_nw, h.pa_wk);
 }
 
 void launch_layoutA(Handle& h) {
