@@ -770,12 +770,14 @@ __global__ void k_block_ranges(const int64_t* __restrict__ tptr, int G, int64_t 
 }
 
 // Stages of CTA c = (range c / G, group c % G): from the range's first tile, a stage ends at FT tiles
-// or at the PB-th patient boundary, whichever comes first (greedy walk). Counting pass (st_f null):
-// cnt[c] = stages; writing pass: stages at cta_st[c].
+// or at the PB-th patient boundary, whichever comes first (greedy walk). Warp per CTA: the walk is
+// sequential, its two patient searches are warp ballots over 32 run starts. Counting pass (st_f
+// null): cnt[c] = stages; writing pass: stages at cta_st[c].
 __global__ void k_stage_walk(const int64_t* __restrict__ tptr, const int64_t* __restrict__ block_k, int G, int64_t K,
                              int nc, int64_t FT, int64_t PB, int32_t* __restrict__ cnt,
                              const int32_t* __restrict__ cta_st, int64_t* __restrict__ st_f, int32_t* __restrict__ st_k) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (c >= nc) return;
   const int r = c / G, g = c % G;
   const int64_t* gp = tptr + (int64_t)g * (K + 1);
@@ -787,15 +789,27 @@ __global__ void k_stage_walk(const int64_t* __restrict__ tptr, const int64_t* __
     const int64_t fend = gp[kr1];
     int64_t k = kr0;
     while (f < fend) {
-      while (gp[k + 1] <= f) ++k;  // first patient whose run ends after f
+      // first patient whose run ends after f: first k' >= k with gp[k' + 1] > f (exists: f < fend)
+      for (;;) {
+        const int64_t q = k + 1 + lane;
+        const unsigned b = __ballot_sync(0xffffffffu, q > kr1 || gp[q] > f);
+        if (b) { k += __ffs(b) - 1; break; }
+        k += 32;
+      }
       int64_t f1 = f + FT < fend ? f + FT : fend;
+      // first kk >= k + 1 with kk >= kr1 or gp[kk] >= f1
       int64_t kk = k + 1;
-      while (kk < kr1 && gp[kk] < f1) ++kk;
+      for (;;) {
+        const int64_t q = kk + lane;
+        const unsigned b = __ballot_sync(0xffffffffu, q >= kr1 || gp[q] >= f1);
+        if (b) { kk += __ffs(b) - 1; break; }
+        kk += 32;
+      }
       if (kk - k > PB) {
         kk = k + PB;
         f1 = gp[kk];
       }
-      if (st_f) {
+      if (st_f && lane == 0) {
         st_f[2 * (o + n)] = f;
         st_f[2 * (o + n) + 1] = f1;
         st_k[2 * (o + n)] = (int32_t)k;
@@ -806,7 +820,7 @@ __global__ void k_stage_walk(const int64_t* __restrict__ tptr, const int64_t* __
       k = kk - 1;
     }
   }
-  if (!st_f) cnt[c] = (int32_t)n;
+  if (!st_f && lane == 0) cnt[c] = (int32_t)n;
 }
 
 __global__ void k_cta_scan(const int32_t* __restrict__ cnt, int nc, int32_t* __restrict__ cta_st) {
@@ -858,8 +872,8 @@ bool plan_streams_device(Handle& h, const int32_t* gcnt, const int32_t* tcnt, in
   const int nr = h.sc_ranges, nc = nr * G;
   k_block_ranges<<<(unsigned)((nr + 1 + 127) / 128), 128, 0, s>>>(h.tptr, G, K, nr, h.block_k);
   int32_t* cnt = reinterpret_cast<int32_t*>(tmp);
-  k_stage_walk<<<(unsigned)((nc + 63) / 64), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, cnt, nullptr,
-                                                         nullptr, nullptr);
+  k_stage_walk<<<(unsigned)((nc + 1) / 2), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, cnt, nullptr,
+                                                       nullptr, nullptr);
   k_cta_scan<<<1, 32, 0, s>>>(cnt, nc, h.cta_st);
   int64_t tot[3] = {0, 0, 0};  // stages, tiles, fibers
   int32_t nst32 = 0;
@@ -873,8 +887,8 @@ bool plan_streams_device(Handle& h, const int32_t* gcnt, const int32_t* tcnt, in
   if (h.nst >= INT32_MAX || h.nst > h.nst_cap || h.ntiles > tiles_cap(h) || tot[2] > h.F ||
       8 * h.nst + h.ntiles > stage_tab_cap(h) || stage_tab_cap(h) > INT32_MAX)
     return false;
-  k_stage_walk<<<(unsigned)((nc + 63) / 64), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, nullptr,
-                                                         h.cta_st, h.st_f, h.st_k);
+  k_stage_walk<<<(unsigned)((nc + 1) / 2), 64, 0, s>>>(h.tptr, h.block_k, G, K, nc, h.sc_FB, h.sc_PB, nullptr,
+                                                       h.cta_st, h.st_f, h.st_k);
   int32_t* len = reinterpret_cast<int32_t*>(tmp);
   k_stage_len<<<(unsigned)((h.nst + 1 + 255) / 256), 256, 0, s>>>(h.st_f, h.nst, len);
   tb = h.cub_temp_bytes;
