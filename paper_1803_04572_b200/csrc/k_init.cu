@@ -365,7 +365,7 @@ void launch_count_groups(Handle& h, int32_t* gcnt, int32_t* tcnt) {
 // then rows one after the other, lanes over the row's (nonzero, a) pairs: a row's nonzeros have
 // distinct labels, so the updates Fs(f, a) = fma(x, C(i, a), Fs(f, a)) of one row never collide, and
 // every fiber entry is accumulated in ascending row order (deterministic).
-constexpr int kBfWF = 256;   // fiber ranks per shared-memory window
+constexpr int kBfWF = 128;   // fiber ranks per shared-memory window
 constexpr int kBfWarps = 4;  // warps (patients in flight) per block
 constexpr int kBfNZ = 256;   // staged nonzeros per row chunk
 
