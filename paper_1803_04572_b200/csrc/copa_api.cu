@@ -303,7 +303,17 @@ struct InitTimer {
 };
 }  // namespace
 
+// val_ready (copa_fit): an event after which p->val is on the device; until then only the other
+// inputs may be read (the values' copy overlaps the init stages before the fiber build).
+static copa_status init_impl(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out,
+                             cudaEvent_t val_ready);
+
 copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out) {
+  return init_impl(p, o, ws, bytes, out, nullptr);
+}
+
+static copa_status init_impl(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out,
+                             cudaEvent_t val_ready) {
   copa_status st = check_args(p, o);
   if (st != COPA_OK) return st;
   if (!out || !ws) return fail(COPA_E_ARG, "null workspace/out");
@@ -334,10 +344,16 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     static const unsigned long long d0[kDiagSlots] = {0, 0x7ff0000000000000ull, 0, 0, 0x7ff0000000000000ull, 0, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(h.diag, d0, sizeof(d0), cudaMemcpyHostToDevice, s), "diag init");
   }
-  launch_validate(h);
+  launch_validate(h, val_ready == nullptr);
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
   tm.mark("memset+validate");
+  auto values_in = [&]() -> copa_status {  // the values have landed (copa_fit) and are finite
+    if (!val_ready) return COPA_OK;
+    cudaStreamWaitEvent(s, val_ready, 0);
+    launch_validate_vals(h);
+    return check_err(h);
+  };
   if (h.fib) {
     if (h.K > 0) k_srow_smooth<<<(unsigned)((h.K + 256) / 256), 256, 0, s>>>(h.K, h.l, h.srow);
     launch_count_fibers(h, h.fiber_ptr, h.fhist);
@@ -385,6 +401,9 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
     tm.mark("passA ranges");
     launch_basis(h);
     tm.mark("basis");
+    st = values_in();
+    if (st != COPA_OK) { delete H; return st; }
+    tm.mark("values in");
     launch_build_fibers(h);
     tm.mark("build_fibers");
     cudaMemsetAsync(h.fa_col + h.F, 0, 64 * sizeof(int32_t), s);  // slack read by the pass-A chunk grid
@@ -403,6 +422,8 @@ copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, si
       cudaMemsetAsync(h.Prow, 0, sizeof(double) * (size_t)(h.rows * h.R), s);
       cudaMemsetAsync(h.Nrow, 0, sizeof(double) * (size_t)(h.rows * h.R), s);
     }
+    st = values_in();
+    if (st != COPA_OK) { delete H; return st; }
     const int rc = build_csc(h);
     if (rc != 0) {
       delete H;
@@ -863,14 +884,31 @@ copa_status copa_fit(const copa_problem* hp, const copa_options* ho, void* ws, s
   double* V0 = c.take<double>(hp->J * hp->R);
   double* W0 = c.take<double>(hp->K_local * hp->R);
   if (c.off > bytes) return fail(COPA_E_WORKSPACE, "workspace too small for the inputs");
+  // the structure, columns and times first (on the caller's stream, read by the first init
+  // stages), then the values on a second stream, overlapped with those stages (init_impl waits for
+  // them before the fiber build)
   CUDA_TRY(cudaMemcpyAsync(prp, hp->patient_row_ptr, sizeof(int64_t) * (hp->K_local + 1), cudaMemcpyDefault, s), "h2d");
   CUDA_TRY(cudaMemcpyAsync(rp, hp->row_ptr, sizeof(int64_t) * (hp->rows + 1), cudaMemcpyDefault, s), "h2d");
-  if (hp->nnz > 0) {
-    CUDA_TRY(cudaMemcpyAsync(col, hp->col, sizeof(int32_t) * hp->nnz, cudaMemcpyDefault, s), "h2d");
-    CUDA_TRY(cudaMemcpyAsync(val, hp->val, sizeof(double) * hp->nnz, cudaMemcpyDefault, s), "h2d");
-  }
+  if (hp->nnz > 0) CUDA_TRY(cudaMemcpyAsync(col, hp->col, sizeof(int32_t) * hp->nnz, cudaMemcpyDefault, s), "h2d");
   if (hp->visit_time && hp->rows > 0)
     CUDA_TRY(cudaMemcpyAsync(tim, hp->visit_time, sizeof(double) * hp->rows, cudaMemcpyDefault, s), "h2d");
+  struct Aux {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t first = nullptr, vals = nullptr;
+    ~Aux() {
+      if (s2) cudaStreamSynchronize(s2);
+      if (first) cudaEventDestroy(first);
+      if (vals) cudaEventDestroy(vals);
+      if (s2) cudaStreamDestroy(s2);
+    }
+  } aux;
+  CUDA_TRY(cudaStreamCreateWithFlags(&aux.s2, cudaStreamNonBlocking), "fit stream");
+  CUDA_TRY(cudaEventCreateWithFlags(&aux.first, cudaEventDisableTiming), "fit event");
+  CUDA_TRY(cudaEventCreateWithFlags(&aux.vals, cudaEventDisableTiming), "fit event");
+  CUDA_TRY(cudaEventRecord(aux.first, s), "fit event");
+  CUDA_TRY(cudaStreamWaitEvent(aux.s2, aux.first, 0), "fit event");
+  if (hp->nnz > 0) CUDA_TRY(cudaMemcpyAsync(val, hp->val, sizeof(double) * hp->nnz, cudaMemcpyDefault, aux.s2), "h2d");
+  CUDA_TRY(cudaEventRecord(aux.vals, aux.s2), "fit event");
   copa_options dopt = *ho;
   CUDA_TRY(cudaMemcpyAsync(H0, ho->H0, sizeof(double) * hp->R * hp->R, cudaMemcpyDefault, s), "h2d");
   CUDA_TRY(cudaMemcpyAsync(V0, ho->V0, sizeof(double) * hp->J * hp->R, cudaMemcpyDefault, s), "h2d");
@@ -880,7 +918,7 @@ copa_status copa_fit(const copa_problem* hp, const copa_options* ho, void* ws, s
   dp.patient_row_ptr = prp; dp.row_ptr = rp; dp.col = col; dp.val = val;
   dp.visit_time = hp->visit_time ? tim : nullptr;
   copa_handle* h = nullptr;
-  st = copa_init(&dp, &dopt, (char*)ws + c.off, bytes - c.off, &h);
+  st = init_impl(&dp, &dopt, (char*)ws + c.off, bytes - c.off, &h, aux.vals);
   if (st != COPA_OK) return st;
   st = copa_iterate(h, n_outer, fit_host);
   if (st == COPA_OK) st = copa_get_factors(h, H_out, V_out, W_out);

@@ -324,7 +324,8 @@ inline void max_smem_attr(const Handle& h, int bytes = 227 * 1024) {
 
 // ------------------------------------------------------------------ launchers
 // init
-void launch_validate(Handle& h);
+void launch_validate(Handle& h, bool vals = true);
+void launch_validate_vals(Handle& h);
 void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/, unsigned long long* hist);
 void launch_basis(Handle& h);
 void launch_build_fibers(Handle& h);

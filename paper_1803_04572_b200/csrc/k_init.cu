@@ -26,6 +26,8 @@ __global__ void k_validate_patients(const int64_t* prp, int64_t K, int64_t rows,
   }
 }
 
+// val may be null: the structure and columns only (copa_fit validates the values once their copy,
+// overlapped with the first init stages, has landed: launch_validate_vals)
 __global__ void k_validate_rows(const int64_t* rp, const int32_t* col, const double* val, int64_t rows, int64_t nnz,
                                 int64_t J, int* err) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -35,19 +37,29 @@ __global__ void k_validate_rows(const int64_t* rp, const int32_t* col, const dou
   for (int64_t e = a; e < b; ++e) {
     int32_t j = col[e];
     if (j < 0 || j >= J) { set_err(err, ERR_SHAPE); return; }
-    if (!isfinite(val[e])) { set_err(err, ERR_INPUT_NONFINITE); return; }
+    if (val && !isfinite(val[e])) { set_err(err, ERR_INPUT_NONFINITE); return; }
     for (int64_t f = a; f < e; ++f)
       if (col[f] == j) { set_err(err, ERR_SHAPE); return; }
   }
 }
 
-void launch_validate(Handle& h) {
+__global__ void k_validate_vals(const double* val, int64_t nnz, int* err) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz; e += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(val[e])) { set_err(err, ERR_INPUT_NONFINITE); return; }
+}
+
+void launch_validate(Handle& h, bool vals) {
   if (h.K > 0)
     k_validate_patients<<<(unsigned)((h.K + 255) / 256), 256, 0, h.stream>>>(h.p.patient_row_ptr, h.K, h.rows,
                                                                                h.smooth ? h.p.visit_time : nullptr, h.err);
   if (h.rows > 0)
-    k_validate_rows<<<(unsigned)((h.rows + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col, h.p.val, h.rows,
-                                                                            h.nnz, h.J, h.err);
+    k_validate_rows<<<(unsigned)((h.rows + 255) / 256), 256, 0, h.stream>>>(h.p.row_ptr, h.p.col,
+                                                                            vals ? h.p.val : nullptr, h.rows, h.nnz,
+                                                                            h.J, h.err);
+}
+
+void launch_validate_vals(Handle& h) {
+  if (h.nnz > 0) k_validate_vals<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.p.val, h.nnz, h.err);
 }
 
 // ------------------------------------------------------------------ fibers: count

@@ -189,3 +189,18 @@ def test_rank_cut_diagnostics(copa, name, K):
     for kept, dropped, tau in ((st["polar_min_kept"], st["polar_max_dropped"], 1e-10),
                                (st["basis_min_kept"], st["basis_max_dropped"], 1e-6)):
         assert kept - tau > 1e-12 and tau - dropped > 1e-12, (name, kept, dropped, tau)
+
+
+@pytest.mark.parametrize("name,K", [("small", 300), ("medium", 300)])
+def test_copa_fit_rejects_nonfinite_values(copa, name, K):
+    """copa_fit copies the values on a second stream, overlapped with the first init stages, and
+    validates them once they land (before the fiber build / CSC copy): a NaN is still rejected."""
+    p = synthgen.generate(name, K=K)
+    opts = copa.Options.from_config(p.cfg)
+    bad = dataclasses.replace(p, val=p.val.copy())
+    bad.val[len(bad.val) // 2] = np.nan
+    with pytest.raises(copa.CopaError) as e:
+        copa.fit_host(bad, opts, 1)
+    assert e.value.status == -3, str(e.value)
+    f1, _, _, _ = copa.fit_host(p, opts, 1)  # the library is usable afterwards
+    assert np.isfinite(f1[0])
