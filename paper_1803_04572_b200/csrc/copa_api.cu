@@ -303,17 +303,25 @@ struct InitTimer {
 };
 }  // namespace
 
-// val_ready (copa_fit): an event after which p->val is on the device; until then only the other
-// inputs may be read (the values' copy overlaps the init stages before the fiber build).
+// Values arriving in chunks (copa_fit): chunk i holds the values of patients [k[i-1], k[i]) (entries
+// [e[i-1], e[i])) and is on the device once ev[i] has completed; until then only the other inputs
+// may be read. The first init stages run meanwhile, and the fiber build follows chunk by chunk.
+struct ValChunks {
+  int n = 0;
+  int64_t e0 = 0;               // first referenced value (row_ptr[patient_row_ptr[0]])
+  int64_t k[8] = {}, e[8] = {};  // chunk i: patients [k[i-1], k[i]), values [e[i-1], e[i]) (absolute)
+  cudaEvent_t ev[8] = {};
+};
+
 static copa_status init_impl(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out,
-                             cudaEvent_t val_ready);
+                             const ValChunks* vc);
 
 copa_status copa_init(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out) {
   return init_impl(p, o, ws, bytes, out, nullptr);
 }
 
 static copa_status init_impl(const copa_problem* p, const copa_options* o, void* ws, size_t bytes, copa_handle** out,
-                             cudaEvent_t val_ready) {
+                             const ValChunks* vc) {
   copa_status st = check_args(p, o);
   if (st != COPA_OK) return st;
   if (!out || !ws) return fail(COPA_E_ARG, "null workspace/out");
@@ -344,14 +352,16 @@ static copa_status init_impl(const copa_problem* p, const copa_options* o, void*
     static const unsigned long long d0[kDiagSlots] = {0, 0x7ff0000000000000ull, 0, 0, 0x7ff0000000000000ull, 0, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(h.diag, d0, sizeof(d0), cudaMemcpyHostToDevice, s), "diag init");
   }
-  launch_validate(h, val_ready == nullptr);
+  launch_validate(h, vc == nullptr);
   st = check_err(h);
   if (st != COPA_OK) { delete H; return st; }
   tm.mark("memset+validate");
-  auto values_in = [&]() -> copa_status {  // the values have landed (copa_fit) and are finite
-    if (!val_ready) return COPA_OK;
-    cudaStreamWaitEvent(s, val_ready, 0);
-    launch_validate_vals(h);
+  auto values_in = [&]() -> copa_status {  // every value chunk has landed (copa_fit) and is finite
+    if (!vc) return COPA_OK;
+    for (int i = 0; i < vc->n; ++i) {
+      cudaStreamWaitEvent(s, vc->ev[i], 0);
+      launch_validate_vals(h, i ? vc->e[i - 1] : vc->e0, vc->e[i]);
+    }
     return check_err(h);
   };
   if (h.fib) {
@@ -401,10 +411,17 @@ static copa_status init_impl(const copa_problem* p, const copa_options* o, void*
     tm.mark("passA ranges");
     launch_basis(h);
     tm.mark("basis");
-    st = values_in();
-    if (st != COPA_OK) { delete H; return st; }
-    tm.mark("values in");
-    launch_build_fibers(h);
+    if (vc) {  // fiber build chunk by chunk as the values land
+      for (int i = 0; i < vc->n; ++i) {
+        cudaStreamWaitEvent(s, vc->ev[i], 0);
+        launch_validate_vals(h, i ? vc->e[i - 1] : vc->e0, vc->e[i]);
+        launch_build_fibers(h, i ? vc->k[i - 1] : 0, vc->k[i]);
+      }
+      st = check_err(h);
+      if (st != COPA_OK) { delete H; return st; }
+    } else {
+      launch_build_fibers(h);
+    }
     tm.mark("build_fibers");
     cudaMemsetAsync(h.fa_col + h.F, 0, 64 * sizeof(int32_t), s);  // slack read by the pass-A chunk grid
     cudaMemsetAsync(h.fa_val + h.F * h.l, 0, 64 * sizeof(double) * (size_t)h.l, s);
@@ -838,8 +855,12 @@ copa_status copa_fit_workspace_size(const copa_problem* p, const copa_options* o
       pool.emplace_back([&, t]() {
         std::vector<uint64_t> bits((size_t)((p->J + 63) / 64), 0);
         int64_t cnt = 0;
+        auto rowp = [&](int64_t k) -> int64_t {  // unvalidated input: every host read stays in bounds
+          const int64_t r = std::min<int64_t>(std::max<int64_t>(p->patient_row_ptr[k], 0), p->rows);
+          return std::min<int64_t>(std::max<int64_t>(p->row_ptr[r], 0), p->nnz);
+        };
         for (int64_t k = K * t / nth; k < K * (t + 1) / nth; ++k) {
-          const int64_t a = p->row_ptr[p->patient_row_ptr[k]], b = p->row_ptr[p->patient_row_ptr[k + 1]];
+          const int64_t a = rowp(k), b = std::max(a, rowp(k + 1));
           for (int64_t x = a; x < b; ++x) {
             const int32_t j = p->col[x];
             if (j < 0 || j >= p->J) { ++cnt; continue; }
@@ -894,21 +915,46 @@ copa_status copa_fit(const copa_problem* hp, const copa_options* ho, void* ws, s
     CUDA_TRY(cudaMemcpyAsync(tim, hp->visit_time, sizeof(double) * hp->rows, cudaMemcpyDefault, s), "h2d");
   struct Aux {
     cudaStream_t s2 = nullptr;
-    cudaEvent_t first = nullptr, vals = nullptr;
+    cudaEvent_t first = nullptr;
+    ValChunks vc;
     ~Aux() {
       if (s2) cudaStreamSynchronize(s2);
       if (first) cudaEventDestroy(first);
-      if (vals) cudaEventDestroy(vals);
+      for (int i = 0; i < vc.n; ++i) cudaEventDestroy(vc.ev[i]);
       if (s2) cudaStreamDestroy(s2);
     }
   } aux;
   CUDA_TRY(cudaStreamCreateWithFlags(&aux.s2, cudaStreamNonBlocking), "fit stream");
   CUDA_TRY(cudaEventCreateWithFlags(&aux.first, cudaEventDisableTiming), "fit event");
-  CUDA_TRY(cudaEventCreateWithFlags(&aux.vals, cudaEventDisableTiming), "fit event");
   CUDA_TRY(cudaEventRecord(aux.first, s), "fit event");
   CUDA_TRY(cudaStreamWaitEvent(aux.s2, aux.first, 0), "fit event");
-  if (hp->nnz > 0) CUDA_TRY(cudaMemcpyAsync(val, hp->val, sizeof(double) * hp->nnz, cudaMemcpyDefault, aux.s2), "h2d");
-  CUDA_TRY(cudaEventRecord(aux.vals, aux.s2), "fit event");
+  {  // the values in 4 patient chunks (host CSR offsets), one event each
+    // (validated structure is not known yet: the offsets are clamped to [0, nnz]; a malformed
+    // row_ptr is rejected by init's validation before any value is read)
+    const int nch = 4;
+    const int64_t K = hp->K_local, nnz = hp->nnz;
+    auto at = [&](int64_t k) -> int64_t {  // host reads of unvalidated input stay in bounds
+      if (K <= 0) return 0;
+      const int64_t r = std::min<int64_t>(std::max<int64_t>(hp->patient_row_ptr[k], 0), hp->rows);
+      const int64_t e = hp->row_ptr[r];
+      return e < 0 ? 0 : (e > nnz ? nnz : e);
+    };
+    aux.vc.e0 = at(0);
+    int64_t c0 = 0;  // copy ranges cover [0, nnz) whatever the offsets
+    for (int i = 0; i < nch; ++i) {
+      const int64_t k1 = K * (i + 1) / nch;
+      int64_t e1 = std::max(at(k1), i ? aux.vc.e[i - 1] : aux.vc.e0);
+      const int64_t c1 = i == nch - 1 ? nnz : std::max(e1, c0);
+      CUDA_TRY(cudaEventCreateWithFlags(&aux.vc.ev[i], cudaEventDisableTiming), "fit event");
+      aux.vc.n = i + 1;
+      aux.vc.k[i] = k1;
+      aux.vc.e[i] = e1;
+      if (c1 > c0)
+        CUDA_TRY(cudaMemcpyAsync(val + c0, hp->val + c0, sizeof(double) * (c1 - c0), cudaMemcpyDefault, aux.s2), "h2d");
+      c0 = c1;
+      CUDA_TRY(cudaEventRecord(aux.vc.ev[i], aux.s2), "fit event");
+    }
+  }
   copa_options dopt = *ho;
   CUDA_TRY(cudaMemcpyAsync(H0, ho->H0, sizeof(double) * hp->R * hp->R, cudaMemcpyDefault, s), "h2d");
   CUDA_TRY(cudaMemcpyAsync(V0, ho->V0, sizeof(double) * hp->J * hp->R, cudaMemcpyDefault, s), "h2d");
@@ -918,7 +964,7 @@ copa_status copa_fit(const copa_problem* hp, const copa_options* ho, void* ws, s
   dp.patient_row_ptr = prp; dp.row_ptr = rp; dp.col = col; dp.val = val;
   dp.visit_time = hp->visit_time ? tim : nullptr;
   copa_handle* h = nullptr;
-  st = init_impl(&dp, &dopt, (char*)ws + c.off, bytes - c.off, &h, aux.vals);
+  st = init_impl(&dp, &dopt, (char*)ws + c.off, bytes - c.off, &h, &aux.vc);
   if (st != COPA_OK) return st;
   st = copa_iterate(h, n_outer, fit_host);
   if (st == COPA_OK) st = copa_get_factors(h, H_out, V_out, W_out);

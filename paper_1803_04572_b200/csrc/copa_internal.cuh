@@ -325,10 +325,10 @@ inline void max_smem_attr(const Handle& h, int bytes = 227 * 1024) {
 // ------------------------------------------------------------------ launchers
 // init
 void launch_validate(Handle& h, bool vals = true);
-void launch_validate_vals(Handle& h);
+void launch_validate_vals(Handle& h, int64_t e0 = 0, int64_t e1 = -1);  // values [e0, e1)
 void launch_count_fibers(Handle& h, int64_t* counts_out /*[K+1], counts at [k+1]*/, unsigned long long* hist);
 void launch_basis(Handle& h);
-void launch_build_fibers(Handle& h);
+void launch_build_fibers(Handle& h, int64_t kb = 0, int64_t ke = -1);  // patients [kb, ke)
 void launch_count_groups(Handle& h, int32_t* gcnt /*[G][K]*/, int32_t* tcnt /*[G][K]*/);
 void launch_row_patient(Handle& h);
 void launch_sumsq(Handle& h, double* out);

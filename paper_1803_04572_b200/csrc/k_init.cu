@@ -58,8 +58,9 @@ void launch_validate(Handle& h, bool vals) {
                                                                             h.J, h.err);
 }
 
-void launch_validate_vals(Handle& h) {
-  if (h.nnz > 0) k_validate_vals<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.p.val, h.nnz, h.err);
+void launch_validate_vals(Handle& h, int64_t e0, int64_t e1) {
+  if (e1 < 0) e1 = h.nnz;
+  if (e1 > e0) k_validate_vals<<<(unsigned)(h.sms * 8), 256, 0, h.stream>>>(h.p.val + e0, e1 - e0, h.err);
 }
 
 // ------------------------------------------------------------------ fibers: count
@@ -390,7 +391,7 @@ __host__ __device__ inline size_t bf_warp_doubles(int l, int words) {
 __global__ void __launch_bounds__(32 * kBfWarps) k_build_fibers(
     const int64_t* prp, const int64_t* rp, const int32_t* col, const double* val, const double* times, int64_t K,
     int words, int l, int d, const double* Bk, const int32_t* m, const int64_t* gptr, int G, int Jg,
-    const int32_t* perm, int32_t* fiber_col, double* fiber_val) {
+    const int32_t* perm, int32_t* fiber_col, double* fiber_val, int64_t kb, int64_t ke) {
   extern __shared__ double smem_bf[];
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(32 * kBfWarps) k_build_fibers(
   int* pref = (int*)(bits + words);
   const int64_t nwarps = (int64_t)gridDim.x * kBfWarps;
   const int64_t K1 = K + 1;
-  for (int64_t k = blockIdx.x * (int64_t)kBfWarps + wib; k < K; k += nwarps) {
+  for (int64_t k = kb + blockIdx.x * (int64_t)kBfWarps + wib; k < ke; k += nwarps) {  // patients [kb, ke)
     patient_label_bitmap(prp, rp, col, perm, k, words, bits, pref);
     const int nf = pref[words - 1] + __popc(bits[words - 1]);
     if (lane < G) gd[lane] = gptr[lane * K1 + k] - label_rank(bits, pref, words, (int64_t)lane * Jg);
@@ -495,16 +496,17 @@ __global__ void __launch_bounds__(32 * kBfWarps) k_build_fibers(
   }
 }
 
-void launch_build_fibers(Handle& h) {
-  if (h.K == 0) return;
+void launch_build_fibers(Handle& h, int64_t kb, int64_t ke) {
+  if (ke < 0) ke = h.K;
+  if (ke <= kb) return;
   const int words = (int)((h.Jl + 31) / 32);  // bitmap over relabeled feature ids
   const size_t smem = (size_t)kBfWarps * bf_warp_doubles(h.l, words) * sizeof(double);
   max_smem_attr<k_build_fibers>(h);
-  int64_t blocks = (h.K + kBfWarps - 1) / kBfWarps;
+  int64_t blocks = (ke - kb + kBfWarps - 1) / kBfWarps;
   if (blocks > h.sms * 32) blocks = h.sms * 32;
   k_build_fibers<<<(unsigned)blocks, kBfWarps * 32, smem, h.stream>>>(
       h.p.patient_row_ptr, h.p.row_ptr, h.p.col, h.p.val, h.p.visit_time, h.K, words, h.l, h.d, h.Bk, h.m, h.gptr,
-      h.sc_G, (int)h.sc_Jg, h.perm, h.fiber_col, h.fiber_val);
+      h.sc_G, (int)h.sc_Jg, h.perm, h.fiber_col, h.fiber_val, kb, ke);
 }
 
 // ------------------------------------------------------------------ non-smooth helpers
