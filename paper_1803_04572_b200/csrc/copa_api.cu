@@ -389,7 +389,7 @@ static copa_status init_impl(const copa_problem* p, const copa_options* o, void*
       const int64_t GK = (int64_t)G * h.K;
       int32_t* gcnt_dev = (int32_t*)h.layout_tmp;
       int32_t* tcnt_dev = gcnt_dev + GK + 4;
-      int64_t* plan_tmp = reinterpret_cast<int64_t*>(h.layout_tmp + 2 * sizeof(int32_t) * (GK + 4));
+      int64_t* plan_tmp = reinterpret_cast<int64_t*>((char*)h.layout_tmp + 2 * sizeof(int32_t) * (GK + 4));
       CUDA_TRY(cudaMemsetAsync(gcnt_dev + GK, 0, 4 * sizeof(int32_t), s), "counts pad");
       CUDA_TRY(cudaMemsetAsync(tcnt_dev + GK, 0, 4 * sizeof(int32_t), s), "counts pad");
       launch_count_groups(h, gcnt_dev, tcnt_dev);

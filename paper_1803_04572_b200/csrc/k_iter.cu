@@ -98,7 +98,98 @@ __global__ void k_reduce_partials(const double* partial, int nb, int RR, double*
   C[p] = s;
 }
 
+// Tall-skinny Gram on the FP64 tensor cores (R <= 40): C = sum_s A(s,:)^T (B(s,:) * w(s,:)) as
+// mma.sync m8n8k4 with M = r, N = c, K = 4 rows; warp per contiguous row range (multiple of 4 rows),
+// all NT x NT output tiles in its accumulators, U k-steps of loads in flight; the per-warp partials
+// are summed in a fixed order (k_reduce_partials): deterministic.
+__device__ __forceinline__ void mma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(128) k_gram_mma(const double* __restrict__ A, const double* __restrict__ B, int64_t n,
+                                                  int R, const double* __restrict__ Wrows,
+                                                  const int32_t* __restrict__ row_pat, int lstride, int nwarps,
+                                                  double* __restrict__ partial) {
+  constexpr int U = 4;  // k-steps per load batch
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wid >= nwarps) return;
+  const int64_t per = (((n + nwarps - 1) / nwarps) + 3) & ~(int64_t)3;
+  const int64_t s0 = (int64_t)wid * per;
+  const int64_t s1 = s0 + per < n ? s0 + per : n;
+  double acc[NT][NT][2];
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  bool cok[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) cok[i] = 8 * i + g < R;
+  for (int64_t sb = s0; sb < s1; sb += 4 * U) {
+    double a[U][NT], b[U][NT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = sb + 4 * u + t;
+      const bool rok = row < s1;
+      const double* Ar = A + row * R;
+      const double* Br = B + row * R;
+      const double* Wr = (Wrows && rok) ? Wrows + patient_of(row, row_pat, lstride) * R : nullptr;
+#pragma unroll
+      for (int i = 0; i < NT; ++i) {
+        const int c = 8 * i + g;
+        const bool ok = rok && cok[i];
+        a[u][i] = ok ? Ar[c] : 0.0;
+        double bv = ok ? Br[c] : 0.0;
+        if (Wr && ok) bv *= Wr[c];
+        b[u][i] = bv;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int i = 0; i < NT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) mma_f64(acc[i][j][0], acc[i][j][1], a[u][i], b[u][j]);
+  }
+  double* out = partial + (int64_t)wid * R * R;
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = 8 * i + g, c = 8 * j + 2 * t + e;
+        if (r < R && c < R) out[r * R + c] = acc[i][j][e];
+      }
+}
+
+template <int NT>
+static int gram_mma_inst(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C) {
+  const int RR = h.R * h.R;
+  int nw = 2 * kPartBlocks;  // partial holds 2 kPartBlocks R x R blocks
+  const int64_t want = (nrows + 63) / 64;  // at least 64 rows per warp
+  if (want < nw) nw = (int)(want > 0 ? want : 1);
+  k_gram_mma<NT><<<(unsigned)((nw + 3) / 4), 128, 0, h.stream>>>(A, B, nrows, h.R, wmode ? h.W : nullptr,
+                                                                  h.smooth ? nullptr : h.row_patient,
+                                                                  h.smooth ? h.l : 1, nw, h.partial);
+  k_reduce_partials<<<(RR + 255) / 256, 256, 0, h.stream>>>(h.partial, nw, RR, C);
+  return 2;
+}
+
 int launch_gram(Handle& h, const double* A, const double* B, int64_t nrows, int wmode, double* C) {
+  // tall (state rows, patients): tensor cores; short (J rows of V̄): the block kernel below, whose
+  // 32-row chunks spread over more SMs (measured: FIT phase 0.03 vs 0.04-0.05 ms at J = 300-1300)
+  if (nrows >= (int64_t)1 << 16) switch ((h.R + 7) / 8) {
+    case 1: return gram_mma_inst<1>(h, A, B, nrows, wmode, C);
+    case 2: return gram_mma_inst<2>(h, A, B, nrows, wmode, C);
+    case 3: return gram_mma_inst<3>(h, A, B, nrows, wmode, C);
+    case 4: return gram_mma_inst<4>(h, A, B, nrows, wmode, C);
+    case 5: return gram_mma_inst<5>(h, A, B, nrows, wmode, C);
+    default: break;
+  }
   int RR = h.R * h.R;
   int nb = kPartBlocks;
   if (nrows < (int64_t)nb * kGramRows) nb = (int)((nrows + kGramRows - 1) / kGramRows);
@@ -137,16 +228,18 @@ __device__ int block_chol(double* Ls, int R, int* fail) {
   return *fail;
 }
 
-__device__ __forceinline__ void chol_solve(const double* L, int R, double* x) {
+// Solves L L^T x = b in place; x[r] lives at x[r st] (per-thread vectors interleaved in shared
+// memory: thread t's vector at base + t, stride st = number of threads, conflict-free).
+__device__ __forceinline__ void chol_solve(const double* L, int R, double* x, int st = 1) {
   for (int i = 0; i < R; ++i) {
-    double v = x[i];
-    for (int k = 0; k < i; ++k) v -= L[i * R + k] * x[k];
-    x[i] = v / L[i * R + i];
+    double v = x[i * st];
+    for (int k = 0; k < i; ++k) v -= L[i * R + k] * x[k * st];
+    x[i * st] = v / L[i * R + i];
   }
   for (int i = R - 1; i >= 0; --i) {
-    double v = x[i];
-    for (int k = i + 1; k < R; ++k) v -= L[k * R + i] * x[k];
-    x[i] = v / L[i * R + i];
+    double v = x[i * st];
+    for (int k = i + 1; k < R; ++k) v -= L[k * R + i] * x[k * st];
+    x[i * st] = v / L[i * R + i];
   }
 }
 
@@ -162,20 +255,21 @@ __device__ double block_G_rho(const double* G1, const double* G2, int R, double 
 
 // One row of Alg.1 l.15-l.18, up to n_inner times: z = (f + rho (zb + d)) (G + rho I)^-1;
 // zb = prox(z - d); d += zb - z; with tol > 0 the row stops early (reading R-inner-tol).
-// Returns the steps taken.
-__device__ __forceinline__ int admm_row(const double* L, int R, const double* f, double* zb, double* dd, double rho,
-                                        int n_inner, int kind, double param, double tol) {
-  double z[kMaxR];
+// f is read in place (global); zb, dd and the scratch z are the thread's interleaved shared-memory
+// vectors (stride st). Returns the steps taken.
+__device__ __forceinline__ int admm_row(const double* L, int R, const double* f, double* zb, double* dd, double* z,
+                                        int st, double rho, int n_inner, int kind, double param, double tol) {
   int it = 0;
   while (it < n_inner) {
-    for (int r = 0; r < R; ++r) z[r] = f[r] + rho * (zb[r] + dd[r]);
-    chol_solve(L, R, z);
+    for (int r = 0; r < R; ++r) z[r * st] = f[r] + rho * (zb[r * st] + dd[r * st]);
+    chol_solve(L, R, z, st);
     RowResid res;
     for (int r = 0; r < R; ++r) {
-      double nb = prox(kind, param, rho, z[r] - dd[r]);
-      res.add(nb, z[r], zb[r]);
-      dd[r] += nb - z[r];
-      zb[r] = nb;
+      const double zr = z[r * st];
+      double nb = prox(kind, param, rho, zr - dd[r * st]);
+      res.add(nb, zr, zb[r * st]);
+      dd[r * st] += nb - zr;
+      zb[r * st] = nb;
     }
     ++it;
     if (res.done(tol)) break;
@@ -202,12 +296,13 @@ __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const d
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) Ls[x] = Gs[x] + ((x / R == x % R) ? rho : 0.0);
   __syncthreads();
   if (block_chol(Ls, R, &fail)) { if (threadIdx.x == 0) set_err(err, ERR_CHOL); return; }
+  double* vz = Ls + R * R;  // per-row vectors zb, dd, z: [3][R][R], row i interleaved at + i
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
-    double zb[kMaxR], dd[kMaxR], f[kMaxR];
-    for (int r = 0; r < R; ++r) { zb[r] = H[i * R + r]; dd[r] = DH[i * R + r]; f[r] = FH[i * R + r]; }
-    const int st = admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param, tol);
+    double *zb = vz + i, *dd = vz + R * R + i, *z = vz + 2 * R * R + i;
+    for (int r = 0; r < R; ++r) { zb[r * R] = H[i * R + r]; dd[r * R] = DH[i * R + r]; }
+    const int st = admm_row(Ls, R, FH + i * R, zb, dd, z, R, rho, n_inner, kind, param, tol);
     atomicAdd(steps, (unsigned long long)st);
-    for (int r = 0; r < R; ++r) { H[i * R + r] = zb[r]; DH[i * R + r] = dd[r]; }
+    for (int r = 0; r < R; ++r) { H[i * R + r] = zb[r * R]; DH[i * R + r] = dd[r * R]; }
   }
   __syncthreads();
   // H̄^T H̄ (new), then G_W = (H̄^T H̄) ∘ (V̄^T V̄), rho_W, chol -> LW
@@ -234,20 +329,22 @@ __global__ void __launch_bounds__(256) k_admm_H(int R, const double* FH, const d
   for (int x = threadIdx.x; x < R * R; x += blockDim.x) LW[x] = Ls[x];
   // (G_W + rho I)^-1 from the cached factor: column i solves L L^T x = e_i (used by the wide W pass)
   for (int i = threadIdx.x; i < R; i += blockDim.x) {
-    double x[kMaxR];
-    for (int r = 0; r < R; ++r) x[r] = r == i ? 1.0 : 0.0;
-    chol_solve(Ls, R, x);
-    for (int r = 0; r < R; ++r) GWi[r * R + i] = x[r];
+    double* x = vz + i;  // column i, interleaved (stride R)
+    for (int r = 0; r < R; ++r) x[r * R] = r == i ? 1.0 : 0.0;
+    chol_solve(Ls, R, x, R);
+    for (int r = 0; r < R; ++r) GWi[r * R + i] = x[r * R];
   }
   if (threadIdx.x == 0) { scal[S_RHO_H] = rho; scal[S_RHO_W] = rho_w; }
 }
 
-static size_t small_smem(Handle& h) { return sizeof(double) * 2 * (size_t)h.R * h.R; }
-constexpr int kSmallSmemMax = (int)(sizeof(double) * 2 * kMaxR * kMaxR);
+// shared memory: G and its factor (2 R^2) + three interleaved R-vectors per row / thread
+static size_t admm_smem(int R, int vecs) { return sizeof(double) * (2 * (size_t)R * R + 3 * (size_t)R * vecs); }
+static int admm_V_threads(int R) { return R > 32 ? 64 : 128; }
+constexpr int kAdmmSmemMax = (int)(sizeof(double) * 5 * kMaxR * kMaxR);  // both kernels at R = kMaxR
 
 int launch_admm_H(Handle& h) {
-  max_smem_attr<k_admm_H>(h, kSmallSmemMax);
-  k_admm_H<<<1, 256, small_smem(h), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind,
+  max_smem_attr<k_admm_H>(h, kAdmmSmemMax);
+  k_admm_H<<<1, 256, admm_smem(h.R, h.R), h.stream>>>(h.R, h.FH, h.VtV, h.WtW, h.o.rho, h.o.admm_inner, h.o.on_H.kind,
                                                 h.o.on_H.param, h.o.admm_tol, h.H, h.DH, h.HtH, h.LW, h.GWi, h.scal,
                                                 h.err, h.steps);
   return 1;
@@ -319,10 +416,11 @@ __global__ void __launch_bounds__(128) k_admm_V(int64_t J, int R, const double* 
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int st = 0;
   if (j < J) {
-    double zb[kMaxR], dd[kMaxR], f[kMaxR];
-    for (int r = 0; r < R; ++r) { zb[r] = V[j * R + r]; dd[r] = DV[j * R + r]; f[r] = FV[j * R + r]; }
-    st = admm_row(Ls, R, f, zb, dd, rho, n_inner, kind, param, tol);
-    for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r]; DV[j * R + r] = dd[r]; }
+    const int S = blockDim.x;  // per-thread vectors zb, dd, z interleaved (stride = threads)
+    double *zb = Ls + R * R + threadIdx.x, *dd = zb + R * S, *z = zb + 2 * R * S;
+    for (int r = 0; r < R; ++r) { zb[r * S] = V[j * R + r]; dd[r * S] = DV[j * R + r]; }
+    st = admm_row(Ls, R, FV + j * R, zb, dd, z, S, rho, n_inner, kind, param, tol);
+    for (int r = 0; r < R; ++r) { V[j * R + r] = zb[r * S]; DV[j * R + r] = dd[r * S]; }
   }
   steps_warp(steps + 2, st);
 }
@@ -342,8 +440,9 @@ void launch_count_zeros(Handle& h) {
 }
 
 int launch_admm_V(Handle& h) {
-  max_smem_attr<k_admm_V>(h, kSmallSmemMax);
-  k_admm_V<<<(unsigned)((h.J + 127) / 128), 128, small_smem(h), h.stream>>>(h.J, h.R, h.FV, h.HtH, h.WtW, h.o.rho,
+  max_smem_attr<k_admm_V>(h, kAdmmSmemMax);
+  const int nt = admm_V_threads(h.R);
+  k_admm_V<<<(unsigned)((h.J + nt - 1) / nt), nt, admm_smem(h.R, nt), h.stream>>>(h.J, h.R, h.FV, h.HtH, h.WtW, h.o.rho,
                                                                  h.o.admm_inner, h.o.on_V.kind, h.o.on_V.param,
                                                                  h.o.admm_tol, h.V, h.DV, h.scal, h.err, h.steps);
   return 1;

@@ -470,10 +470,13 @@ __global__ void k_transpose(const double* __restrict__ A, int R, double* __restr
 int launch_polar_warp(Handle& h) {
   if (h.K == 0) return 0;
   const int R = h.R;
-  if (R <= 4) { polar_thread_inst<4>(h); return 1; }    // small ranks: thread per patient, registers
-  if (R <= 6) { polar_thread_inst<6>(h); return 1; }
-  if (R <= 8) { polar_thread_inst<8>(h); return 1; }
-  if (R <= 10) { polar_thread_inst<10>(h); return 1; }
+  if (polar_thread_ok(h)) {  // small ranks: thread per patient, registers
+    if (R <= 4) { polar_thread_inst<4>(h); return 1; }
+    if (R <= 6) { polar_thread_inst<6>(h); return 1; }
+    if (R <= 8) { polar_thread_inst<8>(h); return 1; }
+    polar_thread_inst<10>(h);
+    return 1;
+  }
   int nwb = kPlainWarps;
   auto smem_of = [&](int w) { return sizeof(double) * (size_t)w * polar_warp_per_warp(R); };
   while (nwb > 1 && smem_of(nwb) > 227 * 1024) --nwb;
@@ -491,6 +494,17 @@ int launch_polar_warp(Handle& h) {
 }
 
 // ------------------------------------------------------------------ W pass (warp per patient)
+// Rows of Q~_k and P'_k are staged 32 at a time into the warp's shared memory with coalesced loads
+// (a patient's rows are contiguous), so no row waits on its own global load; lane r then runs the
+// sequential row loops of its column exactly as before (same operations, same order).
+// rows per stage: 32 for R <= 16, else 8 (keeps several blocks per SM at large R)
+__host__ __device__ inline int stage_rows_of(int R) { return R <= 16 ? 32 : 8; }
+__host__ __device__ inline size_t passB_warp_per_warp(int R) { return 2 * (size_t)stage_rows_of(R) * R; }
+
+__device__ __forceinline__ void stage_rows(double* dst, const double* __restrict__ src, int n) {
+  for (int x = threadIdx.x & 31; x < n; x += 32) dst[x] = src[x];
+}
+
 __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* __restrict__ m,
                                                                  const int64_t* __restrict__ srow, int64_t K, int R,
                                                                  const double* __restrict__ Pp,
@@ -510,16 +524,19 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
     const int r = x / R, q = x - r * R;
     GT[q * R + r] = GWi[x];
   }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double* Qs = smb + 2 * R * R + (size_t)wib * passB_warp_per_warp(R);  // staged rows of Q~_k
+  const int SR = stage_rows_of(R);
+  double* Ps = Qs + SR * R;                                              // ... and of P'_k
   __syncthreads();
   const double rho = scal[S_RHO_W];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const bool has0 = lane < R, has1 = lane + 32 < R;
   const int64_t nw = (int64_t)gridDim.x * kPlainWarps;
   int my_steps = 0;
-  auto t_row = [&](const RowReg& qr, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
+  auto t_row = [&](const double* qrow, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
     double s0 = 0.0, s1 = 0.0;
     for (int i = 0; i < R; ++i) {
-      const double qa = lane_pick(qr.x0, qr.x1, i);
+      const double qa = qrow[i];
       if (has0) s0 = fma(qa, Hs[i * R + lane], s0);
       if (has1) s1 = fma(qa, Hs[i * R + lane + 32], s1);
     }
@@ -530,17 +547,18 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
     const int mk = m[k];
     const double* P = Pp + srow[k] * R;
     const double* Q = Qt + srow[k] * R;
-    double f0 = 0.0, f1 = 0.0;  // F_W(k, r) = sum_a T(a, r) P'(a, r)
-    {
-      RowReg nq, np;
-      if (mk > 0) { nq.load(Q, R); np.load(P, R); }
-      for (int a = 0; a < mk; ++a) {
-        const RowReg cq = nq, cp = np;
-        if (a + 1 < mk) { nq.load(Q + (int64_t)(a + 1) * R, R); np.load(P + (int64_t)(a + 1) * R, R); }
+    double f0 = 0.0, f1 = 0.0;  // F_W(k, r) = sum_a T(a, r) P'(a, r), a ascending
+    for (int a0 = 0; a0 < mk; a0 += SR) {
+      const int na = mk - a0 < SR ? mk - a0 : SR;
+      __syncwarp();
+      stage_rows(Qs, Q + (int64_t)a0 * R, na * R);
+      stage_rows(Ps, P + (int64_t)a0 * R, na * R);
+      __syncwarp();
+      for (int a = 0; a < na; ++a) {
         double t0, t1;
-        t_row(cq, t0, t1);
-        if (has0) f0 = fma(t0, cp.x0, f0);
-        if (has1) f1 = fma(t1, cp.x1, f1);
+        t_row(Qs + a * R, t0, t1);
+        if (has0) f0 = fma(t0, Ps[a * R + lane], f0);
+        if (has1) f1 = fma(t1, Ps[a * R + lane + 32], f1);
       }
     }
     double w0 = has0 ? W[k * R + lane] : 0.0, w1 = has1 ? W[k * R + lane + 32] : 0.0;
@@ -581,15 +599,19 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
     if (has0) { W[k * R + lane] = w0; DW[k * R + lane] = d0; }
     if (has1) { W[k * R + lane + 32] = w1; DW[k * R + lane + 32] = d1; }
     double* N = Nst + srow[k] * R;  // N_k = T S_k (new w̄_k)
-    RowReg nq;
-    if (mk > 0) nq.load(Q, R);
-    for (int a = 0; a < mk; ++a) {
-      const RowReg cq = nq;
-      if (a + 1 < mk) nq.load(Q + (int64_t)(a + 1) * R, R);
-      double t0, t1;
-      t_row(cq, t0, t1);
-      if (has0) N[(int64_t)a * R + lane] = t0 * w0;
-      if (has1) N[(int64_t)a * R + lane + 32] = t1 * w1;
+    for (int a0 = 0; a0 < mk; a0 += SR) {
+      const int na = mk - a0 < SR ? mk - a0 : SR;
+      if (a0 > 0 || mk > SR) {  // (a single stage is still in Qs from the F_W loop)
+        __syncwarp();
+        stage_rows(Qs, Q + (int64_t)a0 * R, na * R);
+        __syncwarp();
+      }
+      for (int a = 0; a < na; ++a) {
+        double t0, t1;
+        t_row(Qs + a * R, t0, t1);
+        if (has0) N[(int64_t)(a0 + a) * R + lane] = t0 * w0;
+        if (has1) N[(int64_t)(a0 + a) * R + lane + 32] = t1 * w1;
+      }
     }
   }
   if (lane == 0 && my_steps) atomicAdd(steps + 1, (unsigned long long)my_steps);
@@ -597,7 +619,7 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
 
 int launch_passB_warp(Handle& h) {
   if (h.K == 0) return 0;
-  const size_t smem = sizeof(double) * 2 * (size_t)h.R * h.R;
+  const size_t smem = sizeof(double) * (2 * (size_t)h.R * h.R + kPlainWarps * passB_warp_per_warp(h.R));
   max_smem_attr<k_passB_warp>(h);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_passB_warp, 32 * kPlainWarps, smem);
