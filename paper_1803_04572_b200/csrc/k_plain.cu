@@ -2,11 +2,11 @@
 // smoothness outside the wide kernels' range (l >= R or l > 12). Per-patient state rows: m_k rows
 // of P'_k, Q~_k, N_k (m_k = I_k without smoothness). Any R <= 64.
 //
-//   polar_warp   warp per patient: A_k = P'_k S_k H̄^T built row by row (lanes over columns);
+//   polar_warp   warp per patient: A_k = P'_k S_k H̄^T built 32 rows at a time (lane per row);
 //                Givens QR of the tall side into an upper-triangular Rf (q x q, q = min(m_k, R),
 //                shared memory); one-sided Jacobi on the rows of Rf with one lane per disjoint row
-//                pair (round-robin ordering); Q~_k = A K or K A with K = V Σ^-1 V^T on the numerical
-//                range (the partial isometry U_r V_r^T, reading R-polar-2/3)      (Alg.1 l.4-5)
+//                pair (round-robin ordering); Q~_k = A K (lane per row) or K A with K = V Σ^-1 V^T on the
+//                numerical range (the partial isometry U_r V_r^T, reading R-polar-2/3) (Alg.1 l.4-5)
 //   passB_warp   warp per patient, lanes over r: T = Q~_k H̄, F_W(k,:) = colsum(T ∘ P'_k), the W-row ADMM
 //                with (G_W + rho I)^-1 (one lane per output column), N_k = T S_k      (l.12-19, W mode)
 //   scatter_csc  F_V = sum_k X_k^T N_k as a gather over a feature-major (CSC) copy of X built at init:
@@ -127,34 +127,35 @@ __device__ __forceinline__ void warp_jacobi_rows(double* Rf, int LD, int q) {
   }
 }
 
-// A row of the patient's state (R values) in the warp's registers: lane t holds x[t] and x[t + 32]
-// (one coalesced load per row; the values are then broadcast with shuffles, no dependent loads).
-struct RowReg {
-  double x0, x1;
-  __device__ __forceinline__ void load(const double* __restrict__ row, int R) {
-    const int lane = threadIdx.x & 31;
-    x0 = lane < R ? row[lane] : 0.0;
-    x1 = lane + 32 < R ? row[lane + 32] : 0.0;
-  }
-};
-
-// Row a of A_k = P'_k S_k H̄^T from the row P'_k(a, :) in registers: lane s gets A(a, s)
-// (v0: s = lane, v1: s = lane + 32); w0/w1 = w̄_k in the same lane layout.
-__device__ __forceinline__ void a_row(const RowReg& p, double w0, double w1, const double* HT, int LDH, int R,
-                                      double& v0, double& v1) {
+// Rows a0 .. a0 + na - 1 of A_k = P'_k S_k H̄^T into Ab (row i at Ab[i LD]), lane i computing row
+// a0 + i in blocks of 8 columns: the same products and the same r-ascending FMA chains as a_row,
+// 32 rows at a time instead of one row per R shuffles.
+__device__ __forceinline__ void a_rows_lane(const double* __restrict__ P, int a0, int na, int R, int LD, double w0,
+                                            double w1, const double* __restrict__ HT, double* Ab) {
   const int lane = threadIdx.x & 31;
-  const double pw0 = p.x0 * w0, pw1 = p.x1 * w1;
-  double s0 = 0.0, s1 = 0.0;
-  for (int r = 0; r < R; ++r) {
-    const double pw = lane_pick(pw0, pw1, r);
-    if (lane < R) s0 = fma(pw, HT[r * LDH + lane], s0);
-    if (lane + 32 < R) s1 = fma(pw, HT[r * LDH + lane + 32], s1);
+  const bool live = lane < na;
+  const double* Pr = P + (int64_t)(a0 + (live ? lane : 0)) * R;
+  for (int sb = 0; sb < R; sb += 8) {
+    double acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    for (int r = 0; r < R; ++r) {
+      const double wr = lane_pick(w0, w1, r);
+      const double pw = live ? Pr[r] * wr : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (sb + e < R) acc[e] = fma(pw, HT[r * R + sb + e], acc[e]);
+    }
+    if (live) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (sb + e < R) Ab[lane * LD + sb + e] = acc[e];
+    }
   }
-  v0 = s0;
-  v1 = s1;
 }
 
-__global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* __restrict__ m,
+template <int RB>  // bound on R (register array of the Q~ rows); small R: occupancy of the general kernel
+__global__ void __launch_bounds__(32 * kPlainWarps, RB <= 16 ? 8 : (RB <= 32 ? 4 : 1)) k_polar_warp(const int32_t* __restrict__ m,
                                                                  const int64_t* __restrict__ srow, int64_t K, int R,
                                                                  const double* __restrict__ Pp,
                                                                  const double* __restrict__ Wg,
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
                                                                  double* __restrict__ Qt, int32_t* __restrict__ rank,
                                                                  unsigned long long* __restrict__ diag) {
   extern __shared__ double smp[];
-  const int LD = odd_ld(R), LDH = R;  // HT: H̄^T in global memory (L1-resident), HT[r R + s] = H̄(s, r)
+  const int LD = odd_ld(R);  // HT: H̄^T in global memory (L1-resident), HT[r R + s] = H̄(s, r)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nwb = blockDim.x >> 5;  // warps of this block (fewer at large R: shared memory)
   double* Rf = smp + (size_t)wib * polar_warp_per_warp(R);
@@ -183,25 +184,22 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
     __syncwarp();
     double dg0 = 0.0, dg1 = 0.0;  // diagonal of Rf (see warp_givens_insert)
     // ---- QR of the tall side: rows of A (tall) or columns of A (wide) inserted one by one
+    const int CR = R < 32 ? R : 32;  // rows of A per chunk in Ab (R x LD doubles)
     if (tall) {
-      RowReg nxt;
-      nxt.load(P, R);
-      for (int a = 0; a < mk; ++a) {
-        const RowReg cur = nxt;
-        if (a + 1 < mk) nxt.load(P + (int64_t)(a + 1) * R, R);  // next row in flight
-        double v0, v1;
-        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
-        warp_givens_insert(Rf, LD, q, v0, v1, dg0, dg1);
+      for (int a0 = 0; a0 < mk; a0 += CR) {
+        const int na = mk - a0 < CR ? mk - a0 : CR;
+        __syncwarp();
+        a_rows_lane(P, a0, na, R, LD, w0, w1, HT, Ab);
+        __syncwarp();
+        for (int i = 0; i < na; ++i) {
+          const double v0 = lane < R ? Ab[i * LD + lane] : 0.0;
+          const double v1 = lane + 32 < R ? Ab[i * LD + lane + 32] : 0.0;
+          warp_givens_insert(Rf, LD, q, v0, v1, dg0, dg1);
+        }
       }
     } else {
-      for (int a = 0; a < mk; ++a) {  // A (m x R) into Ab, row a at Ab[a LD]
-        RowReg cur;
-        cur.load(P + (int64_t)a * R, R);
-        double v0, v1;
-        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
-        if (lane < R) Ab[a * LD + lane] = v0;
-        if (lane + 32 < R) Ab[a * LD + lane + 32] = v1;
-      }
+      for (int a0 = 0; a0 < mk; a0 += 32)  // A (m x R) into Ab, row a at Ab[a LD]
+        a_rows_lane(P, a0, mk - a0 < 32 ? mk - a0 : 32, R, LD, w0, w1, HT, Ab + a0 * LD);
       __syncwarp();
       for (int s = 0; s < R; ++s) {
         const double v0 = lane < mk ? Ab[lane * LD + s] : 0.0;
@@ -245,31 +243,48 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_polar_warp(const int32_t* 
     }
     __syncwarp();
     if (tall) {
-      // Q~(a, :) = A(a, :) K = sum_j (A(a, :) . u_j) u_j^T
-      RowReg nxt;
-      nxt.load(P, R);
-      for (int a = 0; a < mk; ++a) {
-        const RowReg cur = nxt;
-        if (a + 1 < mk) nxt.load(P + (int64_t)(a + 1) * R, R);
-        double v0, v1;
-        a_row(cur, w0, w1, HT, LDH, R, v0, v1);
-        if (lane < R) Ab[lane] = v0;
-        if (lane + 32 < R) Ab[lane + 32] = v1;
+      // Q~(a, :) = A(a, :) K = sum_j (A(a, :) . u_j) u_j^T: lane i takes row a0 + i of the chunk
+      // (d_j in registers, x and j ascending as before); the rows leave through Ab, coalesced
+      for (int a0 = 0; a0 < mk; a0 += CR) {
+        const int na = mk - a0 < CR ? mk - a0 : CR;
         __syncwarp();
-        double d0 = 0.0, d1 = 0.0;
-        if (lane < q)
-          for (int x = 0; x < q; ++x) d0 = fma(Ab[x], Rf[lane * LD + x], d0);
-        if (lane + 32 < q)
-          for (int x = 0; x < q; ++x) d1 = fma(Ab[x], Rf[(lane + 32) * LD + x], d1);
-        double q0 = 0.0, q1 = 0.0;
-        for (int j = 0; j < q; ++j) {
-          const double dj = lane_pick(d0, d1, j);
-          if (lane < R) q0 = fma(dj, Rf[j * LD + lane], q0);
-          if (lane + 32 < R) q1 = fma(dj, Rf[j * LD + lane + 32], q1);
+        a_rows_lane(P, a0, na, R, LD, w0, w1, HT, Ab);
+        __syncwarp();
+        if (lane < na) {
+          double* vr = Ab + lane * LD;
+          double d[RB];  // d_j = A(a, :) . u_j, four independent chains at a time
+#pragma unroll
+          for (int jb = 0; jb < RB; jb += 4) {
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (jb < q)
+              for (int x = 0; x < q; ++x) {
+                const double v = vr[x];
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (jb + e < q) acc[e] = fma(v, Rf[(jb + e) * LD + x], acc[e]);
+              }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[jb + e] = acc[e];
+          }
+          for (int s0 = 0; s0 < R; s0 += 4) {  // Q~(a, s) = sum_j d_j u_j(s), four columns at a time
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < RB; ++j)
+              if (j < q) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  if (s0 + e < R) acc[e] = fma(d[j], Rf[j * LD + s0 + e], acc[e]);
+              }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (s0 + e < R) vr[s0 + e] = acc[e];
+          }
         }
-        if (lane < R) Q[(int64_t)a * R + lane] = q0;
-        if (lane + 32 < R) Q[(int64_t)a * R + lane + 32] = q1;
         __syncwarp();
+        for (int x = lane; x < na * R; x += 32) {
+          const int i = x / R, s2 = x - i * R;
+          Q[(int64_t)(a0 + i) * R + s2] = Ab[i * LD + s2];
+        }
       }
     } else {
       // Q~(:, s) = K A(:, s) = sum_j u_j (u_j . A(:, s)), column by column in place of A
@@ -481,14 +496,19 @@ int launch_polar_warp(Handle& h) {
   auto smem_of = [&](int w) { return sizeof(double) * (size_t)w * polar_warp_per_warp(R); };
   while (nwb > 1 && smem_of(nwb) > 227 * 1024) --nwb;
   const size_t smem = smem_of(nwb);
-  max_smem_attr<k_polar_warp>(h);
+  const auto fn = R <= 16 ? k_polar_warp<16> : R <= 32 ? k_polar_warp<32> : R <= 48 ? k_polar_warp<48>
+                                                                               : k_polar_warp<64>;
+  if (R <= 16) max_smem_attr<k_polar_warp<16>>(h);
+  else if (R <= 32) max_smem_attr<k_polar_warp<32>>(h);
+  else if (R <= 48) max_smem_attr<k_polar_warp<48>>(h);
+  else max_smem_attr<k_polar_warp<64>>(h);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_polar_warp, 32 * nwb, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * nwb, smem);
   int64_t blocks = (h.K + nwb - 1) / nwb;
   const int64_t cap = (int64_t)h.sms * std::max(per_sm, 1);
   if (blocks > cap) blocks = cap;
   k_transpose<<<(unsigned)((R * R + 255) / 256), 256, 0, h.stream>>>(h.H, R, h.HT);
-  k_polar_warp<<<(unsigned)blocks, 32 * nwb, smem, h.stream>>>(h.m, h.srow, h.K, R, h.Pp, h.W, h.HT, h.o.rank_tol,
+  fn<<<(unsigned)blocks, 32 * nwb, smem, h.stream>>>(h.m, h.srow, h.K, R, h.Pp, h.W, h.HT, h.o.rank_tol,
                                                                h.Qt, h.rank, h.diag);
   return 2;
 }
