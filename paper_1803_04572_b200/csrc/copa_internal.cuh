@@ -19,8 +19,9 @@ constexpr int64_t kMaxJ = 65535;
 constexpr int kPartBlocks = 592;  // per-block partials of the R x R reductions (4 x 148 SMs)
 constexpr int kPhases = 11;       // timed phases of one outer iteration (copa_get_phase_times)
 constexpr int kMaxGroups = 8;     // label groups (fiber streams) of the smooth path
-constexpr int kWoS = 16;
-constexpr int64_t kCscChunk = 512;  // entries per chunk of the non-smooth F_V gather          // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
+constexpr int kWoS = 16;         // uint16 entries per (group, patient) record of woff (>= sub-ranges + 1)
+// entries per chunk of the non-smooth F_V gather (a warp walks its chunk serially: 512 took 123 us on Small)
+constexpr int64_t kCscChunk = 128;
 
 constexpr double kJacobiNegl2 = 1e-30;  // see the note at jacobi_rows
 

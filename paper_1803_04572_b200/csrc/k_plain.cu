@@ -525,6 +525,10 @@ __device__ __forceinline__ void stage_rows(double* dst, const double* __restrict
   for (int x = threadIdx.x & 31; x < n; x += 32) dst[x] = src[x];
 }
 
+// RB > 0 (R <= RB <= 32): lane r keeps column r of H̄ and of (G_W + rho I)^-1 in registers and the
+// row loops are unrolled (the kernel was issue-bound on the per-element shared-memory loads and the
+// second-half predicates: 218 instructions per row at R = 10); the FMA order is unchanged.
+template <int RB>
 __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* __restrict__ m,
                                                                  const int64_t* __restrict__ srow, int64_t K, int R,
                                                                  const double* __restrict__ Pp,
@@ -553,12 +557,27 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
   const bool has0 = lane < R, has1 = lane + 32 < R;
   const int64_t nw = (int64_t)gridDim.x * kPlainWarps;
   int my_steps = 0;
+  constexpr int RC = RB > 0 ? RB : 1;
+  double hc[RC], gc[RC];  // RB > 0: hc[i] = H̄(i, lane), gc[q] = Ginv(lane, q)
+  if (RB > 0) {
+#pragma unroll
+    for (int i = 0; i < RC; ++i) {
+      hc[i] = (has0 && i < R) ? Hs[i * R + lane] : 0.0;
+      gc[i] = (has0 && i < R) ? GT[i * R + lane] : 0.0;
+    }
+  }
   auto t_row = [&](const double* qrow, double& t0, double& t1) {  // T(a, r) = sum_i Q~(a, i) H̄(i, r)
     double s0 = 0.0, s1 = 0.0;
-    for (int i = 0; i < R; ++i) {
-      const double qa = qrow[i];
-      if (has0) s0 = fma(qa, Hs[i * R + lane], s0);
-      if (has1) s1 = fma(qa, Hs[i * R + lane + 32], s1);
+    if (RB > 0) {
+#pragma unroll
+      for (int i = 0; i < RC; ++i)
+        if (i < R) s0 = fma(qrow[i], hc[i], s0);
+    } else {
+      for (int i = 0; i < R; ++i) {
+        const double qa = qrow[i];
+        if (has0) s0 = fma(qa, Hs[i * R + lane], s0);
+        if (has1) s1 = fma(qa, Hs[i * R + lane + 32], s1);
+      }
     }
     t0 = s0;
     t1 = s1;
@@ -588,10 +607,16 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
       const double h0 = has0 ? f0 + rho * (w0 + d0) : 0.0;
       const double h1 = has1 ? f1 + rho * (w1 + d1) : 0.0;
       double z0 = 0.0, z1 = 0.0;
-      for (int qq = 0; qq < R; ++qq) {
-        const double hq = lane_pick(h0, h1, qq);
-        if (has0) z0 = fma(GT[qq * R + lane], hq, z0);
-        if (has1) z1 = fma(GT[qq * R + lane + 32], hq, z1);
+      if (RB > 0) {
+#pragma unroll
+        for (int qq = 0; qq < RC; ++qq)
+          if (qq < R) z0 = fma(gc[qq], __shfl_sync(kFull, h0, qq), z0);
+      } else {
+        for (int qq = 0; qq < R; ++qq) {
+          const double hq = lane_pick(h0, h1, qq);
+          if (has0) z0 = fma(GT[qq * R + lane], hq, z0);
+          if (has1) z1 = fma(GT[qq * R + lane + 32], hq, z1);
+        }
       }
       RowResid res;
       if (has0) {
@@ -640,13 +665,16 @@ __global__ void __launch_bounds__(32 * kPlainWarps) k_passB_warp(const int32_t* 
 int launch_passB_warp(Handle& h) {
   if (h.K == 0) return 0;
   const size_t smem = sizeof(double) * (2 * (size_t)h.R * h.R + kPlainWarps * passB_warp_per_warp(h.R));
-  max_smem_attr<k_passB_warp>(h);
+  const auto fn = h.R <= 16 ? k_passB_warp<16> : h.R <= 32 ? k_passB_warp<32> : k_passB_warp<0>;
+  if (h.R <= 16) max_smem_attr<k_passB_warp<16>>(h);
+  else if (h.R <= 32) max_smem_attr<k_passB_warp<32>>(h);
+  else max_smem_attr<k_passB_warp<0>>(h);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_passB_warp, 32 * kPlainWarps, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kPlainWarps, smem);
   int64_t blocks = (h.K + kPlainWarps - 1) / kPlainWarps;
   const int64_t cap = (int64_t)h.sms * std::max(per_sm, 1);
   if (blocks > cap) blocks = cap;
-  k_passB_warp<<<(unsigned)blocks, 32 * kPlainWarps, smem, h.stream>>>(
+  fn<<<(unsigned)blocks, 32 * kPlainWarps, smem, h.stream>>>(
       h.m, h.srow, h.K, h.R, h.Pp, h.Qt, h.H, h.GWi, h.scal, h.o.admm_inner, h.o.on_W.kind, h.o.on_W.param,
       h.o.admm_tol, h.W, h.DW, h.Nst, h.steps);
   return 1;
@@ -791,15 +819,30 @@ __global__ void __launch_bounds__(256) k_scatter_csc(const int64_t* __restrict__
   }
 }
 
-__global__ void k_sum_chunks(int64_t J, int R, const double* __restrict__ part,
-                             const int64_t* __restrict__ chunk_first /*[J+1] first chunk of column j*/,
-                             double* __restrict__ FV) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= J * R) return;
-  const int64_t j = x / R, r = x - j * R;
+// F_V(j, r) = sum of column j's chunk partials in a fixed order: 32 entries (j, r) per block, the
+// column's chunks c = first + g, first + g + 32, ... summed by thread g of the entry, then the 32
+// group sums in ascending g (columns of up to 32 chunks: plain ascending-chunk order). Under the
+// Zipf feature law one column holds hundreds of chunks; one thread walking them took 88 us on Small.
+__global__ void __launch_bounds__(1024) k_sum_chunks(int64_t J, int R, const double* __restrict__ part,
+                                                     const int64_t* __restrict__ chunk_first /*[J+1] first chunk of column j*/,
+                                                     double* __restrict__ FV) {
+  __shared__ double sm[32][33];
+  const int px = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t x = blockIdx.x * (int64_t)32 + px;
   double s = 0.0;
-  for (int64_t c = chunk_first[j]; c < chunk_first[j + 1]; ++c) s += part[c * R + r];
-  FV[x] = s;
+  if (x < J * R) {
+    const int64_t j = x / R, r = x - j * R;
+    const int64_t c1 = chunk_first[j + 1];
+    for (int64_t c = chunk_first[j] + g; c < c1; c += 32) s += part[c * R + r];
+  }
+  sm[g][px] = s;
+  __syncthreads();
+  if (g == 0 && x < J * R) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) t += sm[q][px];
+    FV[x] = t;
+  }
 }
 
 int launch_scatter_csc(Handle& h, const double* Nrows) {
@@ -812,7 +855,7 @@ int launch_scatter_csc(Handle& h, const double* Nrows) {
   k_scatter_csc<<<(unsigned)blocks, 256, 0, h.stream>>>(h.csc_chunk, h.csc_chunks, h.R, h.csc_row, h.csc_val, Nrows,
                                                         h.csc_part);
   const int64_t n = h.J * h.R;
-  k_sum_chunks<<<(unsigned)((n + 255) / 256), 256, 0, h.stream>>>(h.J, h.R, h.csc_part,
+  k_sum_chunks<<<(unsigned)((n + 31) / 32), 1024, 0, h.stream>>>(h.J, h.R, h.csc_part,
                                                                   h.csc_chunk_first, h.FV);
   return 2;
 }
